@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: Smart Laplacian node-updates/s on B200 (BASELINE.json metric).
+
+One STEP = one smooth() of `--passes` passes (default 100, move_tol 0 so every pass runs) over
+the whole mesh, coordinates resident in HBM.  Default workload: cfg3, the graded /
+irregular-valence 16M-node triangulation (the north star's ">= 60 % of HBM
+roofline on a 16M-node mesh" is quoted on it; its 1.5+ GB per-pass working set exceeds the
+126 MB L2, so no L2 flush is needed between steps), Form A, fp64, AoS, ping-pong, fused.
+
+JSON keys (one line, rank 0):
+  value        nv * passes * steps * n_gpus / max-over-ranks device time (CUDA events on the
+               engine's stream, barrier + synchronize on both sides)
+  e2e          the same metric through the C-ABI host-buffer entry point tsg_smooth_host:
+               pinned host coords -> H2D -> passes -> D2H every step, wall-clock timed
+  roofline     node-update kernel: algorithmic bytes per launch (SURVEY §8d B_pass, the
+               reference data model) / its mean CUDA-event duration, vs MEASURED_PEAKS hbm_gbs
+  cpu_baseline the reference (oracle/_ref, built from the reference's own sources) smooth()
+               with Backend::Parallel and all host cores on the same mesh, bounded sample
+  clocks       nvidia-smi samples taken during the timed region
+
+--impl reference runs the reference's CPU implementation instead (rank 0 only).
+Multi-GPU (torchrun): every rank smooths its own replica of the mesh (weak scaling); the
+partitioned halo-exchange path is DESIGN.md §6 "next".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(gen="grid", args=(100, 100, 0.3, 1), form="b", strategy="twophase", chunks=1, layout="aos",
+                 precision="f64", passes=100, move_tol=1e-6, reorder=False,
+                 label="perturbed grid 100x100 (10K nodes), reference defaults: Form B serial, TwoPhase, AoS"),
+    "cfg2": dict(gen="delaunay", args=(1_000_000, 42), form="a", strategy="fused", chunks=1, layout="aos",
+                 precision="f64", passes=100, move_tol=0.0, reorder=True,
+                 label="random Delaunay 1M nodes (seed 42), Form A, AoS"),
+    "cfg3": dict(gen="graded", args=(16_000_000, 1, 1e-3, 1024), form="a", strategy="fused", chunks=1,
+                 layout="aos", precision="f64", passes=100, move_tol=0.0, reorder=True,
+                 label="graded / irregular-valence Delaunay 16M nodes (0.1% hubs, valence 32..1024), Form A"),
+    "cfg4": dict(gen="grid", args=(8000, 8000, 0.3, 1), form="a", strategy="fused", chunks=1, layout="aos",
+                 precision="f64", passes=100, move_tol=0.0, reorder=False,
+                 label="perturbed grid 8000x8000 (64M nodes), Form A, fp64"),
+    "cfg5": dict(gen="delaunay", args=(256_000_000, 42), form="a", strategy="fused", chunks=1, layout="aos",
+                 precision="f32", passes=100, move_tol=0.0, reorder=True,
+                 label="random Delaunay 256M nodes, fp32"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_mesh(ts, cfg, nodes=None):
+    gen, args = cfg["gen"], list(cfg["args"])
+    if nodes:
+        if gen == "grid":
+            side = int(round(nodes ** 0.5))
+            args[0] = args[1] = side
+        else:
+            args[0] = nodes
+    t0 = time.time()
+    if gen == "grid":
+        xy, tri = ts.grid_arrays(*args)
+    elif gen == "delaunay":
+        xy, tri = ts.delaunay_arrays(*args)
+    else:
+        xy, tri = ts.graded_arrays(*args)
+    log(f"[bench] mesh {gen}{tuple(args)}: nv={len(xy)} nt={len(tri)} in {time.time() - t0:.1f}s")
+    return xy, tri, args
+
+
+def algorithmic_bytes_per_pass(nv, nt, sum_deg, precision):
+    """every array element counted once per pass, in the reference data model."""
+    c = 16 if precision == "f64" else 8
+    return 2 * c * nv + 4 * (nv + 1) + 4 * sum_deg + 4 * (nv + 1) + 12 * nt + 12 * nt + nv
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_rate(xy, tri, cfg, budget_s=20.0):
+    """The reference itself (oracle/_ref/libtsref.so: proj/src compiled out-of-tree) on host cores:
+    smooth() with Backend::Parallel and all hardware threads (Form A is bit-identical to serial;
+    Form B with W chunks is the semantics the W-chunk GPU run matches).  node-updates/s from the
+    reference's own iter_ms.  Falls back to the single-threaded oracle port if _ref is absent."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, Port, Ref
+
+    nv = len(xy)
+    if os.path.exists(REF_SO):
+        ref = Ref()
+        cores = ref.hardware_concurrency() or os.cpu_count() or 1
+        # probe one pass, then size the sample to the budget
+        backend = "parallel" if cores > 1 else "serial"
+        if cfg["form"] == "b" and cfg["chunks"] == 1:
+            backend, cores_used = "serial", 1
+        else:
+            cores_used = cores
+        probe = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend,
+                           workers=cores_used, max_iters=1, move_tol=0.0, layout=cfg["layout"])
+        per_pass = max(probe.stats["iter_ms"], 1e-3) / 1000.0
+        passes = int(max(1, min(cfg["passes"], budget_s / per_pass)))
+        r = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=cores_used,
+                       max_iters=passes, move_tol=0.0, layout=cfg["layout"])
+        rate = nv * r.iterations / (r.stats["iter_ms"] / 1000.0)
+        return dict(value=rate, unit="node-updates/s", cores=cores_used, kind="reference",
+                    sample=f"{r.iterations} passes of reference smooth() (form {cfg['form']}, {backend}, "
+                           f"W={cores_used}) on the same {nv}-node mesh; rate from its iter_ms "
+                           f"({r.stats['iter_ms']:.0f} ms); prep {r.stats['topo_ms'] + r.stats['init_ms'] + r.stats['constr_ms']:.0f} ms excluded")
+    port = Port()
+    t0 = time.time()
+    r = port.smooth(xy, tri, form=cfg["form"], chunks=cfg["chunks"], max_iters=1, move_tol=0.0)
+    dt = time.time() - t0
+    return dict(value=nv / dt, unit="node-updates/s", cores=1, kind="port",
+                sample=f"1 pass of the oracle restatement incl. its topology build on {nv} nodes")
+
+
+def run_reference_arm(args, cfg):
+    """--impl reference: the reference CPU implementation, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1502_00355_b200 as ts  # fixture generator only (reference cannot build >1M meshes)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, Ref
+
+    xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
+    nv = len(xy)
+    if not os.path.exists(REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtsref.so was not built"}))
+        return
+    ref = Ref()
+    cores = ref.hardware_concurrency() or 1
+    serial_b = cfg["form"] == "b" and cfg["chunks"] == 1
+    backend, workers = ("serial", 1) if serial_b or cores == 1 else ("parallel", cores)
+    probe = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=workers,
+                       max_iters=1, move_tol=0.0, layout=cfg["layout"])
+    per_pass = max(probe.stats["iter_ms"], 1e-3) / 1000.0
+    passes = int(max(1, min(cfg["passes"], args.ref_budget / per_pass)))
+    total_updates, total_ms = 0, 0.0
+    for i in range(args.warmup + args.steps):
+        r = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=workers,
+                       max_iters=passes, move_tol=cfg["move_tol"] if cfg["passes"] == passes else 0.0,
+                       layout=cfg["layout"])
+        if i >= args.warmup:
+            total_updates += nv * r.iterations
+            total_ms += r.stats["iter_ms"]
+    value = total_updates / (total_ms / 1000.0)
+    out = {
+        "impl": "reference", "metric": "node-updates/sec (Smart Laplacian)", "value": value,
+        "unit": "node-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": len(tri),
+                   "passes_per_step": passes, "form": cfg["form"], "layout": cfg["layout"],
+                   "generator_args": list(gargs)},
+        "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": workers, "kind": "reference",
+                         "sample": f"{passes} passes per step of the reference smooth() (prep excluded: "
+                                   f"rate from its iter_ms), {backend} backend, W={workers}"},
+        "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
+    ap.add_argument("--nodes", type=int, default=None, help="override the mesh size")
+    ap.add_argument("--passes", type=int, default=None)
+    ap.add_argument("--layout", choices=["aos", "soa"], default=None)
+    ap.add_argument("--precision", choices=["f64", "f32"], default=None)
+    ap.add_argument("--form", choices=["a", "b"], default=None)
+    ap.add_argument("--strategy", choices=["fused", "twophase"], default=None)
+    ap.add_argument("--swap", choices=["pingpong", "copy"], default="pingpong")
+    ap.add_argument("--chunks", type=int, default=None)
+    ap.add_argument("--no-reorder", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=2.0, help="reference arm: target seconds of passes per step")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no e2e / baseline")
+    args = ap.parse_args()
+
+    cfg = dict(CONFIGS[args.config])
+    for k in ("passes", "layout", "precision", "form", "strategy", "chunks"):
+        if getattr(args, k) is not None:
+            cfg[k] = getattr(args, k)
+    if args.no_reorder or cfg["form"] == "b":
+        cfg["reorder"] = False
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_1502_00355_b200 as ts
+    from paper_1502_00355_b200 import capi
+
+    xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
+    nv, nt = len(xy), len(tri)
+    t0 = time.time()
+    topo = ts.topology(nv, tri)
+    order = capi.hilbert_order(xy) if cfg["reorder"] else None
+    ctx = capi.Context(local_rank)
+    dm = capi.DeviceMesh(ctx, xy, tri, topo, layout=cfg["layout"], precision=cfg["precision"], order=order)
+    prep_s = time.time() - t0
+    deg = np.diff(topo["nbr_off"])
+    sum_deg = int(topo["nbr_off"][-1])
+    movable = topo["boundary"] == 0
+    log(f"[bench] prep {prep_s:.1f}s, device bytes {dm.device_bytes / 1e9:.2f} GB, max valence {deg.max()}, "
+        f"hubs(>16) {int(((deg > 16) & movable).sum())}")
+    diag = ts.bbox_diagonal(xy)
+    passes = cfg["passes"]
+    mk = lambda driver="graph": capi.make_cfg(form=cfg["form"], strategy=cfg["strategy"], chunks=cfg["chunks"],
+                                              swap=args.swap, max_iters=passes, driver=driver,
+                                              move_tol=cfg["move_tol"], bbox_diag=diag)
+    scfg = mk()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
+
+    if args.profile:
+        dm.smooth(mk("stream"))
+        torch.cuda.synchronize()
+        log("[bench] profile run done")
+        return
+
+    for _ in range(args.warmup):
+        r = dm.smooth(scfg)
+    launches_per_step = r["launches"]
+    iters_per_step = r["iterations"]
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    updates = 0
+    launches = 0
+    for _ in range(args.steps):
+        r = dm.smooth(scfg)
+        updates += nv * r["iterations"]
+        launches += r["launches"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = updates * world / (elapsed_ms / 1000.0)
+
+    # Roofline of the dominant kernel: node-update launches bracketed by events (stream driver).
+    rs = dm.smooth(mk("stream"))
+    node_ms_per_launch = rs["node_kernel_ms"] / max(1, rs["iterations"])
+    b_pass = algorithmic_bytes_per_pass(nv, nt, sum_deg, cfg["precision"])
+    peak, peak_src = measured_peak()
+    achieved = b_pass / (node_ms_per_launch / 1000.0) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pt = json.load(f)
+        key = f"{args.config}:{cfg['precision']}:{cfg['layout']}:{cfg['form']}:{nv}"
+        traffic = pt.get(key)
+    pass_ms = elapsed_ms / max(1, args.steps * iters_per_step)
+
+    # End to end through the C ABI with pinned host buffers, copies inside the timed region.
+    e2e = None
+    if rank == 0 or world > 1:
+        xin = torch.from_numpy(np.ascontiguousarray(xy)).pin_memory()
+        xout = torch.empty_like(xin).pin_memory()
+        xin_np, xout_np = xin.numpy(), xout.numpy()
+        dm.smooth_host(xin_np, scfg, xout_np)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_updates = 0
+        for _ in range(args.steps):
+            _, r2 = dm.smooth_host(xin_np, scfg, xout_np)
+            e2e_updates += nv * r2["iterations"]
+        e2e_s = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": e2e_updates * world / e2e_s, "unit": "node-updates/s",
+               "h2d_bytes_per_step": int(xin.numel() * 8), "d2h_bytes_per_step": int(xout.numel() * 8),
+               "ms_per_step": 1000 * e2e_s / args.steps,
+               "path": "tsg_smooth_host (C ABI): pinned host xy -> device -> passes -> host xy"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_rate(xy, tri, cfg)
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "error": str(exc)}
+
+    if rank == 0:
+        out = {
+            "metric": "node-updates/sec (Smart Laplacian)", "value": value, "unit": "node-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": nt,
+                       "passes_per_step": iters_per_step, "form": cfg["form"], "strategy": cfg["strategy"],
+                       "layout": cfg["layout"], "swap": args.swap, "chunks": cfg["chunks"],
+                       "locality_order": "hilbert" if cfg["reorder"] else "none",
+                       "generator_args": list(gargs), "max_valence": int(deg.max()),
+                       "l2": "per-pass working set exceeds L2 (126 MB); no flush" if b_pass > 126e6
+                       else "per-pass working set fits L2: passes re-read L2-resident data",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "driver": "conditional-WHILE CUDA graph, 1 launch per step"},
+            "ms_per_pass": pass_ms,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "node_update (thread per vertex) + hub_update",
+                         "bytes_per_launch": b_pass, "launch_ms": node_ms_per_launch,
+                         "bytes_model": "SURVEY 8(d) B_pass: 2c*nv + 8(nv+1) + 4*sum_deg + 24*nt + nv"},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "launches_per_step": launches_per_step,
+            "prep_s": prep_s,
+        }
+        print(json.dumps(out))
+    dm.free()
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

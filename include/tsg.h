@@ -1,0 +1,159 @@
+/*
+ * tsg.h — C ABI of the B200 Smart Laplacian engine (libtsg.so).
+ *
+ * This is the drop-in boundary between host code (the trismooth C++ API in
+ * include/trismooth/, the pybind11 module _trismooth, or any FFI: ctypes, cgo, JNI)
+ * and the sm_100a kernels.  Plain C: explicit int64 counts, caller-owned host
+ * buffers, library-owned device buffers behind opaque handles, integer status
+ * (TSG_OK = 0) plus a thread-local message (tsg_last_error).  No exceptions and no
+ * torch types cross this boundary.  One host thread drives a context at a time
+ * (the reference's single-orchestrator rule, proj/include/trismooth/parallel.hpp:26-28).
+ *
+ * Reference interfaces each entry point replaces (paths under /root/reference/proj):
+ *   tsg_mesh_upload        the in-memory Mesh + Adjacency after find_neighbors /
+ *                          determine_constraints (src/topology.cpp:69-95, src/mesh.cpp:20-53)
+ *   tsg_tri_alpha          compute_all_qualities        (src/quality.cpp:27-32)
+ *   tsg_vertex_minima      reduce_vertex_minima         (src/quality.cpp:60-65)
+ *   tsg_smooth             run_passes                   (src/smoothing.cpp:76-142), i.e.
+ *                          smooth_range / neighbor_mean / min_alpha_at per vertex
+ *                          (include/trismooth/smoothing.hpp:70-109, quality.hpp:54-64)
+ *   tsg_mesh_set_coords /  the coordinate fields of AosMesh / SoaMesh
+ *   tsg_mesh_get_coords    (include/trismooth/mesh.hpp:61-70, :203-212)
+ *   tsg_smooth_host        smooth() minus host topology prep (src/smoothing.cpp:146-182):
+ *                          host coords in -> passes -> host coords + stats out
+ */
+#ifndef TSG_H_
+#define TSG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_ABI_VERSION 1
+
+typedef int32_t tsg_status;
+enum {
+  TSG_OK = 0,
+  TSG_ERR_INVALID = 1, /* bad argument / unsupported combination */
+  TSG_ERR_CUDA = 2,    /* CUDA runtime or driver error (message has the detail) */
+  TSG_ERR_NOMEM = 3,   /* device or host allocation failed */
+  TSG_ERR_NODEVICE = 4 /* no CUDA device / extension cannot run here */
+};
+
+enum { TSG_LAYOUT_AOS = 0, TSG_LAYOUT_SOA = 1 };          /* mesh.hpp:24 Layout */
+enum { TSG_F64 = 0, TSG_F32 = 1 };                        /* coordinate + arithmetic type */
+enum { TSG_FORM_A = 0, TSG_FORM_B = 1 };                  /* smoothing.hpp:14 IterationForm */
+enum { TSG_STRATEGY_FUSED = 0, TSG_STRATEGY_TWOPHASE = 1 }; /* smoothing.hpp:20 UpdateStrategy */
+enum { TSG_SWAP_PINGPONG = 0, TSG_SWAP_COPY = 1 };        /* no-copy pointer swap / explicit copy */
+enum { TSG_STOP_MAX_ITERS = 0, TSG_STOP_DISPLACEMENT = 1, TSG_STOP_NO_MOVES = 2 };
+enum { TSG_DRIVER_GRAPH = 0, TSG_DRIVER_STREAM = 1 };     /* WHILE-graph loop / plain launches */
+
+typedef struct tsg_context tsg_context;
+typedef struct tsg_mesh tsg_mesh;
+
+/*
+ * Host description of a prepared mesh.  All arrays are in ORIGINAL vertex / triangle
+ * numbering and are read only during tsg_mesh_upload.
+ *   nbr_off/nbr   unique-neighbour CSR, each row ascending (Adjacency::unique)
+ *   inc_off/inc   incident-triangle CSR, each row ascending (Adjacency::incident)
+ *   boundary      1 = pinned (determine_constraints)
+ *   order         optional locality order: order[s] = original id stored at device
+ *                 slot s (a permutation of 0..nv-1); NULL = identity.  Results are
+ *                 unaffected: neighbour sums keep ascending ORIGINAL-id order and
+ *                 Form B chunks / lower-id tests use original ids.
+ */
+typedef struct {
+  int64_t nv;
+  int64_t nt;
+  const double* xy;      /* 2*nv interleaved x,y */
+  const int32_t* tri;    /* 3*nt */
+  const int64_t* nbr_off;
+  const int32_t* nbr;
+  const int64_t* inc_off;
+  const int32_t* inc;
+  const uint8_t* boundary;
+  const int64_t* order;
+  int32_t layout;    /* TSG_LAYOUT_* : device coordinate layout */
+  int32_t precision; /* TSG_F64 | TSG_F32 */
+} tsg_mesh_desc;
+
+typedef struct {
+  int32_t form;      /* TSG_FORM_* */
+  int32_t strategy;  /* TSG_STRATEGY_* (identical results; schedule differs) */
+  int32_t chunks;    /* Form B chunk count W (Backend::Parallel workers); 1 = serial */
+  int32_t swap;      /* TSG_SWAP_* */
+  int32_t max_iters; /* >= 1 */
+  int32_t driver;    /* TSG_DRIVER_* */
+  double move_tol;   /* >= 0; 0 disables the displacement stop */
+  double bbox_diag;  /* std::hypot of the bbox extents, computed by the caller */
+} tsg_smooth_cfg;
+
+typedef struct {
+  int32_t iterations;
+  int32_t stop;          /* TSG_STOP_* */
+  int64_t node_updates;  /* nv * iterations (pinned vertices counted, as the reference) */
+  double device_ms;      /* CUDA-event time of the pass loop */
+  double node_kernel_ms; /* CUDA-event time summed over node-update launches (stream driver) */
+  int64_t launches;      /* kernels launched by this call */
+} tsg_smooth_stats;
+
+/* ---- context ---- */
+int32_t tsg_abi_version(void);
+const char* tsg_last_error(void);
+int32_t tsg_device_count(void);
+tsg_status tsg_context_create(int32_t device, tsg_context** out);
+tsg_status tsg_context_destroy(tsg_context* ctx);
+/* Returns the cudaStream_t the context launches on (for callers that sync / time). */
+void* tsg_context_stream(tsg_context* ctx);
+
+/* ---- mesh ---- */
+tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* desc, tsg_mesh** out);
+tsg_status tsg_mesh_free(tsg_mesh* mesh);
+/* bytes of device memory held by the mesh */
+int64_t tsg_mesh_device_bytes(const tsg_mesh* mesh);
+/* Coordinates in ORIGINAL numbering (2*nv doubles; f32 meshes round on upload). */
+tsg_status tsg_mesh_set_coords(tsg_mesh* mesh, const double* xy);
+tsg_status tsg_mesh_get_coords(tsg_mesh* mesh, double* xy_out);
+
+/* ---- quality (device) ---- */
+/* alpha_out: nt doubles in original triangle order (compute_all_qualities). */
+tsg_status tsg_tri_alpha(tsg_mesh* mesh, double* alpha_out);
+/* vmin_out: nv doubles, NaN for vertices without incident triangles (reduce_vertex_minima). */
+tsg_status tsg_vertex_minima(tsg_mesh* mesh, double* vmin_out);
+/* {min alpha, max alpha, count alpha <= 0}; exact (order-free) reductions. */
+tsg_status tsg_alpha_extrema(tsg_mesh* mesh, double* min_out, double* max_out, int64_t* nonpos_out);
+
+/* ---- the hot path ---- */
+/*
+ * Runs passes until max_iters, accepted == 0 (NoMoves) or max_disp < move_tol*bbox_diag
+ * (Displacement), in the reference's order (src/smoothing.cpp:132-141).  Coordinates stay
+ * on the device.  accepted_per_pass / max_disp_per_pass receive min(capacity, iterations)
+ * entries (either may be NULL).
+ */
+tsg_status tsg_smooth(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, tsg_smooth_stats* stats,
+                      int32_t* accepted_per_pass, double* max_disp_per_pass, int32_t capacity);
+
+/* Host-buffer variant: H2D of xy_in, tsg_smooth, D2H into xy_out (both original order). */
+tsg_status tsg_smooth_host(tsg_mesh* mesh, const double* xy_in, const tsg_smooth_cfg* cfg,
+                           double* xy_out, tsg_smooth_stats* stats, int32_t* accepted_per_pass,
+                           double* max_disp_per_pass, int32_t capacity);
+
+/*
+ * One pass in lockstep from the current device state, without the stop rule; writes the
+ * per-vertex decision (1 accept, 0 reject, -1 pinned; original order) and advances the
+ * coordinates.  Used for the fp32 lockstep parity contract.
+ */
+tsg_status tsg_pass_lockstep(tsg_mesh* mesh, int32_t form, int32_t chunks, int8_t* decision_out,
+                             int32_t* accepted_out, double* max_disp_out);
+
+/* ---- locality ordering (host prep helper) ---- */
+/* order_out[s] = original id for slot s: vertices sorted along a Hilbert curve over the
+ * bounding box (ties by original id).  Pure host code, deterministic. */
+tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSG_H_ */

@@ -1,0 +1,225 @@
+"""ctypes binding of the C ABI in include/tsg.h (libtsg.so).
+
+This is the binding a reference-side maintainer would add for the FFI route (see
+INTEGRATION.md); the tests use it to exercise the C ABI directly and bench.py uses it for the
+end-to-end (host buffers in, host buffers out) measurement.  It raises if libtsg.so is missing
+or a call fails — no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtsg.so")
+
+TSG_OK, TSG_ERR_INVALID, TSG_ERR_CUDA, TSG_ERR_NOMEM, TSG_ERR_NODEVICE = 0, 1, 2, 3, 4
+LAYOUT = {"aos": 0, "soa": 1}
+PRECISION = {"f64": 0, "f32": 1}
+FORM = {"a": 0, "b": 1}
+STRATEGY = {"fused": 0, "twophase": 1}
+SWAP = {"pingpong": 0, "copy": 1}
+DRIVER = {"graph": 0, "stream": 1}
+STOP = ("max_iters", "displacement", "no_moves")
+
+# Every symbol include/tsg.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = (
+    "tsg_abi_version", "tsg_last_error", "tsg_device_count", "tsg_context_create",
+    "tsg_context_destroy", "tsg_context_stream", "tsg_mesh_upload", "tsg_mesh_free",
+    "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_tri_alpha",
+    "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
+    "tsg_pass_lockstep", "tsg_hilbert_order",
+)
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("nv", C.c_int64), ("nt", C.c_int64), ("xy", C.c_void_p), ("tri", C.c_void_p),
+                ("nbr_off", C.c_void_p), ("nbr", C.c_void_p), ("inc_off", C.c_void_p),
+                ("inc", C.c_void_p), ("boundary", C.c_void_p), ("order", C.c_void_p),
+                ("layout", C.c_int32), ("precision", C.c_int32)]
+
+
+class SmoothCfg(C.Structure):
+    _fields_ = [("form", C.c_int32), ("strategy", C.c_int32), ("chunks", C.c_int32),
+                ("swap", C.c_int32), ("max_iters", C.c_int32), ("driver", C.c_int32),
+                ("move_tol", C.c_double), ("bbox_diag", C.c_double)]
+
+
+class SmoothStats(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("stop", C.c_int32), ("node_updates", C.c_int64),
+                ("device_ms", C.c_double), ("node_kernel_ms", C.c_double), ("launches", C.c_int64)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing — build with `make` (nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        P, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        sig = {
+            "tsg_abi_version": (i32, []),
+            "tsg_last_error": (C.c_char_p, []),
+            "tsg_device_count": (i32, []),
+            "tsg_context_create": (i32, [i32, C.POINTER(P)]),
+            "tsg_context_destroy": (i32, [P]),
+            "tsg_context_stream": (P, [P]),
+            "tsg_mesh_upload": (i32, [P, C.POINTER(MeshDesc), C.POINTER(P)]),
+            "tsg_mesh_free": (i32, [P]),
+            "tsg_mesh_device_bytes": (i64, [P]),
+            "tsg_mesh_set_coords": (i32, [P, P]),
+            "tsg_mesh_get_coords": (i32, [P, P]),
+            "tsg_tri_alpha": (i32, [P, P]),
+            "tsg_vertex_minima": (i32, [P, P]),
+            "tsg_alpha_extrema": (i32, [P, P, P, P]),
+            "tsg_smooth": (i32, [P, C.POINTER(SmoothCfg), C.POINTER(SmoothStats), P, P, i32]),
+            "tsg_smooth_host": (i32, [P, P, C.POINTER(SmoothCfg), P, C.POINTER(SmoothStats), P, P, i32]),
+            "tsg_pass_lockstep": (i32, [P, i32, i32, P, P, P]),
+            "tsg_hilbert_order": (i32, [i64, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def check(status: int, what: str):
+    if status != TSG_OK:
+        raise RuntimeError(f"{what}: {lib().tsg_last_error().decode()} (status {status})")
+
+
+def hilbert_order(xy: np.ndarray) -> np.ndarray:
+    xy = np.ascontiguousarray(xy, dtype=np.float64)
+    out = np.empty(len(xy), dtype=np.int64)
+    check(lib().tsg_hilbert_order(len(xy), _ptr(xy), _ptr(out)), "tsg_hilbert_order")
+    return out
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        check(lib().tsg_context_create(device, C.byref(self.h)), "tsg_context_create")
+
+    @property
+    def stream(self) -> int:
+        return lib().tsg_context_stream(self.h) or 0
+
+    def close(self):
+        if self.h:
+            lib().tsg_context_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_cfg(form="a", strategy="fused", chunks=1, swap="pingpong", max_iters=100, driver="graph",
+             move_tol=0.0, bbox_diag=0.0) -> SmoothCfg:
+    return SmoothCfg(FORM[form], STRATEGY[strategy], chunks, SWAP[swap], max_iters, DRIVER[driver],
+                     move_tol, bbox_diag)
+
+
+class DeviceMesh:
+    """A tsg_mesh: upload from host arrays (original numbering)."""
+
+    def __init__(self, ctx: Context, xy, tri, topo: dict, layout="aos", precision="f64", order=None):
+        self.ctx = ctx
+        self.xy = np.ascontiguousarray(xy, dtype=np.float64)
+        self.tri = np.ascontiguousarray(tri, dtype=np.int32)
+        self.nv, self.nt = len(self.xy), len(self.tri)
+        keep = dict(nbr_off=np.ascontiguousarray(topo["nbr_off"], dtype=np.int64),
+                    nbr=np.ascontiguousarray(topo["nbr"], dtype=np.int32),
+                    inc_off=np.ascontiguousarray(topo["inc_off"], dtype=np.int64),
+                    inc=np.ascontiguousarray(topo["inc"], dtype=np.int32),
+                    boundary=np.ascontiguousarray(topo["boundary"], dtype=np.uint8))
+        order = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+        d = MeshDesc(self.nv, self.nt, _ptr(self.xy), _ptr(self.tri), _ptr(keep["nbr_off"]),
+                     _ptr(keep["nbr"]), _ptr(keep["inc_off"]), _ptr(keep["inc"]),
+                     _ptr(keep["boundary"]), _ptr(order), LAYOUT[layout], PRECISION[precision])
+        self.h = C.c_void_p()
+        check(lib().tsg_mesh_upload(ctx.h, C.byref(d), C.byref(self.h)), "tsg_mesh_upload")
+
+    def free(self):
+        if self.h:
+            lib().tsg_mesh_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(lib().tsg_mesh_device_bytes(self.h))
+
+    def set_coords(self, xy):
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        check(lib().tsg_mesh_set_coords(self.h, _ptr(xy)), "tsg_mesh_set_coords")
+
+    def get_coords(self) -> np.ndarray:
+        out = np.empty((self.nv, 2))
+        check(lib().tsg_mesh_get_coords(self.h, _ptr(out)), "tsg_mesh_get_coords")
+        return out
+
+    def tri_alpha(self) -> np.ndarray:
+        out = np.empty(self.nt)
+        check(lib().tsg_tri_alpha(self.h, _ptr(out)), "tsg_tri_alpha")
+        return out
+
+    def vertex_minima(self) -> np.ndarray:
+        out = np.empty(self.nv)
+        check(lib().tsg_vertex_minima(self.h, _ptr(out)), "tsg_vertex_minima")
+        return out
+
+    def alpha_extrema(self):
+        lo, hi, n = C.c_double(), C.c_double(), C.c_int64()
+        check(lib().tsg_alpha_extrema(self.h, C.byref(lo), C.byref(hi), C.byref(n)), "tsg_alpha_extrema")
+        return lo.value, hi.value, n.value
+
+    def smooth(self, cfg: SmoothCfg):
+        st = SmoothStats()
+        acc = np.zeros(cfg.max_iters, dtype=np.int32)
+        md = np.zeros(cfg.max_iters)
+        check(lib().tsg_smooth(self.h, C.byref(cfg), C.byref(st), _ptr(acc), _ptr(md), cfg.max_iters),
+              "tsg_smooth")
+        it = st.iterations
+        return dict(iterations=it, stop=STOP[st.stop], accepted=acc[:it], max_disp=md[:it],
+                    device_ms=st.device_ms, node_kernel_ms=st.node_kernel_ms, launches=st.launches,
+                    node_updates=st.node_updates)
+
+    def smooth_host(self, xy_in, cfg: SmoothCfg, xy_out=None):
+        xy_in = np.ascontiguousarray(xy_in, dtype=np.float64)
+        if xy_out is None:
+            xy_out = np.empty_like(xy_in)
+        st = SmoothStats()
+        acc = np.zeros(cfg.max_iters, dtype=np.int32)
+        md = np.zeros(cfg.max_iters)
+        check(lib().tsg_smooth_host(self.h, _ptr(xy_in), C.byref(cfg), _ptr(xy_out), C.byref(st),
+                                    _ptr(acc), _ptr(md), cfg.max_iters), "tsg_smooth_host")
+        it = st.iterations
+        return xy_out, dict(iterations=it, stop=STOP[st.stop], accepted=acc[:it], max_disp=md[:it],
+                            device_ms=st.device_ms, launches=st.launches)
+
+    def pass_lockstep(self, form="a", chunks=1):
+        dec = np.empty(self.nv, dtype=np.int8)
+        acc = C.c_int32()
+        md = C.c_double()
+        check(lib().tsg_pass_lockstep(self.h, FORM[form], chunks, _ptr(dec), C.byref(acc), C.byref(md)),
+              "tsg_pass_lockstep")
+        return dec, acc.value, md.value

@@ -1,0 +1,148 @@
+// Device-side building blocks of the Smart Laplacian node update (sm_100a).
+//
+// Bit-exactness contract (fp64): every floating-point operation below is an explicit
+// round-to-nearest intrinsic (__dadd_rn / __dsub_rn / __dmul_rn / __ddiv_rn / __dsqrt_rn),
+// which nvcc never contracts into FMA, in the operand order of the reference
+// (proj/include/trismooth/quality.hpp:15-23, smoothing.hpp:70-81, :103-105).  The
+// reference binary contains no FMA (x86-64 baseline), so this reproduces its
+// results bit for bit.  The fp32 instantiation uses the same formulas in float.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tsg {
+
+template <typename R>
+struct Arith;
+
+template <>
+struct Arith<double> {
+  using R2 = double2;
+  static constexpr double kAlpha = 3.4641016151377544;  // 2 * 1.7320508075688772935, exact
+  __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static double sub(double a, double b) { return __dsub_rn(a, b); }
+  __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ __forceinline__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+  __device__ __forceinline__ static double sqrt(double a) { return __dsqrt_rn(a); }
+  __device__ __forceinline__ static double2 make(double x, double y) { return make_double2(x, y); }
+};
+
+template <>
+struct Arith<float> {
+  using R2 = float2;
+  static constexpr float kAlpha = 3.4641016151377544f;
+  __device__ __forceinline__ static float add(float a, float b) { return __fadd_rn(a, b); }
+  __device__ __forceinline__ static float sub(float a, float b) { return __fsub_rn(a, b); }
+  __device__ __forceinline__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+  __device__ __forceinline__ static float div(float a, float b) { return __fdiv_rn(a, b); }
+  __device__ __forceinline__ static float sqrt(float a) { return __fsqrt_rn(a); }
+  __device__ __forceinline__ static float2 make(float x, float y) { return make_float2(x, y); }
+};
+
+// Coordinates of one buffer.  AoS: interleaved (x, y) pairs, one 8/16-byte vector load per
+// vertex.  SoA: x[] then y[] in one allocation (y at base + nv).
+template <typename R, bool kSoA>
+struct Coords {
+  using R2 = typename Arith<R>::R2;
+  R* base;
+  int64_t nv;
+  __device__ __forceinline__ R2 load(int64_t i) const {
+    if constexpr (kSoA) {
+      return Arith<R>::make(__ldg(base + i), __ldg(base + nv + i));
+    } else {
+      return __ldg(reinterpret_cast<const R2*>(base) + i);
+    }
+  }
+  // Read of a buffer that other CTAs of the same launch may be writing (Form B fresh reads
+  // happen only across launches, so plain loads are enough; no __ldg on mutable data).
+  __device__ __forceinline__ R2 load_mut(int64_t i) const {
+    if constexpr (kSoA) {
+      return Arith<R>::make(base[i], base[nv + i]);
+    } else {
+      return reinterpret_cast<const R2*>(base)[i];
+    }
+  }
+  __device__ __forceinline__ void store(int64_t i, R2 v) const {
+    if constexpr (kSoA) {
+      base[i] = v.x;
+      base[nv + i] = v.y;
+    } else {
+      reinterpret_cast<R2*>(base)[i] = v;
+    }
+  }
+};
+
+// α of the triangle that has vertex v at position k (0..2) and the other two vertices
+// a = t[(k+1)%3], b = t[(k+2)%3].  dab = b - a and its squares are shared between the
+// pass-start and hypothetical evaluations.  Differences are re-signed exactly
+// (RN(x - y) = -RN(y - x)), so the (ax, ay, bx, by, cx, cy) of triangle_alpha is a signed
+// permutation of (a - v, b - v, b - a):
+//   k = 0: (p1,p2,p3) = (v,a,b): A =  a-v, B =  b-v, C =  b-a
+//   k = 1: (p1,p2,p3) = (b,v,a): A = -(b-v), B = -(b-a), C = a-v
+//   k = 2: (p1,p2,p3) = (a,b,v): A =  b-a, B = -(a-v), C = -(b-v)
+// and the edge-square sum keeps the reference's left-to-right order A, B, C.
+template <typename R>
+__device__ __forceinline__ R alpha_at(int k, R vx, R vy, R ax, R ay, R bx, R by, R dabx, R daby,
+                                      R sabx, R saby) {
+  using O = Arith<R>;
+  const R dax = O::sub(ax, vx), day = O::sub(ay, vy);
+  const R dbx = O::sub(bx, vx), dby = O::sub(by, vy);
+  const R sax = O::mul(dax, dax), say = O::mul(day, day);
+  const R sbx = O::mul(dbx, dbx), sby = O::mul(dby, dby);
+  R ta, es;
+  if (k == 0) {
+    ta = O::sub(O::mul(dax, dby), O::mul(day, dbx));
+    es = O::add(O::add(O::add(O::add(O::add(sax, say), sbx), sby), sabx), saby);
+  } else if (k == 1) {
+    ta = O::sub(O::mul(dbx, daby), O::mul(dby, dabx));
+    es = O::add(O::add(O::add(O::add(O::add(sbx, sby), sabx), saby), sax), say);
+  } else {
+    ta = O::sub(O::mul(daby, dax), O::mul(dabx, day));
+    es = O::add(O::add(O::add(O::add(O::add(sabx, saby), sax), say), sbx), sby);
+  }
+  if (es == R(0)) return R(0);
+  return O::div(O::mul(Arith<R>::kAlpha, ta), es);
+}
+
+// triangle_alpha(p1, p2, p3) literally (quality.hpp:15-23).
+template <typename R>
+__device__ __forceinline__ R alpha_plain(R x1, R y1, R x2, R y2, R x3, R y3) {
+  using O = Arith<R>;
+  const R ax = O::sub(x2, x1), ay = O::sub(y2, y1);
+  const R bx = O::sub(x3, x1), by = O::sub(y3, y1);
+  const R cx = O::sub(x3, x2), cy = O::sub(y3, y2);
+  const R ta = O::sub(O::mul(ax, by), O::mul(ay, bx));
+  const R es = O::add(O::add(O::add(O::add(O::add(O::mul(ax, ax), O::mul(ay, ay)), O::mul(bx, bx)),
+                                    O::mul(by, by)),
+                             O::mul(cx, cx)),
+                      O::mul(cy, cy));
+  if (es == R(0)) return R(0);
+  return O::div(O::mul(Arith<R>::kAlpha, ta), es);
+}
+
+// std::min(best, x) (== x < best ? x : best), NaN-compatible with the reference.
+template <typename R>
+__device__ __forceinline__ R min_ref(R best, R x) {
+  return x < best ? x : best;
+}
+
+// Fan record: neighbour-list positions of a and b, and v's position k in the triangle.
+__host__ __device__ __forceinline__ uint32_t fan_pack(uint32_t i1, uint32_t i2, uint32_t k) {
+  return i1 | (i2 << 15) | (k << 30);
+}
+__device__ __forceinline__ uint32_t fan_i1(uint32_t f) { return f & 0x7fffu; }
+__device__ __forceinline__ uint32_t fan_i2(uint32_t f) { return (f >> 15) & 0x7fffu; }
+__device__ __forceinline__ int fan_k(uint32_t f) { return static_cast<int>(f >> 30); }
+
+constexpr uint32_t kFreshBit = 0x80000000u;  // Form B: read this neighbour from N (live)
+
+// Pass-loop state shared by the node kernels and the finalize kernel.
+struct PassState {
+  int32_t pass;  // index of the pass being executed
+  int32_t done;  // 1 once a stop rule fired
+  int32_t stop;  // TSG_STOP_*
+  int32_t pad;
+};
+
+}  // namespace tsg

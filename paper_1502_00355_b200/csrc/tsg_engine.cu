@@ -1,0 +1,797 @@
+// libtsg.so — the C ABI (include/tsg.h) over the sm_100a Smart Laplacian kernels.
+//
+// Device residency: one tsg_mesh holds the slot-ordered topology (compact CSR + fan records,
+// incident CSR, device triangles), two coordinate buffers and the per-pass stats.  The pass
+// loop runs as a CUDA graph whose body is one pass and whose WHILE condition is set on the
+// device by the finalize kernel, so a whole smooth() is one graph launch and no host
+// round-trip happens between passes (reference loop: proj/src/smoothing.cpp:98-141).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "tsg.h"
+#include "tsg_kernels.cuh"
+#include "tsg_prep.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+tsg_status fail(tsg_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define TSG_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? TSG_ERR_NOMEM : TSG_ERR_CUDA,       \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+  } while (0)
+
+constexpr int kMaxSmallDeg = 16;  // thread-per-vertex path; above: CTA-per-vertex hub path
+constexpr int kHubCap = 4096;     // hub entries staged in shared memory
+
+template <class T>
+tsg_status dalloc(T** p, size_t count, int64_t* bytes) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) return fail(TSG_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  *bytes += static_cast<int64_t>(count * sizeof(T));
+  return TSG_OK;
+}
+
+template <class T>
+tsg_status upload(T** p, const std::vector<T>& v, int64_t* bytes, cudaStream_t s) {
+  tsg_status st = dalloc(p, v.size(), bytes);
+  if (st) return st;
+  if (!v.empty()) {
+    cudaError_t e = cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return fail(TSG_ERR_CUDA, std::string("cudaMemcpyAsync: ") + cudaGetErrorString(e));
+  }
+  return TSG_OK;
+}
+
+// Gather original-order f64 pairs into slot order (both buffers) and back.
+template <typename R, bool kSoA>
+__global__ void coords_from_orig(const double* __restrict__ xy, const int64_t* __restrict__ order,
+                                 int64_t nv, tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = order ? order[s] : s;
+    const auto p = tsg::Arith<R>::make(static_cast<R>(xy[2 * v]), static_cast<R>(xy[2 * v + 1]));
+    b0.store(s, p);
+    b1.store(s, p);
+  }
+}
+
+template <typename R, bool kSoA>
+__global__ void coords_to_orig(tsg::Coords<R, kSoA> b, const int64_t* __restrict__ order,
+                               int64_t nv, double* __restrict__ xy) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = order ? order[s] : s;
+    const auto p = b.load_mut(s);
+    xy[2 * v] = static_cast<double>(p.x);
+    xy[2 * v + 1] = static_cast<double>(p.y);
+  }
+}
+
+template <typename R>
+__global__ void to_double_scatter(const R* __restrict__ in, const int64_t* __restrict__ order,
+                                  int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[order ? order[i] : i] = static_cast<double>(in[i]);
+}
+
+__global__ void scatter_i8(const int8_t* __restrict__ in, const int64_t* __restrict__ order,
+                           int64_t n, int8_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[order ? order[i] : i] = in[i];
+}
+
+unsigned grid_for(int64_t n, int block) {
+  const int64_t g = (n + block - 1) / block;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64)));
+}
+
+struct GraphCache {
+  bool valid = false;
+  int32_t form = -1, strategy = -1, chunks = -1, swap = -1, max_iters = -1;
+  double tol_abs = 0.0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels_per_pass = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    valid = false;
+  }
+};
+
+}  // namespace
+
+struct tsg_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> pass_events;  // stream-timed driver
+};
+
+struct tsg_mesh {
+  tsg_context* ctx = nullptr;
+  tsg::HostMesh hm;
+  int32_t layout = 0, prec = 0;
+  size_t rsize = 8;
+  int64_t bytes = 0;
+  void* buf[2] = {nullptr, nullptr};
+  uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
+           *d_vinc = nullptr;
+  int32_t *d_tri = nullptr, *d_hubs = nullptr;
+  int64_t *d_order = nullptr, *d_tri_order = nullptr;
+  void* d_alpha = nullptr;
+  double* d_xy_stage = nullptr;  // 2*nv original-order doubles
+  double* d_vmin = nullptr;
+  int8_t *d_decision = nullptr, *d_decision_orig = nullptr;
+  tsg::PassState* d_state = nullptr;
+  int32_t* d_acc = nullptr;
+  unsigned long long* d_md = nullptr;
+  unsigned long long* d_ext = nullptr;  // extrema scratch (3)
+  int32_t cap = 0;
+  int cur = 0;
+  int32_t hub_max_deg = 0;
+  // Form B schedule cache
+  int32_t fb_chunks = 0;
+  uint32_t* d_nbr_fresh = nullptr;
+  int32_t *d_fb_nodes = nullptr, *d_fb_hubs = nullptr;
+  std::vector<tsg::Phase> fb_levels;
+  int64_t fb_bytes = 0;
+  GraphCache gc;
+};
+
+namespace {
+
+void free_form_b(tsg_mesh* m) {
+  cudaFree(m->d_nbr_fresh);
+  cudaFree(m->d_fb_nodes);
+  cudaFree(m->d_fb_hubs);
+  m->d_nbr_fresh = nullptr;
+  m->d_fb_nodes = m->d_fb_hubs = nullptr;
+  m->bytes -= m->fb_bytes;
+  m->fb_bytes = 0;
+  m->fb_chunks = 0;
+  m->fb_levels.clear();
+}
+
+tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
+  if (m->fb_chunks == chunks) return TSG_OK;
+  free_form_b(m);
+  m->gc.reset();
+  tsg::FormBSchedule sch;
+  const std::string err = tsg::build_form_b(m->hm, chunks, kMaxSmallDeg, sch);
+  if (!err.empty()) return fail(TSG_ERR_INVALID, err);
+  int64_t b = 0;
+  cudaStream_t s = m->ctx->stream;
+  tsg_status st;
+  if ((st = upload(&m->d_nbr_fresh, sch.nbr_fresh, &b, s))) return st;
+  if ((st = upload(&m->d_fb_nodes, sch.nodes, &b, s))) return st;
+  if ((st = upload(&m->d_fb_hubs, sch.hubs, &b, s))) return st;
+  TSG_CUDA(cudaStreamSynchronize(s));
+  m->fb_levels = std::move(sch.levels);
+  m->fb_bytes = b;
+  m->bytes += b;
+  m->fb_chunks = chunks;
+  return TSG_OK;
+}
+
+template <typename R, bool kSoA>
+tsg::Coords<R, kSoA> coords_of(const tsg_mesh* m, int i) {
+  return tsg::Coords<R, kSoA>{static_cast<R*>(m->buf[i]), m->hm.nv};
+}
+
+// Everything templated on the coordinate type and layout.
+template <typename R, bool kSoA>
+struct Engine {
+  using Args = tsg::PassArgs<R, kSoA>;
+  using R2 = typename tsg::Arith<R>::R2;
+
+  static Args base_args(tsg_mesh* m, const tsg_smooth_cfg& c) {
+    Args a{};
+    a.buf0 = coords_of<R, kSoA>(m, 0);
+    a.buf1 = coords_of<R, kSoA>(m, 1);
+    a.swap = c.swap;
+    a.off = m->d_off;
+    a.nbr = c.form == TSG_FORM_B ? m->d_nbr_fresh : m->d_nbr;
+    a.fan = m->d_fan;
+    a.vinc_off = m->d_vinc_off;
+    a.vinc = m->d_vinc;
+    a.alpha = static_cast<const R*>(m->d_alpha);
+    a.st = m->d_state;
+    a.pass_acc = m->d_acc;
+    a.pass_md = m->d_md;
+    a.decision = nullptr;
+    return a;
+  }
+
+  template <bool kFormB, bool kTwoPhase>
+  static tsg_status launch_phase(tsg_mesh* m, const Args& base, const int32_t* small, int64_t ns,
+                                 const int32_t* hubs, int64_t nh, int32_t hub_cap, cudaStream_t s,
+                                 int64_t* kernels) {
+    if (ns > 0) {
+      Args a = base;
+      a.list = small;
+      a.count = ns;
+      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg>
+          <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    if (nh > 0) {
+      Args a = base;
+      a.list = hubs;
+      a.count = nh;
+      const size_t smem = static_cast<size_t>(hub_cap) * sizeof(R2) * (kFormB ? 2 : 1);
+      auto kfn = tsg::hub_update<R, kSoA, kFormB, kTwoPhase>;
+      kfn<<<static_cast<unsigned>(nh), tsg::kHubBlock, smem, s>>>(a, hub_cap);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    return TSG_OK;
+  }
+
+  template <bool kFormB, bool kTwoPhase>
+  static tsg_status enqueue_pass_t(tsg_mesh* m, const tsg_smooth_cfg& c, cudaStream_t s,
+                                   double tol_abs, cudaGraphConditionalHandle h, int use_handle,
+                                   int8_t* decision, cudaEvent_t ev_begin, cudaEvent_t ev_end,
+                                   int64_t* kernels) {
+    const int64_t nv = m->hm.nv;
+    if (c.swap == TSG_SWAP_COPY)
+      TSG_CUDA(cudaMemcpyAsync(m->buf[1], m->buf[0], 2 * nv * sizeof(R), cudaMemcpyDeviceToDevice, s));
+    if (kTwoPhase) {
+      tsg::tri_alpha<R, kSoA><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
+          coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1), c.swap, m->d_state, m->d_tri,
+          m->hm.nt, static_cast<R*>(m->d_alpha));
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    Args base = base_args(m, c);
+    base.decision = decision;
+    const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
+    if (ev_begin) TSG_CUDA(cudaEventRecord(ev_begin, s));
+    if (!kFormB) {
+      tsg_status st = launch_phase<false, kTwoPhase>(m, base, nullptr, nv, m->d_hubs,
+                                                     static_cast<int64_t>(m->hm.hubs.size()),
+                                                     hub_cap, s, kernels);
+      if (st) return st;
+    } else {
+      for (const tsg::Phase& L : m->fb_levels) {
+        tsg_status st = launch_phase<true, kTwoPhase>(m, base, m->d_fb_nodes + L.small_begin,
+                                                      L.small_count, m->d_fb_hubs + L.hub_begin,
+                                                      L.hub_count, hub_cap, s, kernels);
+        if (st) return st;
+      }
+    }
+    if (ev_end) TSG_CUDA(cudaEventRecord(ev_end, s));
+    tsg::finalize_pass<<<1, 1, 0, s>>>(m->d_state, m->d_acc, m->d_md, tol_abs, c.max_iters, h, use_handle);
+    TSG_CUDA(cudaGetLastError());
+    ++*kernels;
+    return TSG_OK;
+  }
+
+  // Opt-in shared memory for the hub kernels (done outside any stream capture).
+  static tsg_status prepare(tsg_mesh* m) {
+    const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
+    const int smem1 = static_cast<int>(hub_cap * sizeof(R2)), smem2 = 2 * smem1;
+    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
+    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    return TSG_OK;
+  }
+
+  static tsg_status enqueue_pass(tsg_mesh* m, const tsg_smooth_cfg& c, cudaStream_t s, double tol_abs,
+                                 cudaGraphConditionalHandle h, int use_handle, int8_t* decision,
+                                 cudaEvent_t e0, cudaEvent_t e1, int64_t* kernels) {
+    const bool fb = c.form == TSG_FORM_B, tp = c.strategy == TSG_STRATEGY_TWOPHASE;
+    if (fb && tp) return enqueue_pass_t<true, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
+    if (fb) return enqueue_pass_t<true, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
+    if (tp) return enqueue_pass_t<false, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
+    return enqueue_pass_t<false, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
+  }
+
+  static tsg_status set_coords(tsg_mesh* m, const double* xy_host) {
+    cudaStream_t s = m->ctx->stream;
+    const int64_t nv = m->hm.nv;
+    TSG_CUDA(cudaMemcpyAsync(m->d_xy_stage, xy_host, 2 * nv * sizeof(double), cudaMemcpyHostToDevice, s));
+    coords_from_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(m->d_xy_stage, m->d_order, nv,
+                                                                coords_of<R, kSoA>(m, 0),
+                                                                coords_of<R, kSoA>(m, 1));
+    TSG_CUDA(cudaGetLastError());
+    m->cur = 0;
+    return TSG_OK;
+  }
+
+  static tsg_status get_coords(tsg_mesh* m, double* xy_host) {
+    cudaStream_t s = m->ctx->stream;
+    const int64_t nv = m->hm.nv;
+    coords_to_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, m->cur), m->d_order,
+                                                              nv, m->d_xy_stage);
+    TSG_CUDA(cudaGetLastError());
+    TSG_CUDA(cudaMemcpyAsync(xy_host, m->d_xy_stage, 2 * nv * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    return TSG_OK;
+  }
+
+  // Current coordinates into buf0 (both buffers equal afterwards for pinned vertices anyway).
+  static tsg_status normalize(tsg_mesh* m) {
+    if (m->cur != 0) {
+      TSG_CUDA(cudaMemcpyAsync(m->buf[0], m->buf[1], 2 * m->hm.nv * sizeof(R), cudaMemcpyDeviceToDevice,
+                               m->ctx->stream));
+      m->cur = 0;
+    }
+    return TSG_OK;
+  }
+
+  static tsg_status refresh_alpha(tsg_mesh* m) {
+    cudaStream_t s = m->ctx->stream;
+    tsg::tri_alpha<R, kSoA><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
+        coords_of<R, kSoA>(m, m->cur), coords_of<R, kSoA>(m, m->cur), 0, nullptr, m->d_tri, m->hm.nt,
+        static_cast<R*>(m->d_alpha));
+    TSG_CUDA(cudaGetLastError());
+    return TSG_OK;
+  }
+};
+
+template <class F>
+tsg_status dispatch(const tsg_mesh* m, F&& f) {
+  if (m->prec == TSG_F64) {
+    if (m->layout == TSG_LAYOUT_SOA) return f(Engine<double, true>{});
+    return f(Engine<double, false>{});
+  }
+  if (m->layout == TSG_LAYOUT_SOA) return f(Engine<float, true>{});
+  return f(Engine<float, false>{});
+}
+
+tsg_status validate_cfg(const tsg_smooth_cfg* c) {
+  if (!c) return fail(TSG_ERR_INVALID, "null config");
+  if (c->form != TSG_FORM_A && c->form != TSG_FORM_B) return fail(TSG_ERR_INVALID, "form must be A or B");
+  if (c->strategy != TSG_STRATEGY_FUSED && c->strategy != TSG_STRATEGY_TWOPHASE)
+    return fail(TSG_ERR_INVALID, "strategy must be fused or twophase");
+  if (c->swap != TSG_SWAP_PINGPONG && c->swap != TSG_SWAP_COPY)
+    return fail(TSG_ERR_INVALID, "swap must be pingpong or copy");
+  if (c->chunks < 1) return fail(TSG_ERR_INVALID, "workers must be >= 1");
+  if (c->max_iters < 1) return fail(TSG_ERR_INVALID, "max_iters must be >= 1");
+  if (!(c->move_tol >= 0.0)) return fail(TSG_ERR_INVALID, "move_tol must be >= 0");
+  if (c->driver < TSG_DRIVER_GRAPH || c->driver > TSG_DRIVER_STREAM)
+    return fail(TSG_ERR_INVALID, "driver must be graph or stream");
+  return TSG_OK;
+}
+
+tsg_status ensure_stats_capacity(tsg_mesh* m, int32_t n) {
+  if (m->cap >= n) return TSG_OK;
+  cudaFree(m->d_acc);
+  cudaFree(m->d_md);
+  m->d_acc = nullptr;
+  m->d_md = nullptr;
+  TSG_CUDA(cudaMalloc(&m->d_acc, sizeof(int32_t) * n));
+  TSG_CUDA(cudaMalloc(&m->d_md, sizeof(unsigned long long) * n));
+  m->cap = n;
+  m->gc.reset();  // graph captured old pointers
+  return TSG_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- C ABI
+
+extern "C" {
+
+int32_t tsg_abi_version(void) { return TSG_ABI_VERSION; }
+
+const char* tsg_last_error(void) { return g_err.c_str(); }
+
+int32_t tsg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+tsg_status tsg_context_create(int32_t device, tsg_context** out) {
+  if (!out) return fail(TSG_ERR_INVALID, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(TSG_ERR_NODEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= n) return fail(TSG_ERR_INVALID, "device index out of range");
+  TSG_CUDA(cudaSetDevice(device));
+  auto ctx = std::make_unique<tsg_context>();
+  ctx->device = device;
+  TSG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  TSG_CUDA(cudaEventCreate(&ctx->ev0));
+  TSG_CUDA(cudaEventCreate(&ctx->ev1));
+  *out = ctx.release();
+  return TSG_OK;
+}
+
+tsg_status tsg_context_destroy(tsg_context* ctx) {
+  if (!ctx) return TSG_OK;
+  cudaSetDevice(ctx->device);
+  for (cudaEvent_t e : ctx->pass_events) cudaEventDestroy(e);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TSG_OK;
+}
+
+void* tsg_context_stream(tsg_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
+  if (nv < 0 || (nv > 0 && (!xy || !order_out))) return fail(TSG_ERR_INVALID, "bad arguments");
+  tsg::hilbert_order(nv, xy, order_out);
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** out) {
+  if (!ctx || !d || !out) return fail(TSG_ERR_INVALID, "null argument");
+  if (!d->xy || !d->tri || !d->nbr_off || !d->nbr || !d->inc_off || !d->inc || !d->boundary)
+    return fail(TSG_ERR_INVALID, "mesh description has null arrays");
+  if (d->layout != TSG_LAYOUT_AOS && d->layout != TSG_LAYOUT_SOA)
+    return fail(TSG_ERR_INVALID, "layout must be aos or soa");
+  if (d->precision != TSG_F64 && d->precision != TSG_F32)
+    return fail(TSG_ERR_INVALID, "precision must be f64 or f32");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  auto m = std::make_unique<tsg_mesh>();
+  m->ctx = ctx;
+  m->layout = d->layout;
+  m->prec = d->precision;
+  m->rsize = d->precision == TSG_F64 ? 8 : 4;
+  const std::string err = tsg::build_host_mesh(*d, kMaxSmallDeg, m->hm);
+  if (!err.empty()) return fail(TSG_ERR_INVALID, err);
+  const auto& hm = m->hm;
+  const int64_t nv = hm.nv, nt = hm.nt;
+  cudaStream_t s = ctx->stream;
+  int64_t* b = &m->bytes;
+  tsg_status st;
+  for (int i = 0; i < 2; ++i) {
+    TSG_CUDA(cudaMalloc(&m->buf[i], 2 * nv * m->rsize));
+    *b += 2 * nv * m->rsize;
+  }
+  if ((st = upload(&m->d_off, hm.off, b, s))) return st;
+  if ((st = upload(&m->d_nbr, hm.nbr, b, s))) return st;
+  if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
+  if ((st = upload(&m->d_vinc_off, hm.vinc_off, b, s))) return st;
+  if ((st = upload(&m->d_vinc, hm.vinc, b, s))) return st;
+  if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
+  if ((st = upload(&m->d_hubs, hm.hubs, b, s))) return st;
+  if (d->order) {
+    if ((st = upload(&m->d_order, hm.order, b, s))) return st;
+    if ((st = upload(&m->d_tri_order, hm.tri_order, b, s))) return st;
+  }
+  TSG_CUDA(cudaMalloc(&m->d_alpha, nt * m->rsize));
+  *b += nt * m->rsize;
+  if ((st = dalloc(&m->d_xy_stage, 2 * nv, b))) return st;
+  if ((st = dalloc(&m->d_vmin, nv, b))) return st;
+  if ((st = dalloc(&m->d_decision, nv, b))) return st;
+  if ((st = dalloc(&m->d_decision_orig, nv, b))) return st;
+  if ((st = dalloc(&m->d_state, 1, b))) return st;
+  if ((st = dalloc(&m->d_ext, 3, b))) return st;
+  for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
+  if ((st = ensure_stats_capacity(m.get(), 128))) return st;
+  st = dispatch(m.get(), [&](auto E) { return decltype(E)::set_coords(m.get(), d->xy); });
+  if (st) return st;
+  st = dispatch(m.get(), [&](auto E) { return decltype(E)::prepare(m.get()); });
+  if (st) return st;
+  TSG_CUDA(cudaStreamSynchronize(s));
+  *out = m.release();
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_free(tsg_mesh* m) {
+  if (!m) return TSG_OK;
+  cudaSetDevice(m->ctx->device);
+  m->gc.reset();
+  free_form_b(m);
+  void* ptrs[] = {m->buf[0], m->buf[1], m->d_off, m->d_nbr, m->d_fan, m->d_vinc_off, m->d_vinc,
+                  m->d_tri, m->d_hubs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
+                  m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md,
+                  m->d_ext};
+  for (void* p : ptrs) cudaFree(p);
+  delete m;
+  return TSG_OK;
+}
+
+int64_t tsg_mesh_device_bytes(const tsg_mesh* m) { return m ? m->bytes : 0; }
+
+tsg_status tsg_mesh_set_coords(tsg_mesh* m, const double* xy) {
+  if (!m || !xy) return fail(TSG_ERR_INVALID, "null argument");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::set_coords(m, xy); });
+  if (st) return st;
+  TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_get_coords(tsg_mesh* m, double* xy_out) {
+  if (!m || !xy_out) return fail(TSG_ERR_INVALID, "null argument");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  return dispatch(m, [&](auto E) { return decltype(E)::get_coords(m, xy_out); });
+}
+
+tsg_status tsg_tri_alpha(tsg_mesh* m, double* alpha_out) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::refresh_alpha(m); });
+  if (st) return st;
+  if (alpha_out) {
+    // device triangle i holds original triangle tri_order[i]
+    double* tmp = m->d_xy_stage;  // 2*nv doubles; triangles may exceed it
+    double* dst = nullptr;
+    bool own = false;
+    if (m->hm.nt <= 2 * m->hm.nv) {
+      dst = tmp;
+    } else {
+      TSG_CUDA(cudaMalloc(&dst, m->hm.nt * sizeof(double)));
+      own = true;
+    }
+    if (m->prec == TSG_F64)
+      to_double_scatter<double><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
+          static_cast<const double*>(m->d_alpha), m->d_tri_order, m->hm.nt, dst);
+    else
+      to_double_scatter<float><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
+          static_cast<const float*>(m->d_alpha), m->d_tri_order, m->hm.nt, dst);
+    TSG_CUDA(cudaGetLastError());
+    TSG_CUDA(cudaMemcpyAsync(alpha_out, dst, m->hm.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    if (own) cudaFree(dst);
+  } else {
+    TSG_CUDA(cudaStreamSynchronize(s));
+  }
+  return TSG_OK;
+}
+
+tsg_status tsg_vertex_minima(tsg_mesh* m, double* vmin_out) {
+  if (!m || !vmin_out) return fail(TSG_ERR_INVALID, "null argument");
+  tsg_status st = tsg_tri_alpha(m, nullptr);
+  if (st) return st;
+  cudaStream_t s = m->ctx->stream;
+  const int64_t nv = m->hm.nv;
+  if (m->prec == TSG_F64)
+    tsg::vertex_min<double><<<grid_for(nv, 256), 256, 0, s>>>(m->d_vinc_off, m->d_vinc,
+                                                              static_cast<const double*>(m->d_alpha), nv, m->d_vmin);
+  else
+    tsg::vertex_min<float><<<grid_for(nv, 256), 256, 0, s>>>(m->d_vinc_off, m->d_vinc,
+                                                             static_cast<const float*>(m->d_alpha), nv, m->d_vmin);
+  TSG_CUDA(cudaGetLastError());
+  to_double_scatter<double><<<grid_for(nv, 256), 256, 0, s>>>(m->d_vmin, m->d_order, nv, m->d_xy_stage);
+  TSG_CUDA(cudaGetLastError());
+  TSG_CUDA(cudaMemcpyAsync(vmin_out, m->d_xy_stage, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  return TSG_OK;
+}
+
+tsg_status tsg_alpha_extrema(tsg_mesh* m, double* min_out, double* max_out, int64_t* nonpos_out) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  tsg_status st = tsg_tri_alpha(m, nullptr);
+  if (st) return st;
+  cudaStream_t s = m->ctx->stream;
+  const unsigned long long init[3] = {~0ULL, 0ULL, 0ULL};
+  TSG_CUDA(cudaMemcpyAsync(m->d_ext, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (m->prec == TSG_F64)
+    tsg::alpha_extrema<double><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
+        static_cast<const double*>(m->d_alpha), m->hm.nt, m->d_ext, m->d_ext + 1, m->d_ext + 2);
+  else
+    tsg::alpha_extrema<float><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
+        static_cast<const float*>(m->d_alpha), m->hm.nt, m->d_ext, m->d_ext + 1, m->d_ext + 2);
+  TSG_CUDA(cudaGetLastError());
+  unsigned long long h[3];
+  TSG_CUDA(cudaMemcpyAsync(h, m->d_ext, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  auto unkey = [](unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+  };
+  if (min_out) *min_out = unkey(h[0]);
+  if (max_out) *max_out = unkey(h[1]);
+  if (nonpos_out) *nonpos_out = static_cast<int64_t>(h[2]);
+  return TSG_OK;
+}
+
+tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* stats,
+                      int32_t* accepted_per_pass, double* max_disp_per_pass, int32_t capacity) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  tsg_status st = validate_cfg(c);
+  if (st) return st;
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  tsg_context* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  if (c->form == TSG_FORM_B && (st = ensure_form_b(m, c->chunks))) return st;
+  if ((st = ensure_stats_capacity(m, c->max_iters))) return st;
+  st = dispatch(m, [&](auto E) { return decltype(E)::normalize(m); });
+  if (st) return st;
+  const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
+  TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_acc, 0, sizeof(int32_t) * c->max_iters, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_md, 0, sizeof(unsigned long long) * c->max_iters, s));
+
+  int64_t kernels_per_pass = 0;
+  double node_ms = -1.0;
+  int64_t launches = 0;
+  if (c->driver == TSG_DRIVER_GRAPH) {
+    GraphCache& g = m->gc;
+    if (!(g.valid && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
+          g.swap == c->swap && g.max_iters == c->max_iters && g.tol_abs == tol_abs)) {
+      g.reset();
+      TSG_CUDA(cudaGraphCreate(&g.graph, 0));
+      cudaGraphConditionalHandle h;
+      TSG_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      TSG_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      TSG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      int64_t k = 0;
+      st = dispatch(m, [&](auto E) {
+        return decltype(E)::enqueue_pass(m, *c, s, tol_abs, h, 1, nullptr, nullptr, nullptr, &k);
+      });
+      cudaGraph_t captured = nullptr;
+      cudaError_t e = cudaStreamEndCapture(s, &captured);
+      if (st) return st;
+      if (e != cudaSuccess) return fail(TSG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+      TSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+      g.valid = true;
+      g.form = c->form;
+      g.strategy = c->strategy;
+      g.chunks = c->chunks;
+      g.swap = c->swap;
+      g.max_iters = c->max_iters;
+      g.tol_abs = tol_abs;
+      g.kernels_per_pass = k;
+    }
+    kernels_per_pass = g.kernels_per_pass;
+    TSG_CUDA(cudaEventRecord(ctx->ev0, s));
+    TSG_CUDA(cudaGraphLaunch(g.exec, s));
+    TSG_CUDA(cudaEventRecord(ctx->ev1, s));
+  } else {
+    // Plain launches; kernels early-exit once done is set.  Per-pass events bracket the
+    // node-update launches so the bench can time the node kernel alone.
+    const size_t need = 2 * static_cast<size_t>(c->max_iters);
+    while (ctx->pass_events.size() < need) {
+      cudaEvent_t e;
+      TSG_CUDA(cudaEventCreate(&e));
+      ctx->pass_events.push_back(e);
+    }
+    TSG_CUDA(cudaEventRecord(ctx->ev0, s));
+    int32_t host_state[4] = {0, 0, 0, 0};
+    int q = 0;
+    for (; q < c->max_iters; ++q) {
+      int64_t k = 0;
+      st = dispatch(m, [&](auto E) {
+        return decltype(E)::enqueue_pass(m, *c, s, tol_abs, cudaGraphConditionalHandle{}, 0, nullptr,
+                                         ctx->pass_events[2 * q], ctx->pass_events[2 * q + 1], &k);
+      });
+      if (st) return st;
+      kernels_per_pass = k;
+      if ((q & 7) == 7 || q + 1 == c->max_iters) {
+        TSG_CUDA(cudaMemcpyAsync(host_state, m->d_state, sizeof(host_state), cudaMemcpyDeviceToHost, s));
+        TSG_CUDA(cudaStreamSynchronize(s));
+        if (host_state[1]) {
+          ++q;
+          break;
+        }
+      }
+    }
+    TSG_CUDA(cudaEventRecord(ctx->ev1, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    launches = kernels_per_pass * q;
+  }
+  TSG_CUDA(cudaStreamSynchronize(s));
+  tsg::PassState hs;
+  TSG_CUDA(cudaMemcpy(&hs, m->d_state, sizeof hs, cudaMemcpyDeviceToHost));
+  float total_ms = 0.f;
+  TSG_CUDA(cudaEventElapsedTime(&total_ms, ctx->ev0, ctx->ev1));
+  const int32_t it = hs.pass;
+  if (c->driver == TSG_DRIVER_STREAM) {
+    node_ms = 0.0;  // node-update launches of the passes that ran (events bracket them)
+    for (int p = 0; p < it; ++p) {
+      float ms = 0.f;
+      TSG_CUDA(cudaEventElapsedTime(&ms, ctx->pass_events[2 * p], ctx->pass_events[2 * p + 1]));
+      node_ms += ms;
+    }
+  }
+  if (c->swap == TSG_SWAP_PINGPONG) m->cur = it & 1;
+  else m->cur = 0;
+  const int32_t n = std::min(capacity, it);
+  if (accepted_per_pass && n > 0)
+    TSG_CUDA(cudaMemcpy(accepted_per_pass, m->d_acc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  if (max_disp_per_pass && n > 0) {
+    std::vector<unsigned long long> bits(n);
+    TSG_CUDA(cudaMemcpy(bits.data(), m->d_md, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+    std::memcpy(max_disp_per_pass, bits.data(), sizeof(double) * n);
+  }
+  if (stats) {
+    stats->iterations = it;
+    stats->stop = hs.stop;
+    stats->node_updates = m->hm.nv * static_cast<int64_t>(it);
+    stats->device_ms = total_ms;
+    stats->node_kernel_ms = node_ms;
+    stats->launches = c->driver == TSG_DRIVER_GRAPH ? kernels_per_pass * it : launches;
+  }
+  return TSG_OK;
+}
+
+tsg_status tsg_smooth_host(tsg_mesh* m, const double* xy_in, const tsg_smooth_cfg* c, double* xy_out,
+                           tsg_smooth_stats* stats, int32_t* accepted_per_pass,
+                           double* max_disp_per_pass, int32_t capacity) {
+  if (!m || !xy_in || !xy_out) return fail(TSG_ERR_INVALID, "null argument");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::set_coords(m, xy_in); });
+  if (st) return st;
+  if ((st = tsg_smooth(m, c, stats, accepted_per_pass, max_disp_per_pass, capacity))) return st;
+  return tsg_mesh_get_coords(m, xy_out);
+}
+
+tsg_status tsg_pass_lockstep(tsg_mesh* m, int32_t form, int32_t chunks, int8_t* decision_out,
+                             int32_t* accepted_out, double* max_disp_out) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  tsg_smooth_cfg c{};
+  c.form = form;
+  c.strategy = TSG_STRATEGY_FUSED;
+  c.chunks = chunks;
+  c.swap = TSG_SWAP_PINGPONG;
+  c.max_iters = 1;
+  c.driver = TSG_DRIVER_STREAM;
+  c.move_tol = 0.0;
+  c.bbox_diag = 0.0;
+  tsg_status st = validate_cfg(&c);
+  if (st) return st;
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  if (form == TSG_FORM_B && (st = ensure_form_b(m, chunks))) return st;
+  st = dispatch(m, [&](auto E) { return decltype(E)::normalize(m); });
+  if (st) return st;
+  TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_acc, 0, sizeof(int32_t), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_md, 0, sizeof(unsigned long long), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_decision, 0xff, m->hm.nv, s));
+  int64_t k = 0;
+  st = dispatch(m, [&](auto E) {
+    return decltype(E)::enqueue_pass(m, c, s, 0.0, cudaGraphConditionalHandle{}, 0, m->d_decision,
+                                     nullptr, nullptr, &k);
+  });
+  if (st) return st;
+  m->cur = 1;
+  if (decision_out) {
+    scatter_i8<<<grid_for(m->hm.nv, 256), 256, 0, s>>>(m->d_decision, m->d_order, m->hm.nv,
+                                                       m->d_decision_orig);
+    TSG_CUDA(cudaGetLastError());
+    TSG_CUDA(cudaMemcpyAsync(decision_out, m->d_decision_orig, m->hm.nv, cudaMemcpyDeviceToHost, s));
+  }
+  int32_t acc = 0;
+  unsigned long long md = 0;
+  TSG_CUDA(cudaMemcpyAsync(&acc, m->d_acc, sizeof acc, cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaMemcpyAsync(&md, m->d_md, sizeof md, cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  if (accepted_out) *accepted_out = acc;
+  if (max_disp_out) std::memcpy(max_disp_out, &md, sizeof(double));
+  return TSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,412 @@
+// sm_100a kernels of one Smart Laplacian pass.
+//
+//   node_update  thread per vertex (deg <= kMaxDeg): gather the one-ring into a per-thread
+//                shared-memory slice (entry-major, conflict-free), ordered neighbour sum,
+//                pass-start threshold and hypothetical min α over the fan, strict accept,
+//                write, block-reduced {accepted, max displacement}.
+//                Reference: smooth_range / neighbor_mean / min_alpha_at
+//                (proj/include/trismooth/smoothing.hpp:70-109, quality.hpp:54-64).
+//   hub_update   CTA per high-valence vertex (the paper's CDP child launches, PAPER.md:334-341,
+//                replaced by cooperative threads): shared-memory staged one-ring, one thread
+//                does the ordered sum while the CTA evaluates the fan, block min-reduction.
+//   tri_alpha    thread per triangle (refresh_tri_alphas, quality.hpp:68-74): the TwoPhase
+//                field and the final write-back.
+//   vertex_min   thread per vertex (reduce_vertex_minima, quality.hpp:78-89).
+//   finalize     1 thread: the stop rule in the reference's order (smoothing.cpp:132-141),
+//                sets the WHILE-graph condition.
+#pragma once
+
+#include "tsg_device.cuh"
+
+namespace tsg {
+
+constexpr int kNodeBlock = 128;
+constexpr int kHubBlock = 256;
+
+enum { kStopMaxIters = 0, kStopDisplacement = 1, kStopNoMoves = 2 };
+enum { kSwapPingPong = 0, kSwapCopy = 1 };
+
+template <typename R, bool kSoA>
+struct PassArgs {
+  Coords<R, kSoA> buf0, buf1;   // ping-pong pair; copy mode: buf0 = live, buf1 = snapshot
+  int32_t swap;
+  const uint32_t* off;          // nv+1, compact CSR over slots (rows only for movable vertices)
+  const uint32_t* nbr;          // slots, ascending ORIGINAL id (| kFreshBit for Form B)
+  const uint32_t* fan;          // fan records, same offsets as nbr
+  const uint32_t* vinc_off;     // TwoPhase: incident-triangle CSR over slots
+  const uint32_t* vinc;
+  const R* alpha;               // TwoPhase: pass-start α field (device triangle order)
+  const int32_t* list;          // phase node list (nullptr = slots [0, count))
+  int64_t count;
+  PassState* st;
+  int32_t* pass_acc;
+  unsigned long long* pass_md;  // max displacement bits (non-negative doubles order as u64)
+  int8_t* decision;             // optional: 1 accept / 0 reject per slot
+};
+
+template <typename R, bool kSoA>
+__device__ __forceinline__ void select_buffers(const PassArgs<R, kSoA>& a, int pass,
+                                               Coords<R, kSoA>& P, Coords<R, kSoA>& N) {
+  if (a.swap == kSwapCopy || (pass & 1)) {
+    P = a.buf1;
+    N = a.buf0;
+  } else {
+    P = a.buf0;
+    N = a.buf1;
+  }
+}
+
+// Block reduction of {accepted, max displacement} and one pair of atomics per block.
+template <int kBlock>
+__device__ __forceinline__ void commit_stats(int accepted, double disp, int32_t* acc_slot,
+                                             unsigned long long* md_slot) {
+  __shared__ int s_acc[kBlock / 32];
+  __shared__ double s_md[kBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  accepted = __reduce_add_sync(0xffffffffu, accepted);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) disp = fmax(disp, __shfl_xor_sync(0xffffffffu, disp, o));
+  if (lane == 0) {
+    s_acc[warp] = accepted;
+    s_md[warp] = disp;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    accepted = lane < kBlock / 32 ? s_acc[lane] : 0;
+    disp = lane < kBlock / 32 ? s_md[lane] : 0.0;
+    accepted = __reduce_add_sync(0xffffffffu, accepted);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) disp = fmax(disp, __shfl_xor_sync(0xffffffffu, disp, o));
+    if (lane == 0) {
+      if (accepted) atomicAdd(acc_slot, accepted);
+      if (disp > 0.0) atomicMax(md_slot, static_cast<unsigned long long>(__double_as_longlong(disp)));
+    }
+  }
+}
+
+// Thread-per-vertex node update.  Shared memory: kMaxDeg x kNodeBlock coordinate pairs,
+// entry-major so that lane t of every warp hits bank group t regardless of the entry it
+// reads (the fan indexes entries at random).
+template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg>
+__global__ void __launch_bounds__(kNodeBlock) node_update(PassArgs<R, kSoA> a) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  __shared__ R2 ring[kMaxDeg * kNodeBlock];
+  const PassState* st = a.st;
+  if (st->done) return;
+  const int pass = st->pass;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, pass, P, N);
+
+  const int tid = threadIdx.x;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kNodeBlock + tid;
+  int accepted = 0;
+  double disp = 0.0;
+  if (i < a.count) {
+    const int64_t s = a.list ? static_cast<int64_t>(a.list[i]) : i;
+    const uint32_t o0 = a.off[s];
+    const int deg = static_cast<int>(a.off[s + 1] - o0);
+    if (deg > 0 && deg <= kMaxDeg) {
+      const uint32_t* nb = a.nbr + o0;
+      const uint32_t* fan = a.fan + o0;
+      const R2 pv = P.load(s);
+      R sx = R(0), sy = R(0);
+      uint32_t fresh = 0;
+      // Gather in batches of 8 (independent loads in flight), ordered accumulation.
+#pragma unroll
+      for (int base = 0; base < kMaxDeg; base += 8) {
+        if (base < deg) {
+          uint32_t u[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) u[j] = (base + j < deg) ? __ldg(nb + base + j) : 0u;
+          R2 c[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (base + j < deg) c[j] = P.load(u[j] & ~kFreshBit);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (base + j < deg) {
+              ring[(base + j) * kNodeBlock + tid] = c[j];
+              if constexpr (kFormB) {
+                if (u[j] & kFreshBit) fresh |= 1u << (base + j);
+              } else {
+                sx = O::add(sx, c[j].x);
+                sy = O::add(sy, c[j].y);
+              }
+            }
+          }
+        }
+      }
+
+      R thr = R(INFINITY);
+      if constexpr (kTwoPhase) {
+        const uint32_t t0 = a.vinc_off[s], t1 = a.vinc_off[s + 1];
+        for (uint32_t t = t0; t < t1; ++t) thr = min_ref(thr, a.alpha[a.vinc[t]]);
+      }
+      R hyp = R(INFINITY);
+      R2 cand;
+      if constexpr (!kFormB && !kTwoPhase) {
+        // Form A, fused: threshold and hypothetical share the rim edge b - a.
+        const R inv = O::div(R(1), static_cast<R>(deg));
+        cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+        for (int j = 0; j < deg; ++j) {
+          const uint32_t f = __ldg(fan + j);
+          const R2 pa = ring[fan_i1(f) * kNodeBlock + tid];
+          const R2 pb = ring[fan_i2(f) * kNodeBlock + tid];
+          const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
+          const R sabx = O::mul(dabx, dabx), saby = O::mul(daby, daby);
+          const int k = fan_k(f);
+          thr = min_ref(thr, alpha_at<R>(k, pv.x, pv.y, pa.x, pa.y, pb.x, pb.y, dabx, daby, sabx, saby));
+          hyp = min_ref(hyp, alpha_at<R>(k, cand.x, cand.y, pa.x, pa.y, pb.x, pb.y, dabx, daby, sabx, saby));
+        }
+      } else {
+        if constexpr (!kTwoPhase) {
+          // Fused threshold from pass-start positions (Form B: before fresh reads patch in).
+          for (int j = 0; j < deg; ++j) {
+            const uint32_t f = __ldg(fan + j);
+            const R2 pa = ring[fan_i1(f) * kNodeBlock + tid];
+            const R2 pb = ring[fan_i2(f) * kNodeBlock + tid];
+            const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
+            thr = min_ref(thr, alpha_at<R>(fan_k(f), pv.x, pv.y, pa.x, pa.y, pb.x, pb.y, dabx, daby,
+                                           O::mul(dabx, dabx), O::mul(daby, daby)));
+          }
+        }
+        if constexpr (kFormB) {
+          // ChunkView (quality.hpp:40-50): in-chunk lower-id neighbours read this pass's values.
+          while (fresh) {
+            const int j = __ffs(fresh) - 1;
+            fresh &= fresh - 1;
+            ring[j * kNodeBlock + tid] = N.load_mut(nb[j] & ~kFreshBit);
+          }
+          for (int j = 0; j < deg; ++j) {
+            const R2 c = ring[j * kNodeBlock + tid];
+            sx = O::add(sx, c.x);
+            sy = O::add(sy, c.y);
+          }
+        }
+        const R inv = O::div(R(1), static_cast<R>(deg));
+        cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+        // Hypothetical min with early rejection: once one triangle falls to <= thr the
+        // strict test (smoothing.hpp:99) cannot pass.
+        for (int j = 0; j < deg; ++j) {
+          const uint32_t f = __ldg(fan + j);
+          const R2 pa = ring[fan_i1(f) * kNodeBlock + tid];
+          const R2 pb = ring[fan_i2(f) * kNodeBlock + tid];
+          const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
+          hyp = min_ref(hyp, alpha_at<R>(fan_k(f), cand.x, cand.y, pa.x, pa.y, pb.x, pb.y, dabx, daby,
+                                         O::mul(dabx, dabx), O::mul(daby, daby)));
+          if (!(hyp > thr)) break;
+        }
+      }
+      const bool acc = hyp > thr;
+      N.store(s, acc ? cand : pv);
+      if (acc) {
+        accepted = 1;
+        const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+        disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      }
+      if (a.decision) a.decision[s] = acc ? 1 : 0;
+    }
+  }
+  commit_stats<kNodeBlock>(accepted, disp, a.pass_acc + pass, a.pass_md + pass);
+}
+
+// CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)
+// by `cap` view pairs; entries beyond cap are read from global memory.
+template <typename R, bool kSoA, bool kFormB, bool kTwoPhase>
+__global__ void __launch_bounds__(kHubBlock) hub_update(PassArgs<R, kSoA> a, int cap) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  extern __shared__ __align__(16) unsigned char hub_smem[];
+  R2* pring = reinterpret_cast<R2*>(hub_smem);
+  R2* vring = pring + cap;
+  __shared__ R2 s_cand;
+  __shared__ R s_thr[kHubBlock / 32], s_hyp[kHubBlock / 32];
+
+  const PassState* st = a.st;
+  if (st->done) return;
+  const int pass = st->pass;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, pass, P, N);
+  const int tid = threadIdx.x;
+  const int64_t s = a.list[blockIdx.x];
+  const uint32_t o0 = a.off[s];
+  const int deg = static_cast<int>(a.off[s + 1] - o0);
+  const uint32_t* nb = a.nbr + o0;
+  const uint32_t* fan = a.fan + o0;
+  const int staged = deg < cap ? deg : cap;
+
+  for (int j = tid; j < staged; j += kHubBlock) {
+    const uint32_t u = nb[j];
+    const R2 c = P.load(u & ~kFreshBit);
+    pring[j] = c;
+    if constexpr (kFormB) vring[j] = (u & kFreshBit) ? N.load_mut(u & ~kFreshBit) : c;
+  }
+  __syncthreads();
+  auto pget = [&](int j) -> R2 { return j < cap ? pring[j] : P.load(nb[j] & ~kFreshBit); };
+  auto vget = [&](int j) -> R2 {
+    if constexpr (kFormB) {
+      if (j < cap) return vring[j];
+      const uint32_t u = nb[j];
+      return (u & kFreshBit) ? N.load_mut(u & ~kFreshBit) : P.load(u);
+    } else {
+      return pget(j);
+    }
+  };
+  const R2 pv = P.load(s);
+  if (tid == 0) {
+    // neighbor_mean: ordered, single chain (smoothing.hpp:72-80).
+    R sx = R(0), sy = R(0);
+#pragma unroll 8
+    for (int j = 0; j < deg; ++j) {
+      const R2 c = vget(j);
+      sx = O::add(sx, c.x);
+      sy = O::add(sy, c.y);
+    }
+    const R inv = O::div(R(1), static_cast<R>(deg));
+    s_cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+  }
+  R thr = R(INFINITY);
+  if constexpr (kTwoPhase) {
+    const uint32_t t0 = a.vinc_off[s], t1 = a.vinc_off[s + 1];
+    for (uint32_t t = t0 + tid; t < t1; t += kHubBlock) thr = min_ref(thr, a.alpha[a.vinc[t]]);
+  } else {
+    for (int j = tid; j < deg; j += kHubBlock) {
+      const uint32_t f = fan[j];
+      const R2 pa = pget(fan_i1(f)), pb = pget(fan_i2(f));
+      const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
+      thr = min_ref(thr, alpha_at<R>(fan_k(f), pv.x, pv.y, pa.x, pa.y, pb.x, pb.y, dabx, daby,
+                                     O::mul(dabx, dabx), O::mul(daby, daby)));
+    }
+  }
+  __syncthreads();
+  const R2 cand = s_cand;
+  R hyp = R(INFINITY);
+  for (int j = tid; j < deg; j += kHubBlock) {
+    const uint32_t f = fan[j];
+    const R2 pa = vget(fan_i1(f)), pb = vget(fan_i2(f));
+    const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
+    hyp = min_ref(hyp, alpha_at<R>(fan_k(f), cand.x, cand.y, pa.x, pa.y, pb.x, pb.y, dabx, daby,
+                                   O::mul(dabx, dabx), O::mul(daby, daby)));
+  }
+  // Exact min in any order (no NaN on finite input).
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    thr = min_ref(thr, __shfl_xor_sync(0xffffffffu, thr, o));
+    hyp = min_ref(hyp, __shfl_xor_sync(0xffffffffu, hyp, o));
+  }
+  if ((tid & 31) == 0) {
+    s_thr[tid >> 5] = thr;
+    s_hyp[tid >> 5] = hyp;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kHubBlock / 32; ++w) {
+      thr = min_ref(thr, s_thr[w]);
+      hyp = min_ref(hyp, s_hyp[w]);
+    }
+    const bool acc = hyp > thr;
+    N.store(s, acc ? cand : pv);
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+    if (acc) {
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      atomicAdd(a.pass_acc + pass, 1);
+      if (d > 0.0) atomicMax(a.pass_md + pass, static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
+  }
+}
+
+// α per triangle from the pass-start buffer (or buf0 when st == nullptr).
+template <typename R, bool kSoA>
+__global__ void __launch_bounds__(256) tri_alpha(Coords<R, kSoA> buf0, Coords<R, kSoA> buf1,
+                                                 int32_t swap, const PassState* st,
+                                                 const int32_t* __restrict__ tri, int64_t nt,
+                                                 R* __restrict__ alpha) {
+  Coords<R, kSoA> P = buf0;
+  if (st) {
+    if (st->done) return;
+    if (swap == kSwapCopy || (st->pass & 1)) P = buf1;
+  }
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v0 = __ldg(tri + 3 * t), v1 = __ldg(tri + 3 * t + 1), v2 = __ldg(tri + 3 * t + 2);
+    const auto p0 = P.load(v0), p1 = P.load(v1), p2 = P.load(v2);
+    alpha[t] = alpha_plain<R>(p0.x, p0.y, p1.x, p1.y, p2.x, p2.y);
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) vertex_min(const uint32_t* __restrict__ vinc_off,
+                                                  const uint32_t* __restrict__ vinc,
+                                                  const R* __restrict__ alpha, int64_t nv,
+                                                  double* __restrict__ out) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t t0 = vinc_off[s], t1 = vinc_off[s + 1];
+    if (t0 == t1) {
+      out[s] = __longlong_as_double(0x7ff8000000000000LL);  // kUnsetQuality (quiet NaN)
+      continue;
+    }
+    R best = R(INFINITY);
+    for (uint32_t t = t0; t < t1; ++t) best = min_ref(best, alpha[vinc[t]]);
+    out[s] = static_cast<double>(best);
+  }
+}
+
+// Order-preserving map double -> u64 for atomic min / max.
+__device__ __forceinline__ unsigned long long ordered_key(double d) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) alpha_extrema(const R* __restrict__ alpha, int64_t nt,
+                                                     unsigned long long* mn, unsigned long long* mx,
+                                                     unsigned long long* nonpos) {
+  unsigned long long lo = ~0ULL, hi = 0ULL, np = 0;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double q = static_cast<double>(alpha[t]);
+    const unsigned long long k = ordered_key(q);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+    np += q <= 0.0 ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+    np += __shfl_xor_sync(0xffffffffu, np, o);
+  }
+  if ((threadIdx.x & 31) != 0) return;
+  atomicMin(mn, lo);
+  atomicMax(mx, hi);
+  if (np) atomicAdd(nonpos, np);
+}
+
+__global__ void finalize_pass(PassState* st, const int32_t* pass_acc,
+                              const unsigned long long* pass_md, double tol_abs, int32_t max_iters,
+                              cudaGraphConditionalHandle handle, int32_t use_handle) {
+  if (!st->done) {
+    const int q = st->pass;
+    const int32_t acc = pass_acc[q];
+    const double md = __longlong_as_double(static_cast<long long>(pass_md[q]));
+    st->pass = q + 1;
+    if (acc == 0) {
+      st->done = 1;
+      st->stop = kStopNoMoves;
+    } else if (md < tol_abs) {
+      st->done = 1;
+      st->stop = kStopDisplacement;
+    } else if (q + 1 >= max_iters) {
+      st->done = 1;
+      st->stop = kStopMaxIters;
+    }
+  }
+  if (use_handle) cudaGraphSetConditional(handle, st->done ? 0u : 1u);
+}
+
+}  // namespace tsg

@@ -1,0 +1,315 @@
+// Host-side preparation of the device mesh.  See tsg_prep.hpp.
+#include "tsg_prep.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <thread>
+
+namespace tsg {
+
+namespace {
+
+uint32_t fan_pack_h(uint32_t i1, uint32_t i2, uint32_t k) { return i1 | (i2 << 15) | (k << 30); }
+
+int worker_count(int64_t n) {
+  const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t by_size = n / 65536 + 1;
+  return static_cast<int>(std::min<int64_t>(std::min<unsigned>(hc, 64u), by_size));
+}
+
+// Contiguous static split of [0, n) over threads; fn(begin, end).
+template <class F>
+void parallel_ranges(int64_t n, F&& fn) {
+  const int T = worker_count(n);
+  if (T <= 1) {
+    fn(int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t step = (n + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    const int64_t b = std::min<int64_t>(n, t * step), e = std::min<int64_t>(n, b + step);
+    th.emplace_back([&fn, b, e] { fn(b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// Sorts 64-bit keys in parallel: per-thread std::sort, then pairwise merges.
+void parallel_sort(std::vector<uint64_t>& keys) {
+  const int64_t n = static_cast<int64_t>(keys.size());
+  int T = worker_count(n);
+  int P = 1;
+  while (P * 2 <= T) P *= 2;
+  if (P <= 1) {
+    std::sort(keys.begin(), keys.end());
+    return;
+  }
+  std::vector<int64_t> cut(P + 1);
+  for (int i = 0; i <= P; ++i) cut[i] = n * i / P;
+  {
+    std::vector<std::thread> th;
+    for (int i = 0; i < P; ++i)
+      th.emplace_back([&, i] { std::sort(keys.begin() + cut[i], keys.begin() + cut[i + 1]); });
+    for (auto& x : th) x.join();
+  }
+  for (int width = 1; width < P; width *= 2) {
+    std::vector<std::thread> th;
+    for (int i = 0; i + width < P; i += 2 * width) {
+      const int64_t b = cut[i], m = cut[i + width], e = cut[std::min(i + 2 * width, P)];
+      th.emplace_back([&keys, b, m, e] {
+        std::inplace_merge(keys.begin() + b, keys.begin() + m, keys.begin() + e);
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+}
+
+// Hilbert index of (x, y) on a 2^16 x 2^16 lattice.
+uint32_t hilbert_d(uint32_t x, uint32_t y) {
+  uint32_t d = 0;
+  for (uint32_t s = 1u << 15; s > 0; s >>= 1) {
+    const uint32_t rx = (x & s) ? 1u : 0u, ry = (y & s) ? 1u : 0u;
+    d += s * s * ((3u * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = 0xffffu - x;
+        y = 0xffffu - y;
+      }
+      std::swap(x, y);
+    }
+  }
+  return d;
+}
+
+}  // namespace
+
+void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
+  double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+  for (int64_t v = 0; v < nv; ++v) {
+    xmin = std::min(xmin, xy[2 * v]);
+    xmax = std::max(xmax, xy[2 * v]);
+    ymin = std::min(ymin, xy[2 * v + 1]);
+    ymax = std::max(ymax, xy[2 * v + 1]);
+  }
+  const double sx = xmax > xmin ? 65535.0 / (xmax - xmin) : 0.0;
+  const double sy = ymax > ymin ? 65535.0 / (ymax - ymin) : 0.0;
+  std::vector<uint64_t> keys(static_cast<size_t>(nv));
+  parallel_ranges(nv, [&](int64_t b, int64_t e) {
+    for (int64_t v = b; v < e; ++v) {
+      const double fx = std::isfinite(xy[2 * v]) ? (xy[2 * v] - xmin) * sx : 0.0;
+      const double fy = std::isfinite(xy[2 * v + 1]) ? (xy[2 * v + 1] - ymin) * sy : 0.0;
+      const uint32_t qx = static_cast<uint32_t>(std::clamp(fx, 0.0, 65535.0));
+      const uint32_t qy = static_cast<uint32_t>(std::clamp(fy, 0.0, 65535.0));
+      keys[v] = (static_cast<uint64_t>(hilbert_d(qx, qy)) << 32) | static_cast<uint64_t>(v);
+    }
+  });
+  parallel_sort(keys);
+  for (int64_t s = 0; s < nv; ++s) order_out[s] = static_cast<int64_t>(keys[s] & 0xffffffffu);
+}
+
+std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostMesh& hm) {
+  const int64_t nv = d.nv, nt = d.nt;
+  if (nv <= 0 || nt <= 0) return "mesh must have vertices and triangles";
+  if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
+  hm.nv = nv;
+  hm.nt = nt;
+  hm.order.resize(nv);
+  hm.rank.resize(nv);
+  if (d.order) {
+    std::vector<uint8_t> seen(nv, 0);
+    for (int64_t s = 0; s < nv; ++s) {
+      const int64_t v = d.order[s];
+      if (v < 0 || v >= nv || seen[v]) return "order is not a permutation of 0..nv-1";
+      seen[v] = 1;
+      hm.order[s] = v;
+      hm.rank[v] = s;
+    }
+  } else {
+    for (int64_t s = 0; s < nv; ++s) hm.order[s] = hm.rank[s] = s;
+  }
+
+  // Row lengths: movable vertices only; interior (all multiplicities 2) implies
+  // #incident == #unique neighbours, which the fan encoding relies on.
+  std::vector<uint32_t> deg(nv, 0);
+  std::atomic<int64_t> bad{-1};
+  std::atomic<int32_t> maxdeg{0};
+  parallel_ranges(nv, [&](int64_t b, int64_t e) {
+    int32_t local_max = 0;
+    for (int64_t s = b; s < e; ++s) {
+      const int64_t v = hm.order[s];
+      if (d.boundary[v]) continue;
+      const int64_t dn = d.nbr_off[v + 1] - d.nbr_off[v];
+      const int64_t di = d.inc_off[v + 1] - d.inc_off[v];
+      if (dn != di || dn <= 0 || dn >= 32768) bad = v;
+      deg[s] = static_cast<uint32_t>(dn);
+      local_max = std::max<int32_t>(local_max, static_cast<int32_t>(dn));
+    }
+    int32_t cur = maxdeg.load();
+    while (local_max > cur && !maxdeg.compare_exchange_weak(cur, local_max)) {
+    }
+  });
+  if (bad >= 0)
+    return "movable vertex " + std::to_string(bad.load()) +
+           " has inconsistent neighbour / incident counts (or degree >= 32768)";
+  hm.max_deg = maxdeg;
+  hm.off.assign(nv + 1, 0);
+  uint64_t total = 0;
+  for (int64_t s = 0; s < nv; ++s) {
+    hm.off[s] = static_cast<uint32_t>(total);
+    total += deg[s];
+    if (total >= 0xffffffffULL) return "adjacency exceeds 2^32 entries";
+  }
+  hm.off[nv] = static_cast<uint32_t>(total);
+  hm.nbr.assign(total, 0);
+  hm.fan.assign(total, 0);
+
+  // Device triangle order: identity, or by the smallest slot among the corners (stable) so
+  // that the triangle kernels stream coordinates in the same locality order as the vertices.
+  hm.tri_order.resize(nt);
+  std::vector<int64_t> tri_rank(nt);
+  if (!d.order) {
+    for (int64_t t = 0; t < nt; ++t) hm.tri_order[t] = tri_rank[t] = t;
+  } else {
+    std::vector<uint64_t> keys(nt);
+    parallel_ranges(nt, [&](int64_t b, int64_t e) {
+      for (int64_t t = b; t < e; ++t) {
+        const int64_t m = std::min({hm.rank[d.tri[3 * t]], hm.rank[d.tri[3 * t + 1]],
+                                    hm.rank[d.tri[3 * t + 2]]});
+        keys[t] = (static_cast<uint64_t>(m) << 32) | static_cast<uint64_t>(t);
+      }
+    });
+    if (nt >= (int64_t{1} << 32)) return "triangle count exceeds 2^32";
+    parallel_sort(keys);
+    for (int64_t i = 0; i < nt; ++i) {
+      hm.tri_order[i] = static_cast<int64_t>(keys[i] & 0xffffffffu);
+      tri_rank[hm.tri_order[i]] = i;
+    }
+  }
+  hm.tri.resize(3 * nt);
+  parallel_ranges(nt, [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i) {
+      const int64_t t = hm.tri_order[i];
+      for (int k = 0; k < 3; ++k) hm.tri[3 * i + k] = static_cast<int32_t>(hm.rank[d.tri[3 * t + k]]);
+    }
+  });
+
+  std::atomic<int64_t> broken{-1};
+  parallel_ranges(nv, [&](int64_t b, int64_t e) {
+    for (int64_t s = b; s < e; ++s) {
+      if (deg[s] == 0) continue;
+      const int64_t v = hm.order[s];
+      const int32_t* row = d.nbr + d.nbr_off[v];
+      const int32_t n = static_cast<int32_t>(deg[s]);
+      uint32_t* out_n = hm.nbr.data() + hm.off[s];
+      uint32_t* out_f = hm.fan.data() + hm.off[s];
+      for (int32_t j = 0; j < n; ++j) out_n[j] = static_cast<uint32_t>(hm.rank[row[j]]);
+      for (int64_t i = d.inc_off[v], j = 0; i < d.inc_off[v + 1]; ++i, ++j) {
+        const int32_t* tv = d.tri + 3 * static_cast<int64_t>(d.inc[i]);
+        const int k = tv[0] == v ? 0 : tv[1] == v ? 1 : 2;
+        const int32_t a = tv[(k + 1) % 3], c = tv[(k + 2) % 3];
+        const int32_t* pa = std::lower_bound(row, row + n, a);
+        const int32_t* pc = std::lower_bound(row, row + n, c);
+        if (tv[k] != v || pa == row + n || *pa != a || pc == row + n || *pc != c) {
+          broken = v;
+          return;
+        }
+        out_f[j] = fan_pack_h(static_cast<uint32_t>(pa - row), static_cast<uint32_t>(pc - row),
+                              static_cast<uint32_t>(k));
+      }
+    }
+  });
+  if (broken >= 0) return "incident / neighbour lists disagree at vertex " + std::to_string(broken.load());
+
+  // Full incident CSR (all vertices) for TwoPhase thresholds and vertex minima.
+  hm.vinc_off.assign(nv + 1, 0);
+  uint64_t it = 0;
+  for (int64_t s = 0; s < nv; ++s) {
+    hm.vinc_off[s] = static_cast<uint32_t>(it);
+    const int64_t v = hm.order[s];
+    it += static_cast<uint64_t>(d.inc_off[v + 1] - d.inc_off[v]);
+    if (it >= 0xffffffffULL) return "incidence exceeds 2^32 entries";
+  }
+  hm.vinc_off[nv] = static_cast<uint32_t>(it);
+  hm.vinc.resize(it);
+  parallel_ranges(nv, [&](int64_t b, int64_t e) {
+    for (int64_t s = b; s < e; ++s) {
+      const int64_t v = hm.order[s];
+      uint32_t* out = hm.vinc.data() + hm.vinc_off[s];
+      int64_t j = 0;
+      for (int64_t i = d.inc_off[v]; i < d.inc_off[v + 1]; ++i)
+        out[j++] = static_cast<uint32_t>(tri_rank[d.inc[i]]);
+      std::sort(out, out + j);
+    }
+  });
+
+  hm.hubs.clear();
+  for (int64_t s = 0; s < nv; ++s)
+    if (deg[s] > static_cast<uint32_t>(max_small_deg)) hm.hubs.push_back(static_cast<int32_t>(s));
+  return "";
+}
+
+std::string build_form_b(const HostMesh& hm, int32_t chunks, int32_t max_small_deg,
+                         FormBSchedule& out) {
+  const int64_t nv = hm.nv;
+  if (chunks < 1) return "chunks must be >= 1";
+  const int64_t k = (nv + chunks - 1) / chunks;  // worker_chunk: ceil(n / workers)
+  out.chunks = chunks;
+  out.nbr_fresh = hm.nbr;
+  std::vector<int32_t> level(nv, -1);  // by ORIGINAL id
+  int32_t nlev = 0;
+  // Forward sweep in original id order: every dependency has a smaller id.
+  for (int64_t v = 0; v < nv; ++v) {
+    const int64_t s = hm.rank[v];
+    const uint32_t o0 = hm.off[s], o1 = hm.off[s + 1];
+    if (o0 == o1) continue;  // pinned
+    int32_t L = 0;
+    const int64_t cv = v / k;
+    for (uint32_t j = o0; j < o1; ++j) {
+      const uint32_t us = hm.nbr[j];
+      const int64_t u = hm.order[us];
+      if (u < v && u / k == cv) {
+        out.nbr_fresh[j] |= 0x80000000u;
+        if (level[u] >= 0) L = std::max(L, level[u] + 1);
+      }
+    }
+    level[v] = L;
+    nlev = std::max(nlev, L + 1);
+  }
+  std::vector<int64_t> small_cnt(nlev + 1, 0), hub_cnt(nlev + 1, 0);
+  for (int64_t s = 0; s < nv; ++s) {
+    const int32_t L = level[hm.order[s]];
+    if (L < 0) continue;
+    const uint32_t dg = hm.off[s + 1] - hm.off[s];
+    if (dg > static_cast<uint32_t>(max_small_deg))
+      ++hub_cnt[L + 1];
+    else
+      ++small_cnt[L + 1];
+  }
+  for (int32_t L = 0; L < nlev; ++L) {
+    small_cnt[L + 1] += small_cnt[L];
+    hub_cnt[L + 1] += hub_cnt[L];
+  }
+  out.nodes.assign(small_cnt[nlev], 0);
+  out.hubs.assign(hub_cnt[nlev], 0);
+  std::vector<int64_t> sf(small_cnt.begin(), small_cnt.end() - 1), hf(hub_cnt.begin(), hub_cnt.end() - 1);
+  for (int64_t s = 0; s < nv; ++s) {  // slot-ascending inside each level
+    const int32_t L = level[hm.order[s]];
+    if (L < 0) continue;
+    const uint32_t dg = hm.off[s + 1] - hm.off[s];
+    if (dg > static_cast<uint32_t>(max_small_deg))
+      out.hubs[hf[L]++] = static_cast<int32_t>(s);
+    else
+      out.nodes[sf[L]++] = static_cast<int32_t>(s);
+  }
+  out.levels.resize(nlev);
+  for (int32_t L = 0; L < nlev; ++L) {
+    out.levels[L].small_begin = small_cnt[L];
+    out.levels[L].small_count = small_cnt[L + 1] - small_cnt[L];
+    out.levels[L].hub_begin = hub_cnt[L];
+    out.levels[L].hub_count = hub_cnt[L + 1] - hub_cnt[L];
+  }
+  return "";
+}
+
+}  // namespace tsg

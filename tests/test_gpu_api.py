@@ -1,0 +1,86 @@
+"""The drop-in Python API on the GPU: the reference's smoke tests for smooth()
+(proj/tests/python/test_smoke.py:35-59) plus full write-back parity of trismooth.smooth() —
+coordinates, boundary flags, triangle alpha field, vertex minima and RunStats — against the
+reference's golden outputs."""
+import numpy as np
+import pytest
+
+import trismooth as ts
+from helpers import sha
+
+pytestmark = pytest.mark.gpu
+
+
+def test_smooth_improves_quality():
+    m = ts.generate_grid(20, 20, perturbation=0.3, seed=3)
+    stats = ts.smooth(m, form="b", strategy="twophase", backend="serial")
+    assert stats["iterations"] >= 1
+    assert stats["stop"] in ("max_iters", "displacement", "no_moves")
+    assert stats["mean_alpha_after"] > stats["mean_alpha_before"]
+    assert stats["min_alpha_after"] >= stats["min_alpha_before"]
+    assert len(stats["accepted_per_pass"]) == stats["iterations"]
+    assert stats["total_ms"] >= stats["iter_ms"]
+
+
+def test_smooth_keeps_boundary_fixed():
+    m = ts.generate_grid(8, 8, perturbation=0.25, seed=11)
+    before = m.points()
+    boundary = m.boundary()
+    ts.smooth(m, max_iters=5)
+    after = m.points()
+    flags = m.boundary()
+    assert any(not f for f in flags)
+    assert sum(1 for i in range(len(after)) if after[i] != before[i]) > 0
+    for i, pinned in enumerate(flags):
+        if pinned:
+            assert after[i] == before[i]
+    assert len(boundary) == len(flags)
+
+
+@pytest.mark.parametrize("name", ["grid100_defaults", "d10k_formB_w8_soa_tol0", "d10k_formA_serial_conv",
+                                  "d10k_formB_w3_fused", "grid12_formB_loose"])
+@pytest.mark.parametrize("precision_layout", ["as_case", "other_layout"])
+def test_drop_in_smooth_write_back(golden, name, precision_layout):
+    case = golden["cases"][name]
+    kw = dict(case["smooth"])
+    layout = kw.pop("layout", "aos")
+    if precision_layout == "other_layout":
+        layout = "soa" if layout == "aos" else "aos"
+    if case["kind"] == "grid":
+        m = ts.generate_grid(*case["args"][:2], perturbation=case["args"][2], seed=case["args"][3], layout=layout)
+    else:
+        m = ts.generate_delaunay(case["args"][0], seed=case["args"][1], layout=layout)
+    s = ts.smooth(m, **kw, detailed=True)
+    assert s["iterations"] == case["iterations"] and s["stop"] == case["stop"]
+    assert s["accepted_per_pass"] == case["accepted"]
+    assert [float(x).hex() for x in s["max_disp_per_pass"]] == case["max_disp"]
+    assert sha(m.points_array()) == case["xy_out"]
+    assert sha(m.tri_alphas()) == case["tri_alpha"]
+    assert sha(m.vertex_minima()) == case["vertex_min"]
+    assert sha(np.array(m.boundary(), dtype=np.uint8)) == case["boundary"]
+    for k in ("min_alpha_before", "min_alpha_after", "mean_alpha_before", "mean_alpha_after"):
+        assert float(s[k]).hex() == case[k], k
+
+
+def test_drop_in_formA_reorder_auto_on_large_mesh(golden):
+    case = golden["cases"]["d100k_formA_20"]
+    m = ts.generate_delaunay(100000, seed=42)
+    s = ts.smooth(m, form="a", max_iters=20, move_tol=0.0, reorder="auto", detailed=True)
+    assert s["accepted_per_pass"] == case["accepted"]
+    assert sha(m.points_array()) == case["xy_out"]
+    assert sha(m.vertex_minima()) == case["vertex_min"]
+
+
+def test_f32_drop_in_runs_and_improves():
+    m = ts.generate_delaunay(20000, seed=3)
+    s = ts.smooth(m, form="a", precision="f32", max_iters=50, move_tol=0.0)
+    assert s["mean_alpha_after"] > s["mean_alpha_before"]
+
+
+def test_device_mesh_class_round_trip():
+    xy, tri = ts.delaunay_arrays(5000, 9)
+    topo = ts.topology(len(xy), tri)
+    dm = ts.DeviceMesh(xy, tri, topo, "soa", "f64", True)
+    assert np.array_equal(dm.get_coords(), xy)
+    r = dm.run(ts.bbox_diagonal(xy), form="a", max_iters=10)
+    assert r["iterations"] == 10 and len(r["max_disp_per_pass"]) == 10
