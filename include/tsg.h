@@ -116,6 +116,9 @@ int64_t tsg_mesh_device_bytes(const tsg_mesh* mesh);
 /* Coordinates in ORIGINAL numbering (2*nv doubles; f32 meshes round on upload). */
 tsg_status tsg_mesh_set_coords(tsg_mesh* mesh, const double* xy);
 tsg_status tsg_mesh_get_coords(tsg_mesh* mesh, double* xy_out);
+/* Device-side reset to the coordinates of the last upload / set_coords (no host traffic;
+ * asynchronous on the context stream).  Benchmarks restart every step from the same mesh. */
+tsg_status tsg_mesh_restore_coords(tsg_mesh* mesh);
 
 /* ---- quality (device) ---- */
 /* alpha_out: nt doubles in original triangle order (compute_all_qualities). */

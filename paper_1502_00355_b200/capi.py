@@ -28,7 +28,8 @@ STOP = ("max_iters", "displacement", "no_moves")
 EXPORTS = (
     "tsg_abi_version", "tsg_last_error", "tsg_device_count", "tsg_context_create",
     "tsg_context_destroy", "tsg_context_stream", "tsg_mesh_upload", "tsg_mesh_free",
-    "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_tri_alpha",
+    "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_mesh_restore_coords",
+    "tsg_tri_alpha",
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
     "tsg_pass_lockstep", "tsg_hilbert_order",
 )
@@ -74,6 +75,7 @@ def lib() -> C.CDLL:
             "tsg_mesh_device_bytes": (i64, [P]),
             "tsg_mesh_set_coords": (i32, [P, P]),
             "tsg_mesh_get_coords": (i32, [P, P]),
+            "tsg_mesh_restore_coords": (i32, [P]),
             "tsg_tri_alpha": (i32, [P, P]),
             "tsg_vertex_minima": (i32, [P, P]),
             "tsg_alpha_extrema": (i32, [P, P, P, P]),
@@ -171,6 +173,9 @@ class DeviceMesh:
     def set_coords(self, xy):
         xy = np.ascontiguousarray(xy, dtype=np.float64)
         check(lib().tsg_mesh_set_coords(self.h, _ptr(xy)), "tsg_mesh_set_coords")
+
+    def restore_coords(self):
+        check(lib().tsg_mesh_restore_coords(self.h), "tsg_mesh_restore_coords")
 
     def get_coords(self) -> np.ndarray:
         out = np.empty((self.nv, 2))

@@ -135,6 +135,7 @@ struct tsg_mesh {
   size_t rsize = 8;
   int64_t bytes = 0;
   void* buf[2] = {nullptr, nullptr};
+  void* init = nullptr;  // slot-ordered copy of the coordinates given at upload / set_coords
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
   int32_t *d_tri = nullptr, *d_hubs = nullptr;
@@ -317,6 +318,7 @@ struct Engine {
                                                                 coords_of<R, kSoA>(m, 0),
                                                                 coords_of<R, kSoA>(m, 1));
     TSG_CUDA(cudaGetLastError());
+    TSG_CUDA(cudaMemcpyAsync(m->init, m->buf[0], 2 * nv * sizeof(R), cudaMemcpyDeviceToDevice, s));
     m->cur = 0;
     return TSG_OK;
   }
@@ -463,8 +465,8 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   cudaStream_t s = ctx->stream;
   int64_t* b = &m->bytes;
   tsg_status st;
-  for (int i = 0; i < 2; ++i) {
-    TSG_CUDA(cudaMalloc(&m->buf[i], 2 * nv * m->rsize));
+  for (void** p : {&m->buf[0], &m->buf[1], &m->init}) {
+    TSG_CUDA(cudaMalloc(p, 2 * nv * m->rsize));
     *b += 2 * nv * m->rsize;
   }
   if ((st = upload(&m->d_off, hm.off, b, s))) return st;
@@ -502,7 +504,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
   free_form_b(m);
-  void* ptrs[] = {m->buf[0], m->buf[1], m->d_off, m->d_nbr, m->d_fan, m->d_vinc_off, m->d_vinc,
+  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md,
                   m->d_ext};
@@ -519,6 +521,16 @@ tsg_status tsg_mesh_set_coords(tsg_mesh* m, const double* xy) {
   tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::set_coords(m, xy); });
   if (st) return st;
   TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_restore_coords(tsg_mesh* m) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  const size_t bytes = 2 * m->hm.nv * m->rsize;
+  TSG_CUDA(cudaMemcpyAsync(m->buf[0], m->init, bytes, cudaMemcpyDeviceToDevice, m->ctx->stream));
+  TSG_CUDA(cudaMemcpyAsync(m->buf[1], m->init, bytes, cudaMemcpyDeviceToDevice, m->ctx->stream));
+  m->cur = 0;
   return TSG_OK;
 }
 
