@@ -121,6 +121,38 @@ __device__ __forceinline__ R alpha_plain(R x1, R y1, R x2, R y2, R x3, R y3) {
   return O::div(O::mul(Arith<R>::kAlpha, ta), es);
 }
 
+// Reciprocal for the fast α path: the SFU estimate refined by two Newton steps
+// (relative error ~2^-52; FMA is fine here, the value is only compared against a guard band).
+__device__ __forceinline__ double rcp_refined(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ float rcp_refined(float x) { return __frcp_rn(x); }
+
+// Decisions whose fast-path margin is within kGuard (absolute; |α| <= 1) are settled exactly.
+constexpr double kGuard = 0x1p-40;
+
+// triangle_alpha with the division replaced by the refined reciprocal; everything before the
+// division is the reference's exact operation sequence.  es == 0 gives exactly 0.
+template <typename R>
+__device__ __forceinline__ R alpha_fast(R x1, R y1, R x2, R y2, R x3, R y3) {
+  using O = Arith<R>;
+  const R ax = O::sub(x2, x1), ay = O::sub(y2, y1);
+  const R bx = O::sub(x3, x1), by = O::sub(y3, y1);
+  const R cx = O::sub(x3, x2), cy = O::sub(y3, y2);
+  const R ta = O::sub(O::mul(ax, by), O::mul(ay, bx));
+  const R es = O::add(O::add(O::add(O::add(O::add(O::mul(ax, ax), O::mul(ay, ay)), O::mul(bx, bx)),
+                                    O::mul(by, by)),
+                             O::mul(cx, cx)),
+                      O::mul(cy, cy));
+  const R q = O::mul(O::mul(Arith<R>::kAlpha, ta), rcp_refined(es));
+  return es == R(0) ? R(0) : q;
+}
+
 // std::min(best, x) (== x < best ? x : best), NaN-compatible with the reference.
 template <typename R>
 __device__ __forceinline__ R min_ref(R best, R x) {
@@ -134,6 +166,8 @@ __host__ __device__ __forceinline__ uint32_t fan_pack(uint32_t i1, uint32_t i2, 
 __device__ __forceinline__ uint32_t fan_i1(uint32_t f) { return f & 0x7fffu; }
 __device__ __forceinline__ uint32_t fan_i2(uint32_t f) { return (f >> 15) & 0x7fffu; }
 __device__ __forceinline__ int fan_k(uint32_t f) { return static_cast<int>(f >> 30); }
+// Small-vertex fan record: ring positions of p1, p2, p3 (5 bits each; kMaxDeg = v itself).
+__device__ __forceinline__ uint32_t fan_p(uint32_t f, int c) { return (f >> (5 * c)) & 31u; }
 
 constexpr uint32_t kFreshBit = 0x80000000u;  // Form B: read this neighbour from N (live)
 

@@ -98,6 +98,40 @@ __global__ void scatter_i8(const int8_t* __restrict__ in, const int64_t* __restr
     out[order ? order[i] : i] = in[i];
 }
 
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void selftest_alpha(int64_t n, uint64_t seed, unsigned long long* max_err,
+                               unsigned long long* nonfinite) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double c[6];
+    const uint64_t h = mix64(seed ^ static_cast<uint64_t>(i));
+    const double scale = __longlong_as_double(static_cast<long long>((1023ULL + (h % 61) - 30) << 52));
+    for (int k = 0; k < 6; ++k)
+      c[k] = (static_cast<double>(mix64(h + 7 * k + 1) >> 11) * 0x1.0p-53 - 0.5) * scale;
+    if ((h >> 60) == 0) {  // near-degenerate: third corner almost on the first edge
+      const double t = static_cast<double>(mix64(h + 99) >> 11) * 0x1.0p-53;
+      c[4] = c[0] + t * (c[2] - c[0]) + 1e-9 * scale;
+      c[5] = c[1] + t * (c[3] - c[1]);
+    }
+    const double e = tsg::alpha_plain<double>(c[0], c[1], c[2], c[3], c[4], c[5]);
+    const double f = tsg::alpha_fast<double>(c[0], c[1], c[2], c[3], c[4], c[5]);
+    if (!(fabs(f) <= 2.0)) {
+      atomicAdd(nonfinite, 1ULL);
+      continue;
+    }
+    if (fabs(e) <= 1.0) {
+      const double d = fabs(f - e);
+      atomicMax(max_err, static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
+  }
+}
+
 unsigned grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64)));
@@ -441,6 +475,24 @@ void* tsg_context_stream(tsg_context* ctx) { return ctx ? static_cast<void*>(ctx
 tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
   if (nv < 0 || (nv > 0 && (!xy || !order_out))) return fail(TSG_ERR_INVALID, "bad arguments");
   tsg::hilbert_order(nv, xy, order_out);
+  return TSG_OK;
+}
+
+tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, double* max_abs_err_out,
+                              int64_t* nonfinite_out) {
+  if (!ctx || n < 0) return fail(TSG_ERR_INVALID, "bad arguments");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  unsigned long long* d = nullptr;
+  TSG_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+  TSG_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  selftest_alpha<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, seed, d, d + 1);
+  TSG_CUDA(cudaGetLastError());
+  unsigned long long h[2];
+  TSG_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d);
+  if (max_abs_err_out) std::memcpy(max_abs_err_out, &h[0], sizeof(double));
+  if (nonfinite_out) *nonfinite_out = static_cast<int64_t>(h[1]);
   return TSG_OK;
 }
 

@@ -84,14 +84,24 @@ __device__ __forceinline__ void commit_stats(int accepted, double disp, int32_t*
   }
 }
 
-// Thread-per-vertex node update.  Shared memory: kMaxDeg x kNodeBlock coordinate pairs,
-// entry-major so that lane t of every warp hits bank group t regardless of the entry it
-// reads (the fan indexes entries at random).
+// Thread-per-vertex node update.  Shared memory: (kMaxDeg + 1) x kNodeBlock coordinate pairs,
+// entry-major so that lane t of every warp hits bank group t regardless of the entry it reads
+// (the fan indexes entries at random).  Entry kMaxDeg is v itself: the pass-start position for
+// the threshold, the candidate for the hypothetical.  A small-vertex fan record holds the ring
+// positions of (p1, p2, p3) of the triangle (5 bits each), so every α is the literal
+// triangle_alpha(p1, p2, p3) with no per-triangle branching.
+//
+// fp64 decisions are exact but division-light: α is first evaluated with a refined
+// reciprocal (|error| < 2^-50 on |α| <= 1); the strict test hyp > thr is settled from those
+// values whenever they are more than kGuard apart, and otherwise (rare: near-ties) every α of
+// the vertex is re-evaluated with IEEE division, exactly as the reference (quality.hpp:15-23).
 template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg>
 __global__ void __launch_bounds__(kNodeBlock) node_update(PassArgs<R, kSoA> a) {
   using O = Arith<R>;
   using R2 = typename O::R2;
-  __shared__ R2 ring[kMaxDeg * kNodeBlock];
+  constexpr int kSelf = kMaxDeg;
+  constexpr bool kExact = sizeof(R) == 8;
+  __shared__ R2 ring[(kMaxDeg + 1) * kNodeBlock];
   const PassState* st = a.st;
   if (st->done) return;
   const int pass = st->pass;
@@ -137,68 +147,83 @@ __global__ void __launch_bounds__(kNodeBlock) node_update(PassArgs<R, kSoA> a) {
           }
         }
       }
+      auto at = [&](uint32_t idx) -> R2 { return ring[idx * kNodeBlock + tid]; };
+      bool bad = false;  // an approximation is not finite: settle exactly
 
+      // Threshold: pass-start minimum incident α (TwoPhase: the stored field, already exact).
+      ring[kSelf * kNodeBlock + tid] = pv;
       R thr = R(INFINITY);
       if constexpr (kTwoPhase) {
         const uint32_t t0 = a.vinc_off[s], t1 = a.vinc_off[s + 1];
         for (uint32_t t = t0; t < t1; ++t) thr = min_ref(thr, a.alpha[a.vinc[t]]);
-      }
-      R hyp = R(INFINITY);
-      R2 cand;
-      if constexpr (!kFormB && !kTwoPhase) {
-        // Form A, fused: threshold and hypothetical share the rim edge b - a.
-        const R inv = O::div(R(1), static_cast<R>(deg));
-        cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+      } else {
         for (int j = 0; j < deg; ++j) {
           const uint32_t f = __ldg(fan + j);
-          const R2 pa = ring[fan_i1(f) * kNodeBlock + tid];
-          const R2 pb = ring[fan_i2(f) * kNodeBlock + tid];
-          const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
-          const R sabx = O::mul(dabx, dabx), saby = O::mul(daby, daby);
-          const int k = fan_k(f);
-          thr = min_ref(thr, alpha_at<R>(k, pv.x, pv.y, pa.x, pa.y, pb.x, pb.y, dabx, daby, sabx, saby));
-          hyp = min_ref(hyp, alpha_at<R>(k, cand.x, cand.y, pa.x, pa.y, pb.x, pb.y, dabx, daby, sabx, saby));
+          const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
+          const R q = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y);
+          bad |= !(fabs(q) <= R(2));
+          thr = min_ref(thr, q);
         }
+      }
+      if constexpr (kFormB) {
+        // ChunkView (quality.hpp:40-50): in-chunk lower-id neighbours read this pass's values.
+        uint32_t m = fresh;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          ring[j * kNodeBlock + tid] = N.load_mut(nb[j] & ~kFreshBit);
+        }
+        for (int j = 0; j < deg; ++j) {
+          const R2 c = at(j);
+          sx = O::add(sx, c.x);
+          sy = O::add(sy, c.y);
+        }
+      }
+      const R inv = O::div(R(1), static_cast<R>(deg));  // 1.0 / deg (smoothing.hpp:78)
+      const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+      ring[kSelf * kNodeBlock + tid] = cand;
+      // Hypothetical minimum with early rejection once one triangle is surely <= thr.
+      R hyp = R(INFINITY);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = __ldg(fan + j);
+        const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
+        const R q = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y);
+        bad |= !(fabs(q) <= R(2));
+        hyp = min_ref(hyp, q);
+        if (kExact && hyp < thr - R(kGuard)) break;
+      }
+      bool acc;
+      if constexpr (!kExact) {
+        acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
+      } else if (!bad && hyp > thr + R(kGuard)) {
+        acc = true;
+      } else if (!bad && hyp < thr - R(kGuard)) {
+        acc = false;
       } else {
+        // Near-tie: the reference's exact values (IEEE division), same operand order.
+        R thr_e = thr;
         if constexpr (!kTwoPhase) {
-          // Fused threshold from pass-start positions (Form B: before fresh reads patch in).
+          thr_e = R(INFINITY);
           for (int j = 0; j < deg; ++j) {
             const uint32_t f = __ldg(fan + j);
-            const R2 pa = ring[fan_i1(f) * kNodeBlock + tid];
-            const R2 pb = ring[fan_i2(f) * kNodeBlock + tid];
-            const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
-            thr = min_ref(thr, alpha_at<R>(fan_k(f), pv.x, pv.y, pa.x, pa.y, pb.x, pb.y, dabx, daby,
-                                           O::mul(dabx, dabx), O::mul(daby, daby)));
+            R2 q[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const uint32_t idx = fan_p(f, c);
+              q[c] = idx == kSelf ? pv
+                     : (kFormB && ((fresh >> idx) & 1u)) ? P.load(nb[idx] & ~kFreshBit) : at(idx);
+            }
+            thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
           }
         }
-        if constexpr (kFormB) {
-          // ChunkView (quality.hpp:40-50): in-chunk lower-id neighbours read this pass's values.
-          while (fresh) {
-            const int j = __ffs(fresh) - 1;
-            fresh &= fresh - 1;
-            ring[j * kNodeBlock + tid] = N.load_mut(nb[j] & ~kFreshBit);
-          }
-          for (int j = 0; j < deg; ++j) {
-            const R2 c = ring[j * kNodeBlock + tid];
-            sx = O::add(sx, c.x);
-            sy = O::add(sy, c.y);
-          }
-        }
-        const R inv = O::div(R(1), static_cast<R>(deg));
-        cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-        // Hypothetical min with early rejection: once one triangle falls to <= thr the
-        // strict test (smoothing.hpp:99) cannot pass.
+        R hyp_e = R(INFINITY);
         for (int j = 0; j < deg; ++j) {
           const uint32_t f = __ldg(fan + j);
-          const R2 pa = ring[fan_i1(f) * kNodeBlock + tid];
-          const R2 pb = ring[fan_i2(f) * kNodeBlock + tid];
-          const R dabx = O::sub(pb.x, pa.x), daby = O::sub(pb.y, pa.y);
-          hyp = min_ref(hyp, alpha_at<R>(fan_k(f), cand.x, cand.y, pa.x, pa.y, pb.x, pb.y, dabx, daby,
-                                         O::mul(dabx, dabx), O::mul(daby, daby)));
-          if (!(hyp > thr)) break;
+          const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
+          hyp_e = min_ref(hyp_e, alpha_plain<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
         }
+        acc = hyp_e > thr_e;
       }
-      const bool acc = hyp > thr;
       N.store(s, acc ? cand : pv);
       if (acc) {
         accepted = 1;

@@ -123,8 +123,22 @@ std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostM
       if (v < 0 || v >= nv || seen[v]) return "order is not a permutation of 0..nv-1";
       seen[v] = 1;
       hm.order[s] = v;
-      hm.rank[v] = s;
     }
+    // Degree sort inside windows of kSigma consecutive slots of the locality order (SELL-C-σ
+    // style): warps then see near-uniform valences (no divergent loop tails) while every
+    // window stays spatially compact.  Results do not depend on the slot order.
+    constexpr int64_t kSigma = 1024;
+    auto degree_key = [&](int64_t v) -> int64_t {
+      return d.boundary[v] ? 0 : d.nbr_off[v + 1] - d.nbr_off[v];
+    };
+    parallel_ranges((nv + kSigma - 1) / kSigma, [&](int64_t b, int64_t e) {
+      for (int64_t w = b; w < e; ++w) {
+        auto first = hm.order.begin() + w * kSigma;
+        auto last = hm.order.begin() + std::min(nv, (w + 1) * kSigma);
+        std::stable_sort(first, last, [&](int64_t x, int64_t y) { return degree_key(x) < degree_key(y); });
+      }
+    });
+    for (int64_t s = 0; s < nv; ++s) hm.rank[hm.order[s]] = s;
   } else {
     for (int64_t s = 0; s < nv; ++s) hm.order[s] = hm.rank[s] = s;
   }
@@ -214,8 +228,17 @@ std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostM
           broken = v;
           return;
         }
-        out_f[j] = fan_pack_h(static_cast<uint32_t>(pa - row), static_cast<uint32_t>(pc - row),
-                              static_cast<uint32_t>(k));
+        const uint32_t ia = static_cast<uint32_t>(pa - row), ic = static_cast<uint32_t>(pc - row);
+        if (n <= max_small_deg) {
+          // ring positions of (p1, p2, p3); v itself is ring entry max_small_deg
+          uint32_t p[3];
+          p[k] = static_cast<uint32_t>(max_small_deg);
+          p[(k + 1) % 3] = ia;
+          p[(k + 2) % 3] = ic;
+          out_f[j] = p[0] | (p[1] << 5) | (p[2] << 10);
+        } else {
+          out_f[j] = fan_pack_h(ia, ic, static_cast<uint32_t>(k));
+        }
       }
     }
   });
