@@ -83,7 +83,7 @@ def lib() -> C.CDLL:
             "tsg_smooth_host": (i32, [P, P, C.POINTER(SmoothCfg), P, C.POINTER(SmoothStats), P, P, i32]),
             "tsg_pass_lockstep": (i32, [P, i32, i32, P, P, P]),
             "tsg_hilbert_order": (i32, [i64, P, P]),
-            "tsg_selftest_alpha": (i32, [P, i64, C.c_uint64, P, P]),
+            "tsg_selftest_alpha": (i32, [P, i64, C.c_uint64, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -118,9 +118,10 @@ class Context:
     def stream(self) -> int:
         return lib().tsg_context_stream(self.h) or 0
 
-    def selftest_alpha(self, n=1 << 22, seed=1):
+    def selftest_alpha(self, n=1 << 22, seed=1, newton_steps=1):
         err, bad = C.c_double(), C.c_int64()
-        check(lib().tsg_selftest_alpha(self.h, n, seed, C.byref(err), C.byref(bad)), "tsg_selftest_alpha")
+        check(lib().tsg_selftest_alpha(self.h, n, seed, newton_steps, C.byref(err), C.byref(bad)),
+              "tsg_selftest_alpha")
         return err.value, bad.value
 
     def close(self):

@@ -123,22 +123,29 @@ __device__ __forceinline__ R alpha_plain(R x1, R y1, R x2, R y2, R x3, R y3) {
 
 // Reciprocal for the fast α path: the SFU estimate refined by two Newton steps
 // (relative error ~2^-52; FMA is fine here, the value is only compared against a guard band).
+template <int kSteps>
 __device__ __forceinline__ double rcp_refined(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+#pragma unroll
+  for (int i = 0; i < kSteps; ++i) {
+    const double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+  }
+  return r;
 }
-__device__ __forceinline__ float rcp_refined(float x) { return __frcp_rn(x); }
+template <int kSteps>
+__device__ __forceinline__ float rcp_refined(float x) {
+  return __frcp_rn(x);
+}
 
 // Decisions whose fast-path margin is within kGuard (absolute; |α| <= 1) are settled exactly.
 constexpr double kGuard = 0x1p-40;
 
 // triangle_alpha with the division replaced by the refined reciprocal; everything before the
-// division is the reference's exact operation sequence.  es == 0 gives exactly 0.
-template <typename R>
+// division is the reference's exact operation sequence.  A degenerate triangle (es == 0 or a
+// denormal es flushed to zero) yields NaN / inf, which callers detect and settle exactly.
+template <typename R, int kSteps = 1>
 __device__ __forceinline__ R alpha_fast(R x1, R y1, R x2, R y2, R x3, R y3) {
   using O = Arith<R>;
   const R ax = O::sub(x2, x1), ay = O::sub(y2, y1);
@@ -149,8 +156,7 @@ __device__ __forceinline__ R alpha_fast(R x1, R y1, R x2, R y2, R x3, R y3) {
                                     O::mul(by, by)),
                              O::mul(cx, cx)),
                       O::mul(cy, cy));
-  const R q = O::mul(O::mul(Arith<R>::kAlpha, ta), rcp_refined(es));
-  return es == R(0) ? R(0) : q;
+  return O::mul(O::mul(Arith<R>::kAlpha, ta), rcp_refined<kSteps>(es));
 }
 
 // std::min(best, x) (== x < best ? x : best), NaN-compatible with the reference.

@@ -35,7 +35,11 @@ tsg_status fail(tsg_status code, const std::string& msg) {
                   std::string(#call) + ": " + cudaGetErrorString(e_));                  \
   } while (0)
 
-constexpr int kMaxSmallDeg = 16;  // thread-per-vertex path; above: CTA-per-vertex hub path
+// Valence tiers: thread-per-vertex (<= 12, CTA of 128, every slot in Form A), thread-per-vertex
+// over a list (13..31, CTA of 64: larger per-thread ring), CTA-per-vertex hubs (>= 32).
+constexpr int kMaxSmallDeg = 12;
+constexpr int kMaxMedDeg = 31;
+constexpr tsg::Tiers kTiers{kMaxSmallDeg, kMaxMedDeg};
 constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 
 template <class T>
@@ -105,7 +109,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__global__ void selftest_alpha(int64_t n, uint64_t seed, unsigned long long* max_err,
+__global__ void selftest_alpha(int64_t n, uint64_t seed, int steps, unsigned long long* max_err,
                                unsigned long long* nonfinite) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -120,7 +124,8 @@ __global__ void selftest_alpha(int64_t n, uint64_t seed, unsigned long long* max
       c[5] = c[1] + t * (c[3] - c[1]);
     }
     const double e = tsg::alpha_plain<double>(c[0], c[1], c[2], c[3], c[4], c[5]);
-    const double f = tsg::alpha_fast<double>(c[0], c[1], c[2], c[3], c[4], c[5]);
+    const double f = steps == 1 ? tsg::alpha_fast<double, 1>(c[0], c[1], c[2], c[3], c[4], c[5])
+                                : tsg::alpha_fast<double, 2>(c[0], c[1], c[2], c[3], c[4], c[5]);
     if (!(fabs(f) <= 2.0)) {
       atomicAdd(nonfinite, 1ULL);
       continue;
@@ -170,9 +175,10 @@ struct tsg_mesh {
   int64_t bytes = 0;
   void* buf[2] = {nullptr, nullptr};
   void* init = nullptr;  // slot-ordered copy of the coordinates given at upload / set_coords
+  uint16_t* d_fan16 = nullptr;
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
-  int32_t *d_tri = nullptr, *d_hubs = nullptr;
+  int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr;
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   void* d_alpha = nullptr;
   double* d_xy_stage = nullptr;  // 2*nv original-order doubles
@@ -188,7 +194,7 @@ struct tsg_mesh {
   // Form B schedule cache
   int32_t fb_chunks = 0;
   uint32_t* d_nbr_fresh = nullptr;
-  int32_t *d_fb_nodes = nullptr, *d_fb_hubs = nullptr;
+  int32_t *d_fb_nodes = nullptr, *d_fb_hubs = nullptr, *d_fb_medium = nullptr;
   std::vector<tsg::Phase> fb_levels;
   int64_t fb_bytes = 0;
   GraphCache gc;
@@ -200,6 +206,8 @@ void free_form_b(tsg_mesh* m) {
   cudaFree(m->d_nbr_fresh);
   cudaFree(m->d_fb_nodes);
   cudaFree(m->d_fb_hubs);
+  cudaFree(m->d_fb_medium);
+  m->d_fb_medium = nullptr;
   m->d_nbr_fresh = nullptr;
   m->d_fb_nodes = m->d_fb_hubs = nullptr;
   m->bytes -= m->fb_bytes;
@@ -213,7 +221,7 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   free_form_b(m);
   m->gc.reset();
   tsg::FormBSchedule sch;
-  const std::string err = tsg::build_form_b(m->hm, chunks, kMaxSmallDeg, sch);
+  const std::string err = tsg::build_form_b(m->hm, chunks, kTiers, sch);
   if (!err.empty()) return fail(TSG_ERR_INVALID, err);
   int64_t b = 0;
   cudaStream_t s = m->ctx->stream;
@@ -221,6 +229,7 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   if ((st = upload(&m->d_nbr_fresh, sch.nbr_fresh, &b, s))) return st;
   if ((st = upload(&m->d_fb_nodes, sch.nodes, &b, s))) return st;
   if ((st = upload(&m->d_fb_hubs, sch.hubs, &b, s))) return st;
+  if ((st = upload(&m->d_fb_medium, sch.medium, &b, s))) return st;
   TSG_CUDA(cudaStreamSynchronize(s));
   m->fb_levels = std::move(sch.levels);
   m->fb_bytes = b;
@@ -248,6 +257,7 @@ struct Engine {
     a.off = m->d_off;
     a.nbr = c.form == TSG_FORM_B ? m->d_nbr_fresh : m->d_nbr;
     a.fan = m->d_fan;
+    a.fan16 = m->d_fan16;
     a.vinc_off = m->d_vinc_off;
     a.vinc = m->d_vinc;
     a.alpha = static_cast<const R*>(m->d_alpha);
@@ -260,14 +270,25 @@ struct Engine {
 
   template <bool kFormB, bool kTwoPhase>
   static tsg_status launch_phase(tsg_mesh* m, const Args& base, const int32_t* small, int64_t ns,
+                                 const int32_t* medium, int64_t nmed,
                                  const int32_t* hubs, int64_t nh, int32_t hub_cap, cudaStream_t s,
                                  int64_t* kernels) {
     if (ns > 0) {
       Args a = base;
       a.list = small;
       a.count = ns;
-      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg>
+      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock>
           <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    if (nmed > 0) {
+      constexpr int kMedBlock = 64;
+      Args a = base;
+      a.list = medium;
+      a.count = nmed;
+      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxMedDeg, kMedBlock>
+          <<<static_cast<unsigned>((nmed + kMedBlock - 1) / kMedBlock), kMedBlock, 0, s>>>(a);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
@@ -304,14 +325,16 @@ struct Engine {
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
     if (ev_begin) TSG_CUDA(cudaEventRecord(ev_begin, s));
     if (!kFormB) {
-      tsg_status st = launch_phase<false, kTwoPhase>(m, base, nullptr, nv, m->d_hubs,
+      tsg_status st = launch_phase<false, kTwoPhase>(m, base, nullptr, nv, m->d_medium,
+                                                     static_cast<int64_t>(m->hm.medium.size()), m->d_hubs,
                                                      static_cast<int64_t>(m->hm.hubs.size()),
                                                      hub_cap, s, kernels);
       if (st) return st;
     } else {
       for (const tsg::Phase& L : m->fb_levels) {
         tsg_status st = launch_phase<true, kTwoPhase>(m, base, m->d_fb_nodes + L.small_begin,
-                                                      L.small_count, m->d_fb_hubs + L.hub_begin,
+                                                      L.small_count, m->d_fb_medium + L.medium_begin,
+                                                      L.medium_count, m->d_fb_hubs + L.hub_begin,
                                                       L.hub_count, hub_cap, s, kernels);
         if (st) return st;
       }
@@ -478,14 +501,14 @@ tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
   return TSG_OK;
 }
 
-tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, double* max_abs_err_out,
-                              int64_t* nonfinite_out) {
+tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_t newton_steps,
+                              double* max_abs_err_out, int64_t* nonfinite_out) {
   if (!ctx || n < 0) return fail(TSG_ERR_INVALID, "bad arguments");
   TSG_CUDA(cudaSetDevice(ctx->device));
   unsigned long long* d = nullptr;
   TSG_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
   TSG_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  selftest_alpha<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, seed, d, d + 1);
+  selftest_alpha<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, seed, newton_steps, d, d + 1);
   TSG_CUDA(cudaGetLastError());
   unsigned long long h[2];
   TSG_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
@@ -510,7 +533,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   m->layout = d->layout;
   m->prec = d->precision;
   m->rsize = d->precision == TSG_F64 ? 8 : 4;
-  const std::string err = tsg::build_host_mesh(*d, kMaxSmallDeg, m->hm);
+  const std::string err = tsg::build_host_mesh(*d, kTiers, m->hm);
   if (!err.empty()) return fail(TSG_ERR_INVALID, err);
   const auto& hm = m->hm;
   const int64_t nv = hm.nv, nt = hm.nt;
@@ -524,10 +547,12 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_off, hm.off, b, s))) return st;
   if ((st = upload(&m->d_nbr, hm.nbr, b, s))) return st;
   if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
+  if ((st = upload(&m->d_fan16, hm.fan16, b, s))) return st;
   if ((st = upload(&m->d_vinc_off, hm.vinc_off, b, s))) return st;
   if ((st = upload(&m->d_vinc, hm.vinc, b, s))) return st;
   if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
   if ((st = upload(&m->d_hubs, hm.hubs, b, s))) return st;
+  if ((st = upload(&m->d_medium, hm.medium, b, s))) return st;
   if (d->order) {
     if ((st = upload(&m->d_order, hm.order, b, s))) return st;
     if ((st = upload(&m->d_tri_order, hm.tri_order, b, s))) return st;
@@ -556,8 +581,8 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
   free_form_b(m);
-  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_vinc_off, m->d_vinc,
-                  m->d_tri, m->d_hubs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
+  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_vinc_off, m->d_vinc,
+                  m->d_tri, m->d_hubs, m->d_medium, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md,
                   m->d_ext};
   for (void* p : ptrs) cudaFree(p);

@@ -32,7 +32,8 @@ struct PassArgs {
   int32_t swap;
   const uint32_t* off;          // nv+1, compact CSR over slots (rows only for movable vertices)
   const uint32_t* nbr;          // slots, ascending ORIGINAL id (| kFreshBit for Form B)
-  const uint32_t* fan;          // fan records, same offsets as nbr
+  const uint32_t* fan;          // hub fan records (i1, i2, k), same offsets as nbr
+  const uint16_t* fan16;        // small-vertex fan records (p1, p2, p3 ring positions)
   const uint32_t* vinc_off;     // TwoPhase: incident-triangle CSR over slots
   const uint32_t* vinc;
   const R* alpha;               // TwoPhase: pass-start α field (device triangle order)
@@ -95,145 +96,185 @@ __device__ __forceinline__ void commit_stats(int accepted, double disp, int32_t*
 // reciprocal (|error| < 2^-50 on |α| <= 1); the strict test hyp > thr is settled from those
 // values whenever they are more than kGuard apart, and otherwise (rare: near-ties) every α of
 // the vertex is re-evaluated with IEEE division, exactly as the reference (quality.hpp:15-23).
-template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg>
-__global__ void __launch_bounds__(kNodeBlock) node_update(PassArgs<R, kSoA> a) {
+template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg, int kBlock>
+__global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(PassArgs<R, kSoA> a) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr int kSelf = kMaxDeg;
   constexpr bool kExact = sizeof(R) == 8;
-  __shared__ R2 ring[(kMaxDeg + 1) * kNodeBlock];
-  const PassState* st = a.st;
-  if (st->done) return;
-  const int pass = st->pass;
-  Coords<R, kSoA> P, N;
-  select_buffers(a, pass, P, N);
-
+  __shared__ R2 ring[(kMaxDeg + 1) * kBlock];
+  __shared__ uint16_t fan_s[kMaxDeg * kBlock];
   const int tid = threadIdx.x;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * kNodeBlock + tid;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + tid;
+
+  // Topology loads do not depend on the pass state: issue them before waiting for it.
+  int64_t s = 0;
+  uint32_t o0 = 0;
+  int deg = 0;
+  if (i < a.count) {
+    s = a.list ? static_cast<int64_t>(a.list[i]) : i;
+    o0 = a.off[s];
+    deg = static_cast<int>(a.off[s + 1] - o0);
+    if (deg > kMaxDeg) deg = 0;  // hub: handled by hub_update
+  }
+  const PassState* st = a.st;
+  const int2 state = *reinterpret_cast<const int2*>(st);  // {pass, done}
+  const uint32_t* nb = a.nbr + o0;
+  const uint16_t* fan = a.fan16 + o0;
+
   int accepted = 0;
   double disp = 0.0;
-  if (i < a.count) {
-    const int64_t s = a.list ? static_cast<int64_t>(a.list[i]) : i;
-    const uint32_t o0 = a.off[s];
-    const int deg = static_cast<int>(a.off[s + 1] - o0);
-    if (deg > 0 && deg <= kMaxDeg) {
-      const uint32_t* nb = a.nbr + o0;
-      const uint32_t* fan = a.fan + o0;
-      const R2 pv = P.load(s);
-      R sx = R(0), sy = R(0);
-      uint32_t fresh = 0;
-      // Gather in batches of 8 (independent loads in flight), ordered accumulation.
+  R2 pv{}, cand{};
+  R sx = R(0), sy = R(0);
+  uint32_t fresh = 0;
+  Coords<R, kSoA> P, N;
+  // Gather in batches of 8 (ids + fan records, then coordinates: independent loads in
+  // flight), ordered accumulation of the neighbour sum (Form A).
 #pragma unroll
-      for (int base = 0; base < kMaxDeg; base += 8) {
-        if (base < deg) {
-          uint32_t u[8];
+  for (int base = 0; base < kMaxDeg; base += 8) {
+    if (base < deg) {
+      uint32_t u[8];
+      uint16_t f[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) u[j] = (base + j < deg) ? __ldg(nb + base + j) : 0u;
-          R2 c[8];
+      for (int j = 0; j < 8; ++j) {
+        u[j] = (base + j < deg) ? __ldg(nb + base + j) : 0u;
+        f[j] = (base + j < deg) ? __ldg(fan + base + j) : uint16_t{0};
+      }
+      if (base == 0) {
+        if (state.y) return;  // stop rule fired (stream driver); uniform across the block
+        select_buffers(a, state.x, P, N);
+        pv = P.load(s);
+      }
+      R2 c[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (base + j < deg) c[j] = P.load(u[j] & ~kFreshBit);
+      for (int j = 0; j < 8; ++j)
+        if (base + j < deg) c[j] = P.load(u[j] & ~kFreshBit);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (base + j < deg) {
-              ring[(base + j) * kNodeBlock + tid] = c[j];
-              if constexpr (kFormB) {
-                if (u[j] & kFreshBit) fresh |= 1u << (base + j);
-              } else {
-                sx = O::add(sx, c[j].x);
-                sy = O::add(sy, c[j].y);
-              }
-            }
+      for (int j = 0; j < 8; ++j) {
+        if (base + j < deg) {
+          ring[(base + j) * kBlock + tid] = c[j];
+          fan_s[(base + j) * kBlock + tid] = f[j];
+          if constexpr (kFormB) {
+            if (u[j] & kFreshBit) fresh |= 1u << (base + j);
+          } else {
+            sx = O::add(sx, c[j].x);
+            sy = O::add(sy, c[j].y);
           }
         }
       }
-      auto at = [&](uint32_t idx) -> R2 { return ring[idx * kNodeBlock + tid]; };
-      bool bad = false;  // an approximation is not finite: settle exactly
-
-      // Threshold: pass-start minimum incident α (TwoPhase: the stored field, already exact).
-      ring[kSelf * kNodeBlock + tid] = pv;
-      R thr = R(INFINITY);
-      if constexpr (kTwoPhase) {
-        const uint32_t t0 = a.vinc_off[s], t1 = a.vinc_off[s + 1];
-        for (uint32_t t = t0; t < t1; ++t) thr = min_ref(thr, a.alpha[a.vinc[t]]);
-      } else {
-        for (int j = 0; j < deg; ++j) {
-          const uint32_t f = __ldg(fan + j);
-          const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
-          const R q = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y);
-          bad |= !(fabs(q) <= R(2));
-          thr = min_ref(thr, q);
-        }
-      }
-      if constexpr (kFormB) {
-        // ChunkView (quality.hpp:40-50): in-chunk lower-id neighbours read this pass's values.
-        uint32_t m = fresh;
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          ring[j * kNodeBlock + tid] = N.load_mut(nb[j] & ~kFreshBit);
-        }
-        for (int j = 0; j < deg; ++j) {
-          const R2 c = at(j);
-          sx = O::add(sx, c.x);
-          sy = O::add(sy, c.y);
-        }
-      }
-      const R inv = O::div(R(1), static_cast<R>(deg));  // 1.0 / deg (smoothing.hpp:78)
-      const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-      ring[kSelf * kNodeBlock + tid] = cand;
-      // Hypothetical minimum with early rejection once one triangle is surely <= thr.
-      R hyp = R(INFINITY);
-      for (int j = 0; j < deg; ++j) {
-        const uint32_t f = __ldg(fan + j);
-        const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
-        const R q = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y);
-        bad |= !(fabs(q) <= R(2));
-        hyp = min_ref(hyp, q);
-        if (kExact && hyp < thr - R(kGuard)) break;
-      }
-      bool acc;
-      if constexpr (!kExact) {
-        acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
-      } else if (!bad && hyp > thr + R(kGuard)) {
-        acc = true;
-      } else if (!bad && hyp < thr - R(kGuard)) {
-        acc = false;
-      } else {
-        // Near-tie: the reference's exact values (IEEE division), same operand order.
-        R thr_e = thr;
-        if constexpr (!kTwoPhase) {
-          thr_e = R(INFINITY);
-          for (int j = 0; j < deg; ++j) {
-            const uint32_t f = __ldg(fan + j);
-            R2 q[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const uint32_t idx = fan_p(f, c);
-              q[c] = idx == kSelf ? pv
-                     : (kFormB && ((fresh >> idx) & 1u)) ? P.load(nb[idx] & ~kFreshBit) : at(idx);
-            }
-            thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
-          }
-        }
-        R hyp_e = R(INFINITY);
-        for (int j = 0; j < deg; ++j) {
-          const uint32_t f = __ldg(fan + j);
-          const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
-          hyp_e = min_ref(hyp_e, alpha_plain<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
-        }
-        acc = hyp_e > thr_e;
-      }
-      N.store(s, acc ? cand : pv);
-      if (acc) {
-        accepted = 1;
-        const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
-        disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-      }
-      if (a.decision) a.decision[s] = acc ? 1 : 0;
     }
   }
-  commit_stats<kNodeBlock>(accepted, disp, a.pass_acc + pass, a.pass_md + pass);
+  if (deg == 0) {
+    if (state.y) return;
+    select_buffers(a, state.x, P, N);
+  }
+  const int pass = state.x;
+  if (deg > 0) {
+    auto at = [&](uint32_t idx) -> R2 { return ring[idx * kBlock + tid]; };
+    auto fan_at = [&](int j) -> uint32_t { return fan_s[j * kBlock + tid]; };
+    // Fast α of fan triangle j.  fp64: NaN / inf (degenerate triangle) poisons `nan_acc` and
+    // the decision falls back to exact evaluation; fp32: degenerate gives 0 as the reference.
+    auto fast = [&](int j) -> R {
+      const uint32_t f = fan_at(j);
+      const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
+      return alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y);
+    };
+    R nan_acc = R(0);
+
+    // Threshold: pass-start minimum incident α (TwoPhase: the stored field, already exact).
+    ring[kSelf * kBlock + tid] = pv;
+    R thr = R(INFINITY);
+    if constexpr (kTwoPhase) {
+      const uint32_t t0 = a.vinc_off[s], t1 = a.vinc_off[s + 1];
+      for (uint32_t t = t0; t < t1; ++t) thr = min_ref(thr, a.alpha[a.vinc[t]]);
+    } else {
+#pragma unroll 4
+      for (int j = 0; j < deg; ++j) {
+        R q = fast(j);
+        if constexpr (!kExact) q = isfinite(q) ? q : R(0);
+        nan_acc = O::add(nan_acc, q);
+        thr = fmin(thr, q);
+      }
+    }
+    bool view_moved = false;  // Form B: some fresh neighbour differs from its pass-start value
+    if constexpr (kFormB) {
+      // ChunkView (quality.hpp:40-50): in-chunk lower-id neighbours read this pass's values.
+      uint32_t m = fresh;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const R2 now = N.load_mut(nb[j] & ~kFreshBit);
+        const R2 was = at(j);
+        view_moved |= (now.x != was.x) || (now.y != was.y);
+        ring[j * kBlock + tid] = now;
+      }
+      for (int j = 0; j < deg; ++j) {
+        const R2 c = at(j);
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
+    }
+    const R inv = O::div(R(1), static_cast<R>(deg));  // 1.0 / deg (smoothing.hpp:78)
+    cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    // Exact tie: candidate == current position and every neighbour read is the pass-start
+    // value, so each hypothetical α equals its threshold α bit for bit and the strict test
+    // fails.  Common once a region has converged; skips the whole hypothetical evaluation.
+    const bool tie = !view_moved && cand.x == pv.x && cand.y == pv.y;
+    ring[kSelf * kBlock + tid] = cand;
+    R hyp = R(INFINITY);
+    if (!tie) {
+#pragma unroll 4
+      for (int j = 0; j < deg; ++j) {
+        R q = fast(j);
+        if constexpr (!kExact) q = isfinite(q) ? q : R(0);
+        nan_acc = O::add(nan_acc, q);
+        hyp = fmin(hyp, q);
+      }
+    }
+    const bool bad = !(fabs(nan_acc) < R(1e30));
+    bool acc;
+    if (tie) {
+      acc = false;
+    } else if constexpr (!kExact) {
+      acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
+    } else if (!bad && hyp > thr + R(kGuard)) {
+      acc = true;
+    } else if (!bad && hyp < thr - R(kGuard)) {
+      acc = false;
+    } else {
+      // Near-tie: the reference's exact values (IEEE division), same operand order.
+      R thr_e = thr;
+      if constexpr (!kTwoPhase) {
+        thr_e = R(INFINITY);
+        for (int j = 0; j < deg; ++j) {
+          const uint32_t f = fan_at(j);
+          R2 q[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const uint32_t idx = fan_p(f, c);
+            q[c] = idx == kSelf ? pv
+                   : (kFormB && ((fresh >> idx) & 1u)) ? P.load(nb[idx] & ~kFreshBit) : at(idx);
+          }
+          thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
+        }
+      }
+      R hyp_e = R(INFINITY);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = fan_at(j);
+        const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
+        hyp_e = min_ref(hyp_e, alpha_plain<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
+      }
+      acc = hyp_e > thr_e;
+    }
+    N.store(s, acc ? cand : pv);
+    if (acc) {
+      accepted = 1;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+    }
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+  }
+  commit_stats<kBlock>(accepted, disp, a.pass_acc + pass, a.pass_md + pass);
 }
 
 // CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)

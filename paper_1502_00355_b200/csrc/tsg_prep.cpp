@@ -108,7 +108,7 @@ void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
   for (int64_t s = 0; s < nv; ++s) order_out[s] = static_cast<int64_t>(keys[s] & 0xffffffffu);
 }
 
-std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostMesh& hm) {
+std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm) {
   const int64_t nv = d.nv, nt = d.nt;
   if (nv <= 0 || nt <= 0) return "mesh must have vertices and triangles";
   if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
@@ -177,6 +177,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostM
   hm.off[nv] = static_cast<uint32_t>(total);
   hm.nbr.assign(total, 0);
   hm.fan.assign(total, 0);
+  hm.fan16.assign(total, 0);
 
   // Device triangle order: identity, or by the smallest slot among the corners (stable) so
   // that the triangle kernels stream coordinates in the same locality order as the vertices.
@@ -229,13 +230,14 @@ std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostM
           return;
         }
         const uint32_t ia = static_cast<uint32_t>(pa - row), ic = static_cast<uint32_t>(pc - row);
-        if (n <= max_small_deg) {
-          // ring positions of (p1, p2, p3); v itself is ring entry max_small_deg
+        const int tier = tiers.tier(static_cast<uint32_t>(n));
+        if (tier < 2) {
+          // ring positions of (p1, p2, p3); v itself is the entry after the tier's last
           uint32_t p[3];
-          p[k] = static_cast<uint32_t>(max_small_deg);
+          p[k] = static_cast<uint32_t>(tier == 0 ? tiers.small_max : tiers.medium_max);
           p[(k + 1) % 3] = ia;
           p[(k + 2) % 3] = ic;
-          out_f[j] = p[0] | (p[1] << 5) | (p[2] << 10);
+          hm.fan16[hm.off[s] + j] = static_cast<uint16_t>(p[0] | (p[1] << 5) | (p[2] << 10));
         } else {
           out_f[j] = fan_pack_h(ia, ic, static_cast<uint32_t>(k));
         }
@@ -267,13 +269,17 @@ std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostM
   });
 
   hm.hubs.clear();
-  for (int64_t s = 0; s < nv; ++s)
-    if (deg[s] > static_cast<uint32_t>(max_small_deg)) hm.hubs.push_back(static_cast<int32_t>(s));
+  hm.medium.clear();
+  for (int64_t s = 0; s < nv; ++s) {
+    if (deg[s] == 0) continue;
+    const int tier = tiers.tier(deg[s]);
+    if (tier == 1) hm.medium.push_back(static_cast<int32_t>(s));
+    if (tier == 2) hm.hubs.push_back(static_cast<int32_t>(s));
+  }
   return "";
 }
 
-std::string build_form_b(const HostMesh& hm, int32_t chunks, int32_t max_small_deg,
-                         FormBSchedule& out) {
+std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out) {
   const int64_t nv = hm.nv;
   if (chunks < 1) return "chunks must be >= 1";
   const int64_t k = (nv + chunks - 1) / chunks;  // worker_chunk: ceil(n / workers)
@@ -299,38 +305,36 @@ std::string build_form_b(const HostMesh& hm, int32_t chunks, int32_t max_small_d
     level[v] = L;
     nlev = std::max(nlev, L + 1);
   }
-  std::vector<int64_t> small_cnt(nlev + 1, 0), hub_cnt(nlev + 1, 0);
+  // counts[t][L + 1]: vertices of tier t on level L, then prefix sums -> list offsets
+  std::vector<int64_t> counts[3];
+  for (auto& c : counts) c.assign(nlev + 1, 0);
   for (int64_t s = 0; s < nv; ++s) {
     const int32_t L = level[hm.order[s]];
-    if (L < 0) continue;
-    const uint32_t dg = hm.off[s + 1] - hm.off[s];
-    if (dg > static_cast<uint32_t>(max_small_deg))
-      ++hub_cnt[L + 1];
-    else
-      ++small_cnt[L + 1];
+    if (L >= 0) ++counts[tiers.tier(hm.off[s + 1] - hm.off[s])][L + 1];
   }
-  for (int32_t L = 0; L < nlev; ++L) {
-    small_cnt[L + 1] += small_cnt[L];
-    hub_cnt[L + 1] += hub_cnt[L];
+  for (auto& c : counts)
+    for (int32_t L = 0; L < nlev; ++L) c[L + 1] += c[L];
+  std::vector<int32_t>* lists[3] = {&out.nodes, &out.medium, &out.hubs};
+  std::vector<int64_t> fill[3];
+  for (int t = 0; t < 3; ++t) {
+    lists[t]->assign(counts[t][nlev], 0);
+    fill[t].assign(counts[t].begin(), counts[t].end() - 1);
   }
-  out.nodes.assign(small_cnt[nlev], 0);
-  out.hubs.assign(hub_cnt[nlev], 0);
-  std::vector<int64_t> sf(small_cnt.begin(), small_cnt.end() - 1), hf(hub_cnt.begin(), hub_cnt.end() - 1);
   for (int64_t s = 0; s < nv; ++s) {  // slot-ascending inside each level
     const int32_t L = level[hm.order[s]];
     if (L < 0) continue;
-    const uint32_t dg = hm.off[s + 1] - hm.off[s];
-    if (dg > static_cast<uint32_t>(max_small_deg))
-      out.hubs[hf[L]++] = static_cast<int32_t>(s);
-    else
-      out.nodes[sf[L]++] = static_cast<int32_t>(s);
+    const int t = tiers.tier(hm.off[s + 1] - hm.off[s]);
+    (*lists[t])[fill[t][L]++] = static_cast<int32_t>(s);
   }
   out.levels.resize(nlev);
   for (int32_t L = 0; L < nlev; ++L) {
-    out.levels[L].small_begin = small_cnt[L];
-    out.levels[L].small_count = small_cnt[L + 1] - small_cnt[L];
-    out.levels[L].hub_begin = hub_cnt[L];
-    out.levels[L].hub_count = hub_cnt[L + 1] - hub_cnt[L];
+    Phase& ph = out.levels[L];
+    ph.small_begin = counts[0][L];
+    ph.small_count = counts[0][L + 1] - counts[0][L];
+    ph.medium_begin = counts[1][L];
+    ph.medium_count = counts[1][L + 1] - counts[1][L];
+    ph.hub_begin = counts[2][L];
+    ph.hub_count = counts[2][L + 1] - counts[2][L];
   }
   return "";
 }

@@ -19,6 +19,18 @@
 
 namespace tsg {
 
+// Valence tiers of movable vertices: thread-per-vertex kernels for small (<= small_max) and
+// medium (<= medium_max, a separate list) rows, CTA-per-vertex for hubs.  A small / medium fan
+// record stores ring positions with v itself at position small_max / medium_max, which must
+// fit 5 bits.
+struct Tiers {
+  int32_t small_max = 12;
+  int32_t medium_max = 31;
+  int tier(uint32_t deg) const {
+    return deg <= static_cast<uint32_t>(small_max) ? 0 : deg <= static_cast<uint32_t>(medium_max) ? 1 : 2;
+  }
+};
+
 struct HostMesh {
   int64_t nv = 0, nt = 0;
   std::vector<int64_t> order;     // slot -> original vertex
@@ -26,31 +38,34 @@ struct HostMesh {
   std::vector<int64_t> tri_order; // device triangle -> original triangle
   std::vector<uint32_t> off;      // nv+1
   std::vector<uint32_t> nbr;      // slots
-  std::vector<uint32_t> fan;
+  std::vector<uint32_t> fan;      // hub rows: (i1, i2, k) records; small rows unused
+  std::vector<uint16_t> fan16;    // small rows: ring positions of (p1, p2, p3), 5 bits each
   std::vector<uint32_t> vinc_off; // nv+1, all vertices
   std::vector<uint32_t> vinc;     // device triangle ids
   std::vector<int32_t> tri;       // 3*nt device slots, device triangle order
-  std::vector<int32_t> hubs;      // slots with deg > max_small_deg
+  std::vector<int32_t> medium;    // slots of the medium tier
+  std::vector<int32_t> hubs;      // slots of the hub tier
   int32_t max_deg = 0;
 };
 
 struct Phase {
-  int64_t small_begin = 0, small_count = 0;  // range in the level node list
-  int64_t hub_begin = 0, hub_count = 0;      // range in the level hub list
+  int64_t small_begin = 0, small_count = 0;    // range in the level node list
+  int64_t medium_begin = 0, medium_count = 0;  // range in the level medium list
+  int64_t hub_begin = 0, hub_count = 0;        // range in the level hub list
 };
 
 struct FormBSchedule {
   int32_t chunks = 0;
   std::vector<uint32_t> nbr_fresh;  // nbr with kFreshBit on in-chunk lower-id neighbours
   std::vector<int32_t> nodes;       // small-degree slots grouped by level
+  std::vector<int32_t> medium;      // medium-tier slots grouped by level
   std::vector<int32_t> hubs;        // hub slots grouped by level
   std::vector<Phase> levels;
 };
 
 // Returns "" on success, else an error message.
-std::string build_host_mesh(const tsg_mesh_desc& d, int32_t max_small_deg, HostMesh& out);
-std::string build_form_b(const HostMesh& hm, int32_t chunks, int32_t max_small_deg,
-                         FormBSchedule& out);
+std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
+std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
 
 }  // namespace tsg
