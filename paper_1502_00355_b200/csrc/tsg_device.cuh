@@ -145,7 +145,7 @@ constexpr double kGuard = 0x1p-40;
 // triangle_alpha with the division replaced by the refined reciprocal; everything before the
 // division is the reference's exact operation sequence.  A degenerate triangle (es == 0 or a
 // denormal es flushed to zero) yields NaN / inf, which callers detect and settle exactly.
-template <typename R, int kSteps = 1>
+template <typename R, int kSteps = 2>
 __device__ __forceinline__ R alpha_fast(R x1, R y1, R x2, R y2, R x3, R y3) {
   using O = Arith<R>;
   const R ax = O::sub(x2, x1), ay = O::sub(y2, y1);

@@ -165,6 +165,11 @@ struct tsg_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> pass_events;  // stream-timed driver
+  // Side stream for the medium / hub tiers, forked from and joined back into `stream` so
+  // the tiers of one pass (or one Form B level) run concurrently (also inside graphs).
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> fork_events;
+  size_t fork_next = 0;
 };
 
 struct tsg_mesh {
@@ -269,16 +274,39 @@ struct Engine {
   }
 
   template <bool kFormB, bool kTwoPhase>
+  // Events for fork/join (reused round-robin; a graph capture keeps its own edges, a plain
+  // launch sequence only needs each event until the matching wait has been enqueued).
+  static tsg_status next_event(tsg_context* ctx, cudaEvent_t* ev) {
+    if (ctx->fork_next == ctx->fork_events.size()) {
+      cudaEvent_t e;
+      TSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->fork_events.push_back(e);
+    }
+    *ev = ctx->fork_events[ctx->fork_next++];
+    return TSG_OK;
+  }
+
   static tsg_status launch_phase(tsg_mesh* m, const Args& base, const int32_t* small, int64_t ns,
                                  const int32_t* medium, int64_t nmed,
                                  const int32_t* hubs, int64_t nh, int32_t hub_cap, cudaStream_t s,
                                  int64_t* kernels) {
-    if (ns > 0) {
+    tsg_context* ctx = m->ctx;
+    const bool fork = ns > 0 && (nmed > 0 || nh > 0);
+    cudaStream_t t = s;  // stream of the medium / hub tiers
+    if (fork) {
+      cudaEvent_t e;
+      tsg_status st = next_event(ctx, &e);
+      if (st) return st;
+      TSG_CUDA(cudaEventRecord(e, s));
+      TSG_CUDA(cudaStreamWaitEvent(ctx->side, e, 0));
+      t = ctx->side;
+    }
+    if (nh > 0) {  // longest-latency tier first
       Args a = base;
-      a.list = small;
-      a.count = ns;
-      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock>
-          <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
+      a.list = hubs;
+      a.count = nh;
+      const size_t smem = static_cast<size_t>(hub_cap) * sizeof(R2) * (kFormB ? 2 : 1);
+      tsg::hub_update<R, kSoA, kFormB, kTwoPhase><<<static_cast<unsigned>(nh), tsg::kHubBlock, smem, t>>>(a, hub_cap);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
@@ -288,19 +316,25 @@ struct Engine {
       a.list = medium;
       a.count = nmed;
       tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxMedDeg, kMedBlock>
-          <<<static_cast<unsigned>((nmed + kMedBlock - 1) / kMedBlock), kMedBlock, 0, s>>>(a);
+          <<<static_cast<unsigned>((nmed + kMedBlock - 1) / kMedBlock), kMedBlock, 0, t>>>(a);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
-    if (nh > 0) {
+    if (ns > 0) {
       Args a = base;
-      a.list = hubs;
-      a.count = nh;
-      const size_t smem = static_cast<size_t>(hub_cap) * sizeof(R2) * (kFormB ? 2 : 1);
-      auto kfn = tsg::hub_update<R, kSoA, kFormB, kTwoPhase>;
-      kfn<<<static_cast<unsigned>(nh), tsg::kHubBlock, smem, s>>>(a, hub_cap);
+      a.list = small;
+      a.count = ns;
+      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock>
+          <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
+    }
+    if (fork) {
+      cudaEvent_t e;
+      tsg_status st = next_event(ctx, &e);
+      if (st) return st;
+      TSG_CUDA(cudaEventRecord(e, ctx->side));
+      TSG_CUDA(cudaStreamWaitEvent(s, e, 0));
     }
     return TSG_OK;
   }
@@ -311,6 +345,7 @@ struct Engine {
                                    int8_t* decision, cudaEvent_t ev_begin, cudaEvent_t ev_end,
                                    int64_t* kernels) {
     const int64_t nv = m->hm.nv;
+    m->ctx->fork_next = 0;  // fork/join events are reusable once their waits are enqueued
     if (c.swap == TSG_SWAP_COPY)
       TSG_CUDA(cudaMemcpyAsync(m->buf[1], m->buf[0], 2 * nv * sizeof(R), cudaMemcpyDeviceToDevice, s));
     if (kTwoPhase) {
@@ -478,6 +513,7 @@ tsg_status tsg_context_create(int32_t device, tsg_context** out) {
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   TSG_CUDA(cudaEventCreate(&ctx->ev0));
   TSG_CUDA(cudaEventCreate(&ctx->ev1));
+  TSG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   *out = ctx.release();
   return TSG_OK;
 }
@@ -488,6 +524,8 @@ tsg_status tsg_context_destroy(tsg_context* ctx) {
   for (cudaEvent_t e : ctx->pass_events) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
+  for (cudaEvent_t e : ctx->fork_events) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TSG_OK;
