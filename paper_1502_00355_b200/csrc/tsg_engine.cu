@@ -273,7 +273,6 @@ struct Engine {
     return a;
   }
 
-  template <bool kFormB, bool kTwoPhase>
   // Events for fork/join (reused round-robin; a graph capture keeps its own edges, a plain
   // launch sequence only needs each event until the matching wait has been enqueued).
   static tsg_status next_event(tsg_context* ctx, cudaEvent_t* ev) {
@@ -286,6 +285,7 @@ struct Engine {
     return TSG_OK;
   }
 
+  template <bool kFormB, bool kTwoPhase>
   static tsg_status launch_phase(tsg_mesh* m, const Args& base, const int32_t* small, int64_t ns,
                                  const int32_t* medium, int64_t nmed,
                                  const int32_t* hubs, int64_t nh, int32_t hub_cap, cudaStream_t s,

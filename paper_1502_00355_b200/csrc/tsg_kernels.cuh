@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
     if constexpr (kTwoPhase) {
       const uint32_t t0 = a.vinc_off[s], t1 = a.vinc_off[s + 1];
       for (uint32_t t = t0; t < t1; ++t) thr = min_ref(thr, a.alpha[a.vinc[t]]);
-    } else {
+    } else if constexpr (kFormB) {
+      // (Form A fused evaluates the threshold inside the hypothetical sweep below.)
 #pragma unroll 4
       for (int j = 0; j < deg; ++j) {
         R q = fast(j);
@@ -220,9 +221,30 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
     // value, so each hypothetical α equals its threshold α bit for bit and the strict test
     // fails.  Common once a region has converged; skips the whole hypothetical evaluation.
     const bool tie = !view_moved && cand.x == pv.x && cand.y == pv.y;
-    ring[kSelf * kBlock + tid] = cand;
     R hyp = R(INFINITY);
-    if (!tie) {
+    if constexpr (!kFormB && !kTwoPhase) {
+      // Form A, fused: one sweep over the fan evaluates each triangle at the pass-start
+      // position and at the candidate.  The ring entries are read from shared memory once and
+      // v is swapped for the candidate in registers, halving the shared-memory traffic that
+      // bounds this kernel (L1 data-pipe wavefronts, profiles/).
+#pragma unroll 4
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = fan_at(j);
+        const uint32_t i0 = fan_p(f, 0), i1 = fan_p(f, 1), i2 = fan_p(f, 2);
+        const R2 q1 = at(i0), q2 = at(i1), q3 = at(i2);
+        const R2 c1 = i0 == kSelf ? cand : q1, c2 = i1 == kSelf ? cand : q2, c3 = i2 == kSelf ? cand : q3;
+        R t = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y);
+        R h = alpha_fast<R>(c1.x, c1.y, c2.x, c2.y, c3.x, c3.y);
+        if constexpr (!kExact) {
+          t = isfinite(t) ? t : R(0);
+          h = isfinite(h) ? h : R(0);
+        }
+        nan_acc = O::add(nan_acc, O::add(t, h));
+        thr = fmin(thr, t);
+        hyp = fmin(hyp, h);
+      }
+    } else if (!tie) {
+      ring[kSelf * kBlock + tid] = cand;
 #pragma unroll 4
       for (int j = 0; j < deg; ++j) {
         R q = fast(j);
@@ -261,8 +283,13 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
       R hyp_e = R(INFINITY);
       for (int j = 0; j < deg; ++j) {
         const uint32_t f = fan_at(j);
-        const R2 q1 = at(fan_p(f, 0)), q2 = at(fan_p(f, 1)), q3 = at(fan_p(f, 2));
-        hyp_e = min_ref(hyp_e, alpha_plain<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y));
+        R2 q[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const uint32_t idx = fan_p(f, c);
+          q[c] = idx == kSelf ? cand : at(idx);
+        }
+        hyp_e = min_ref(hyp_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
       }
       acc = hyp_e > thr_e;
     }
