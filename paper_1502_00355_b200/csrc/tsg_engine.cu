@@ -190,8 +190,10 @@ struct tsg_mesh {
   double* d_vmin = nullptr;
   int8_t *d_decision = nullptr, *d_decision_orig = nullptr;
   tsg::PassState* d_state = nullptr;
-  int32_t* d_acc = nullptr;
+  int32_t* d_acc = nullptr;            // per-pass totals (written by finalize_pass)
   unsigned long long* d_md = nullptr;
+  int32_t* d_sacc = nullptr;           // per-pass stat slots (kStatSlots each)
+  unsigned long long* d_smd = nullptr;
   unsigned long long* d_ext = nullptr;  // extrema scratch (3)
   int32_t cap = 0;
   int cur = 0;
@@ -267,8 +269,8 @@ struct Engine {
     a.vinc = m->d_vinc;
     a.alpha = static_cast<const R*>(m->d_alpha);
     a.st = m->d_state;
-    a.pass_acc = m->d_acc;
-    a.pass_md = m->d_md;
+    a.slot_acc = m->d_sacc;
+    a.slot_md = m->d_smd;
     a.decision = nullptr;
     return a;
   }
@@ -375,7 +377,8 @@ struct Engine {
       }
     }
     if (ev_end) TSG_CUDA(cudaEventRecord(ev_end, s));
-    tsg::finalize_pass<<<1, 1, 0, s>>>(m->d_state, m->d_acc, m->d_md, tol_abs, c.max_iters, h, use_handle);
+    tsg::finalize_pass<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, m->d_acc, m->d_md, tol_abs,
+                                        c.max_iters, h, use_handle);
     TSG_CUDA(cudaGetLastError());
     ++*kernels;
     return TSG_OK;
@@ -475,10 +478,16 @@ tsg_status ensure_stats_capacity(tsg_mesh* m, int32_t n) {
   if (m->cap >= n) return TSG_OK;
   cudaFree(m->d_acc);
   cudaFree(m->d_md);
+  cudaFree(m->d_sacc);
+  cudaFree(m->d_smd);
   m->d_acc = nullptr;
   m->d_md = nullptr;
+  m->d_sacc = nullptr;
+  m->d_smd = nullptr;
   TSG_CUDA(cudaMalloc(&m->d_acc, sizeof(int32_t) * n));
   TSG_CUDA(cudaMalloc(&m->d_md, sizeof(unsigned long long) * n));
+  TSG_CUDA(cudaMalloc(&m->d_sacc, sizeof(int32_t) * n * tsg::kStatSlots));
+  TSG_CUDA(cudaMalloc(&m->d_smd, sizeof(unsigned long long) * n * tsg::kStatSlots));
   m->cap = n;
   m->gc.reset();  // graph captured old pointers
   return TSG_OK;
@@ -621,7 +630,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   free_form_b(m);
   void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
-                  m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md,
+                  m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext};
   for (void* p : ptrs) cudaFree(p);
   delete m;
@@ -751,8 +760,8 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   if (st) return st;
   const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
   TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
-  TSG_CUDA(cudaMemsetAsync(m->d_acc, 0, sizeof(int32_t) * c->max_iters, s));
-  TSG_CUDA(cudaMemsetAsync(m->d_md, 0, sizeof(unsigned long long) * c->max_iters, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * c->max_iters, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
 
   int64_t kernels_per_pass = 0;
   double node_ms = -1.0;
@@ -895,8 +904,8 @@ tsg_status tsg_pass_lockstep(tsg_mesh* m, int32_t form, int32_t chunks, int8_t* 
   st = dispatch(m, [&](auto E) { return decltype(E)::normalize(m); });
   if (st) return st;
   TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
-  TSG_CUDA(cudaMemsetAsync(m->d_acc, 0, sizeof(int32_t), s));
-  TSG_CUDA(cudaMemsetAsync(m->d_md, 0, sizeof(unsigned long long), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots, s));
   TSG_CUDA(cudaMemsetAsync(m->d_decision, 0xff, m->hm.nv, s));
   int64_t k = 0;
   st = dispatch(m, [&](auto E) {

@@ -40,8 +40,9 @@ struct PassArgs {
   const int32_t* list;          // phase node list (nullptr = slots [0, count))
   int64_t count;
   PassState* st;
-  int32_t* pass_acc;
-  unsigned long long* pass_md;  // max displacement bits (non-negative doubles order as u64)
+  int32_t* slot_acc;            // [pass][kStatSlots] partial accepted counts
+  unsigned long long* slot_md;  // [pass][kStatSlots] partial max displacement bits
+                                // (non-negative doubles order as u64)
   int8_t* decision;             // optional: 1 accept / 0 reject per slot
 };
 
@@ -57,31 +58,21 @@ __device__ __forceinline__ void select_buffers(const PassArgs<R, kSoA>& a, int p
   }
 }
 
-// Block reduction of {accepted, max displacement} and one pair of atomics per block.
-template <int kBlock>
-__device__ __forceinline__ void commit_stats(int accepted, double disp, int32_t* acc_slot,
-                                             unsigned long long* md_slot) {
-  __shared__ int s_acc[kBlock / 32];
-  __shared__ double s_md[kBlock / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Per-pass statistics are accumulated into kStatSlots spread slots (one pair per warp, slot
+// chosen by the warp's global index) so that no block barrier and no single hot address sits
+// on the critical path; finalize_pass folds the slots into the per-pass totals.
+constexpr int kStatSlots = 32;
+
+__device__ __forceinline__ void commit_stats_warp(int accepted, double disp, int32_t* acc_slots,
+                                                  unsigned long long* md_slots) {
+  const int lane = threadIdx.x & 31;
   accepted = __reduce_add_sync(0xffffffffu, accepted);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) disp = fmax(disp, __shfl_xor_sync(0xffffffffu, disp, o));
-  if (lane == 0) {
-    s_acc[warp] = accepted;
-    s_md[warp] = disp;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    accepted = lane < kBlock / 32 ? s_acc[lane] : 0;
-    disp = lane < kBlock / 32 ? s_md[lane] : 0.0;
-    accepted = __reduce_add_sync(0xffffffffu, accepted);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) disp = fmax(disp, __shfl_xor_sync(0xffffffffu, disp, o));
-    if (lane == 0) {
-      if (accepted) atomicAdd(acc_slot, accepted);
-      if (disp > 0.0) atomicMax(md_slot, static_cast<unsigned long long>(__double_as_longlong(disp)));
-    }
+  if (lane == 0 && (accepted || disp > 0.0)) {
+    const unsigned slot = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kStatSlots - 1);
+    if (accepted) atomicAdd(acc_slots + slot, accepted);
+    if (disp > 0.0) atomicMax(md_slots + slot, static_cast<unsigned long long>(__double_as_longlong(disp)));
   }
 }
 
@@ -226,9 +217,10 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
       // Form A, fused: one sweep over the fan evaluates each triangle at the pass-start
       // position and at the candidate.  The ring entries are read from shared memory once and
       // v is swapped for the candidate in registers, halving the shared-memory traffic that
-      // bounds this kernel (L1 data-pipe wavefronts, profiles/).
+      // bounds this kernel (L1 data-pipe wavefronts, profiles/).  A tie needs neither.
+      const int sweep = tie ? 0 : deg;
 #pragma unroll 4
-      for (int j = 0; j < deg; ++j) {
+      for (int j = 0; j < sweep; ++j) {
         const uint32_t f = fan_at(j);
         const uint32_t i0 = fan_p(f, 0), i1 = fan_p(f, 1), i2 = fan_p(f, 2);
         const R2 q1 = at(i0), q2 = at(i1), q3 = at(i2);
@@ -301,7 +293,7 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
     }
     if (a.decision) a.decision[s] = acc ? 1 : 0;
   }
-  commit_stats<kBlock>(accepted, disp, a.pass_acc + pass, a.pass_md + pass);
+  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
 }
 
 // CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)
@@ -404,8 +396,9 @@ __global__ void __launch_bounds__(kHubBlock) hub_update(PassArgs<R, kSoA> a, int
     if (acc) {
       const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
       const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-      atomicAdd(a.pass_acc + pass, 1);
-      if (d > 0.0) atomicMax(a.pass_md + pass, static_cast<unsigned long long>(__double_as_longlong(d)));
+      const unsigned slot = pass * kStatSlots + (blockIdx.x & (kStatSlots - 1));
+      atomicAdd(a.slot_acc + slot, 1);
+      if (d > 0.0) atomicMax(a.slot_md + slot, static_cast<unsigned long long>(__double_as_longlong(d)));
     }
   }
 }
@@ -480,13 +473,31 @@ __global__ void __launch_bounds__(256) alpha_extrema(const R* __restrict__ alpha
   if (np) atomicAdd(nonpos, np);
 }
 
-__global__ void finalize_pass(PassState* st, const int32_t* pass_acc,
-                              const unsigned long long* pass_md, double tol_abs, int32_t max_iters,
-                              cudaGraphConditionalHandle handle, int32_t use_handle) {
-  if (!st->done) {
-    const int q = st->pass;
-    const int32_t acc = pass_acc[q];
-    const double md = __longlong_as_double(static_cast<long long>(pass_md[q]));
+// One warp: folds the pass's stat slots into pass_acc / pass_md, then lane 0 applies the
+// reference's stop rule and sets the WHILE condition.
+__global__ void finalize_pass(PassState* st, const int32_t* slot_acc, const unsigned long long* slot_md,
+                              int32_t* pass_acc, unsigned long long* pass_md, double tol_abs,
+                              int32_t max_iters, cudaGraphConditionalHandle handle, int32_t use_handle) {
+  const int lane = threadIdx.x;
+  const int q = st->pass;
+  const bool done = st->done != 0;
+  int32_t acc = 0;
+  unsigned long long mdb = 0;
+  if (!done) {
+    acc = slot_acc[q * kStatSlots + lane];
+    mdb = slot_md[q * kStatSlots + lane];
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, mdb, o);
+    mdb = other > mdb ? other : mdb;
+  }
+  if (lane != 0) return;
+  if (!done) {
+    pass_acc[q] = acc;
+    pass_md[q] = mdb;
+    const double md = __longlong_as_double(static_cast<long long>(mdb));
     st->pass = q + 1;
     if (acc == 0) {
       st->done = 1;
