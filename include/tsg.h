@@ -156,7 +156,7 @@ tsg_status tsg_pass_lockstep(tsg_mesh* mesh, int32_t form, int32_t chunks, int8_
  * kernels' fast alpha (refined reciprocal) and with the reference's IEEE division; returns the
  * maximum |fast - exact| over triangles with |exact| <= 1 and the count of non-finite fast
  * values.  newton_steps (1 or 2) selects the reciprocal refinement under test; the kernels'
- * fast path is only trusted outside a 2^-40 guard band (tsg_device.cuh). */
+ * fast path is only trusted outside a 2^-45 guard band (tsg_device.cuh). */
 tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_t newton_steps,
                               double* max_abs_err_out, int64_t* nonfinite_out);
 

@@ -140,7 +140,7 @@ __device__ __forceinline__ float rcp_refined(float x) {
 }
 
 // Decisions whose fast-path margin is within kGuard (absolute; |α| <= 1) are settled exactly.
-constexpr double kGuard = 0x1p-40;
+constexpr double kGuard = 0x1p-45;
 
 // triangle_alpha with the division replaced by the refined reciprocal; everything before the
 // division is the reference's exact operation sequence.  A degenerate triangle (es == 0 or a

@@ -256,7 +256,10 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
     } else if (!bad && hyp < thr - R(kGuard)) {
       acc = false;
     } else {
-      // Near-tie: the reference's exact values (IEEE division), same operand order.
+      // Near-tie: the reference's exact values (IEEE division, same operand order), needed only
+      // for triangles whose fast value lies within kGuard of the fast minimum: any other
+      // triangle is provably above the exact minimum (kGuard >= 2x the fast-path error).  With
+      // a non-finite fast value (degenerate triangle) every triangle is evaluated exactly.
       R thr_e = thr;
       if constexpr (!kTwoPhase) {
         thr_e = R(INFINITY);
@@ -269,7 +272,8 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
             q[c] = idx == kSelf ? pv
                    : (kFormB && ((fresh >> idx) & 1u)) ? P.load(nb[idx] & ~kFreshBit) : at(idx);
           }
-          thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
+          if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) <= thr + R(kGuard))
+            thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
         }
       }
       R hyp_e = R(INFINITY);
@@ -281,7 +285,8 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
           const uint32_t idx = fan_p(f, c);
           q[c] = idx == kSelf ? cand : at(idx);
         }
-        hyp_e = min_ref(hyp_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
+        if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) <= hyp + R(kGuard))
+          hyp_e = min_ref(hyp_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
       }
       acc = hyp_e > thr_e;
     }

@@ -244,8 +244,8 @@ def test_tri_alpha_and_extrema_device(capi, gpu_ctx, ts, port):
 
 
 def test_fast_alpha_error_is_far_inside_the_guard(gpu_ctx):
-    """The decision fast path (SFU reciprocal + 2 Newton steps) must stay far inside its 2^-40
-    guard band, otherwise a near-tie could be settled wrongly instead of falling back to IEEE
+    """The decision fast path (SFU reciprocal + 2 Newton steps) must stay far inside its 2^-45
+    guard band (8x margin), otherwise a near-tie could be settled wrongly instead of falling back to IEEE
     division.  (One Newton step measures ~2^-40 on this hardware: not enough, hence two.)"""
     err, nonfinite = gpu_ctx.selftest_alpha(1 << 22, 7, 2)
     assert err <= 2.0 ** -48, err
