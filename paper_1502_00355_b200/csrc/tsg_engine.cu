@@ -181,10 +181,6 @@ struct tsg_mesh {
   void* buf[2] = {nullptr, nullptr};
   void* init = nullptr;  // slot-ordered copy of the coordinates given at upload / set_coords
   uint16_t* d_fan16 = nullptr;
-  uint32_t* d_ell_nbr = nullptr;   // small tier, column-major ELL (see tsg_prep.hpp)
-  uint16_t* d_ell_fan = nullptr;
-  uint8_t* d_ell_deg = nullptr;
-  uint32_t* d_ell_nbr_fresh = nullptr;  // Form B copy for the cached chunk count
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
   int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr;
@@ -215,8 +211,6 @@ namespace {
 
 void free_form_b(tsg_mesh* m) {
   cudaFree(m->d_nbr_fresh);
-  cudaFree(m->d_ell_nbr_fresh);
-  m->d_ell_nbr_fresh = nullptr;
   cudaFree(m->d_fb_nodes);
   cudaFree(m->d_fb_hubs);
   cudaFree(m->d_fb_medium);
@@ -240,7 +234,6 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   cudaStream_t s = m->ctx->stream;
   tsg_status st;
   if ((st = upload(&m->d_nbr_fresh, sch.nbr_fresh, &b, s))) return st;
-  if ((st = upload(&m->d_ell_nbr_fresh, sch.ell_nbr_fresh, &b, s))) return st;
   if ((st = upload(&m->d_fb_nodes, sch.nodes, &b, s))) return st;
   if ((st = upload(&m->d_fb_hubs, sch.hubs, &b, s))) return st;
   if ((st = upload(&m->d_fb_medium, sch.medium, &b, s))) return st;
@@ -272,11 +265,6 @@ struct Engine {
     a.nbr = c.form == TSG_FORM_B ? m->d_nbr_fresh : m->d_nbr;
     a.fan = m->d_fan;
     a.fan16 = m->d_fan16;
-    a.ell_nbr = m->d_ell_nbr;
-    a.ell_nbr_fresh = m->d_ell_nbr_fresh;
-    a.ell_fan = m->d_ell_fan;
-    a.ell_deg = m->d_ell_deg;
-    a.ell_stride = m->hm.ell_stride;
     a.vinc_off = m->d_vinc_off;
     a.vinc = m->d_vinc;
     a.alpha = static_cast<const R*>(m->d_alpha);
@@ -329,7 +317,7 @@ struct Engine {
       Args a = base;
       a.list = medium;
       a.count = nmed;
-      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxMedDeg, kMedBlock, false>
+      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxMedDeg, kMedBlock>
           <<<static_cast<unsigned>((nmed + kMedBlock - 1) / kMedBlock), kMedBlock, 0, t>>>(a);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
@@ -338,7 +326,7 @@ struct Engine {
       Args a = base;
       a.list = small;
       a.count = ns;
-      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock, true>
+      tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock>
           <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
@@ -607,9 +595,6 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_nbr, hm.nbr, b, s))) return st;
   if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
   if ((st = upload(&m->d_fan16, hm.fan16, b, s))) return st;
-  if ((st = upload(&m->d_ell_nbr, hm.ell_nbr, b, s))) return st;
-  if ((st = upload(&m->d_ell_fan, hm.ell_fan, b, s))) return st;
-  if ((st = upload(&m->d_ell_deg, hm.ell_deg, b, s))) return st;
   if ((st = upload(&m->d_vinc_off, hm.vinc_off, b, s))) return st;
   if ((st = upload(&m->d_vinc, hm.vinc, b, s))) return st;
   if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
@@ -643,8 +628,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
   free_form_b(m);
-  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_ell_nbr,
-                  m->d_ell_fan, m->d_ell_deg, m->d_vinc_off, m->d_vinc,
+  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext};

@@ -34,11 +34,6 @@ struct PassArgs {
   const uint32_t* nbr;          // slots, ascending ORIGINAL id (| kFreshBit for Form B)
   const uint32_t* fan;          // hub fan records (i1, i2, k), same offsets as nbr
   const uint16_t* fan16;        // small-vertex fan records (p1, p2, p3 ring positions)
-  const uint32_t* ell_nbr;      // small tier, column-major ELL: entry j of slot s at j*stride+s
-  const uint32_t* ell_nbr_fresh;  // same with kFreshBit (Form B, current chunk count)
-  const uint16_t* ell_fan;
-  const uint8_t* ell_deg;       // small-tier valence per slot (0: pinned / other tier)
-  int64_t ell_stride;
   const uint32_t* vinc_off;     // TwoPhase: incident-triangle CSR over slots
   const uint32_t* vinc;
   const R* alpha;               // TwoPhase: pass-start α field (device triangle order)
@@ -92,10 +87,7 @@ __device__ __forceinline__ void commit_stats_warp(int accepted, double disp, int
 // reciprocal (|error| < 2^-50 on |α| <= 1); the strict test hyp > thr is settled from those
 // values whenever they are more than kGuard apart, and otherwise (rare: near-ties) every α of
 // the vertex is re-evaluated with IEEE division, exactly as the reference (quality.hpp:15-23).
-// kEll: the small tier reads its neighbour ids / fan records from the column-major ELL arrays
-// (entry j of slot s at j * ell_stride + s): warp loads are coalesced and no offset load sits
-// in front of them.  Otherwise rows come from the CSR (offset load, then row).
-template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg, int kBlock, bool kEll>
+template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg, int kBlock>
 __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(PassArgs<R, kSoA> a) {
   using O = Arith<R>;
   using R2 = typename O::R2;
@@ -108,27 +100,18 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
 
   // Topology loads do not depend on the pass state: issue them before waiting for it.
   int64_t s = 0;
+  uint32_t o0 = 0;
   int deg = 0;
-  const uint32_t* nb = nullptr;
-  const uint16_t* fan = nullptr;
-  int64_t stride = 1;
   if (i < a.count) {
     s = a.list ? static_cast<int64_t>(a.list[i]) : i;
-    if constexpr (kEll) {
-      deg = a.ell_deg[s];  // 0 for pinned vertices and the medium / hub tiers
-      nb = (kFormB ? a.ell_nbr_fresh : a.ell_nbr) + s;
-      fan = a.ell_fan + s;
-      stride = a.ell_stride;
-    } else {
-      const uint32_t o0 = a.off[s];
-      deg = static_cast<int>(a.off[s + 1] - o0);
-      if (deg > kMaxDeg) deg = 0;  // hub: handled by hub_update
-      nb = a.nbr + o0;
-      fan = a.fan16 + o0;
-    }
+    o0 = a.off[s];
+    deg = static_cast<int>(a.off[s + 1] - o0);
+    if (deg > kMaxDeg) deg = 0;  // hub: handled by hub_update
   }
   const PassState* st = a.st;
   const int2 state = *reinterpret_cast<const int2*>(st);  // {pass, done}
+  const uint32_t* nb = a.nbr + o0;
+  const uint16_t* fan = a.fan16 + o0;
 
   int accepted = 0;
   double disp = 0.0;
@@ -145,8 +128,8 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
       uint16_t f[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        u[j] = (base + j < deg) ? __ldg(nb + (base + j) * stride) : 0u;
-        f[j] = (base + j < deg) ? __ldg(fan + (base + j) * stride) : uint16_t{0};
+        u[j] = (base + j < deg) ? __ldg(nb + base + j) : 0u;
+        f[j] = (base + j < deg) ? __ldg(fan + base + j) : uint16_t{0};
       }
       if (base == 0) {
         if (state.y) return;  // stop rule fired (stream driver); uniform across the block
@@ -212,7 +195,7 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        const R2 now = N.load_mut(nb[j * stride] & ~kFreshBit);
+        const R2 now = N.load_mut(nb[j] & ~kFreshBit);
         const R2 was = at(j);
         view_moved |= (now.x != was.x) || (now.y != was.y);
         ring[j * kBlock + tid] = now;
@@ -287,7 +270,7 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(Pas
           for (int c = 0; c < 3; ++c) {
             const uint32_t idx = fan_p(f, c);
             q[c] = idx == kSelf ? pv
-                   : (kFormB && ((fresh >> idx) & 1u)) ? P.load(nb[idx * stride] & ~kFreshBit) : at(idx);
+                   : (kFormB && ((fresh >> idx) & 1u)) ? P.load(nb[idx] & ~kFreshBit) : at(idx);
           }
           if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) <= thr + R(kGuard))
             thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));

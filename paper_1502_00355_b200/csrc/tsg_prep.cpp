@@ -276,23 +276,6 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     if (tier == 1) hm.medium.push_back(static_cast<int32_t>(s));
     if (tier == 2) hm.hubs.push_back(static_cast<int32_t>(s));
   }
-
-  // Column-major ELL copy of the small tier (width small_max, stride nv rounded to 32).
-  hm.ell_stride = (nv + 31) / 32 * 32;
-  const size_t ell_n = static_cast<size_t>(tiers.small_max) * hm.ell_stride;
-  hm.ell_nbr.assign(ell_n, 0);
-  hm.ell_fan.assign(ell_n, 0);
-  hm.ell_deg.assign(hm.ell_stride, 0);
-  parallel_ranges(nv, [&](int64_t b, int64_t e) {
-    for (int64_t s = b; s < e; ++s) {
-      if (deg[s] == 0 || tiers.tier(deg[s]) != 0) continue;
-      hm.ell_deg[s] = static_cast<uint8_t>(deg[s]);
-      for (uint32_t j = 0; j < deg[s]; ++j) {
-        hm.ell_nbr[j * hm.ell_stride + s] = hm.nbr[hm.off[s] + j];
-        hm.ell_fan[j * hm.ell_stride + s] = hm.fan16[hm.off[s] + j];
-      }
-    }
-  });
   return "";
 }
 
@@ -322,10 +305,6 @@ std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers,
     level[v] = L;
     nlev = std::max(nlev, L + 1);
   }
-  out.ell_nbr_fresh = hm.ell_nbr;
-  for (int64_t s = 0; s < nv; ++s)
-    for (uint32_t j = 0; j < hm.ell_deg[s]; ++j)
-      out.ell_nbr_fresh[j * hm.ell_stride + s] = out.nbr_fresh[hm.off[s] + j];
   // counts[t][L + 1]: vertices of tier t on level L, then prefix sums -> list offsets
   std::vector<int64_t> counts[3];
   for (auto& c : counts) c.assign(nlev + 1, 0);

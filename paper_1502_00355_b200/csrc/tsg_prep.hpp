@@ -40,12 +40,6 @@ struct HostMesh {
   std::vector<uint32_t> nbr;      // slots
   std::vector<uint32_t> fan;      // hub rows: (i1, i2, k) records; small rows unused
   std::vector<uint16_t> fan16;    // small rows: ring positions of (p1, p2, p3), 5 bits each
-  // Small tier again, column-major ELL (entry j of slot s at j * ell_stride + s) so warp
-  // loads of entry j are coalesced and need no offset load.
-  int64_t ell_stride = 0;
-  std::vector<uint32_t> ell_nbr;
-  std::vector<uint16_t> ell_fan;
-  std::vector<uint8_t> ell_deg;
   std::vector<uint32_t> vinc_off; // nv+1, all vertices
   std::vector<uint32_t> vinc;     // device triangle ids
   std::vector<int32_t> tri;       // 3*nt device slots, device triangle order
@@ -63,7 +57,6 @@ struct Phase {
 struct FormBSchedule {
   int32_t chunks = 0;
   std::vector<uint32_t> nbr_fresh;  // nbr with kFreshBit on in-chunk lower-id neighbours
-  std::vector<uint32_t> ell_nbr_fresh;  // the same for the small tier's ELL copy
   std::vector<int32_t> nodes;       // small-degree slots grouped by level
   std::vector<int32_t> medium;      // medium-tier slots grouped by level
   std::vector<int32_t> hubs;        // hub slots grouped by level
