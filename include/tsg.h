@@ -151,6 +151,23 @@ tsg_status tsg_smooth_host(tsg_mesh* mesh, const double* xy_in, const tsg_smooth
 tsg_status tsg_pass_lockstep(tsg_mesh* mesh, int32_t form, int32_t chunks, int8_t* decision_out,
                              int32_t* accepted_out, double* max_disp_out);
 
+/* ---- multi-GPU partitions (one process per GPU; see paper_1502_00355_b200/distributed.py) ---- */
+/*
+ * One pass of `cfg` (form, strategy, chunks, swap; max_iters / driver / move_tol ignored) from
+ * the current device state, without the stop rule; returns this mesh's accepted count and max
+ * displacement.  The caller combines them across partitions and applies the stop rule.
+ */
+tsg_status tsg_pass(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, int32_t* accepted_out, double* max_disp_out);
+/* Halo plan in ORIGINAL (local) vertex numbering: send_ids are owned vertices other partitions
+ * read, recv_ids the locally pinned halo copies of other partitions' vertices (peer order). */
+tsg_status tsg_halo_plan(tsg_mesh* mesh, const int64_t* send_ids, int64_t n_send,
+                         const int64_t* recv_ids, int64_t n_recv);
+/* Packs the current coordinates of the send vertices into 2*n_send doubles, or writes 2*n_recv
+ * doubles into the halo vertices (both buffers).  *_is_host: 0 = device pointer (e.g. a buffer an
+ * NCCL all-to-all reads / writes), 1 = host pointer.  Synchronous on the context stream. */
+tsg_status tsg_halo_pack(tsg_mesh* mesh, double* out, int32_t out_is_host);
+tsg_status tsg_halo_unpack(tsg_mesh* mesh, const double* in, int32_t in_is_host);
+
 /* ---- diagnostics ---- */
 /* Evaluates n seeded random triangles (unit scale, tiny, huge, near-degenerate) with the
  * kernels' fast alpha (refined reciprocal) and with the reference's IEEE division; returns the

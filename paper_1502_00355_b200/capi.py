@@ -31,7 +31,8 @@ EXPORTS = (
     "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_mesh_restore_coords",
     "tsg_tri_alpha",
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
-    "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha",
+    "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_pass", "tsg_halo_plan",
+    "tsg_halo_pack", "tsg_halo_unpack",
 )
 
 
@@ -84,6 +85,10 @@ def lib() -> C.CDLL:
             "tsg_pass_lockstep": (i32, [P, i32, i32, P, P, P]),
             "tsg_hilbert_order": (i32, [i64, P, P]),
             "tsg_selftest_alpha": (i32, [P, i64, C.c_uint64, i32, P, P]),
+            "tsg_pass": (i32, [P, C.POINTER(SmoothCfg), P, P]),
+            "tsg_halo_plan": (i32, [P, P, i64, P, i64]),
+            "tsg_halo_pack": (i32, [P, C.c_void_p, i32]),
+            "tsg_halo_unpack": (i32, [P, C.c_void_p, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -235,3 +240,22 @@ class DeviceMesh:
         check(lib().tsg_pass_lockstep(self.h, FORM[form], chunks, _ptr(dec), C.byref(acc), C.byref(md)),
               "tsg_pass_lockstep")
         return dec, acc.value, md.value
+
+    # ---- multi-GPU partitions ----
+    def run_pass(self, cfg: SmoothCfg):
+        acc, md = C.c_int32(), C.c_double()
+        check(lib().tsg_pass(self.h, C.byref(cfg), C.byref(acc), C.byref(md)), "tsg_pass")
+        return acc.value, md.value
+
+    def halo_plan(self, send_ids, recv_ids):
+        self._send = np.ascontiguousarray(send_ids, dtype=np.int64)
+        self._recv = np.ascontiguousarray(recv_ids, dtype=np.int64)
+        check(lib().tsg_halo_plan(self.h, _ptr(self._send), len(self._send), _ptr(self._recv), len(self._recv)),
+              "tsg_halo_plan")
+
+    def halo_pack(self, out_ptr: int, on_host: bool):
+        """Writes 2*n_send doubles at out_ptr (device pointer, or host pointer if on_host)."""
+        check(lib().tsg_halo_pack(self.h, C.c_void_p(out_ptr), 1 if on_host else 0), "tsg_halo_pack")
+
+    def halo_unpack(self, in_ptr: int, on_host: bool):
+        check(lib().tsg_halo_unpack(self.h, C.c_void_p(in_ptr), 1 if on_host else 0), "tsg_halo_unpack")

@@ -95,6 +95,30 @@ __global__ void to_double_scatter(const R* __restrict__ in, const int64_t* __res
     out[order ? order[i] : i] = static_cast<double>(in[i]);
 }
 
+// Halo exchange: current coordinates of the send slots -> packed f64 pairs, and packed pairs
+// -> both buffers of the (locally pinned) halo slots.
+template <typename R, bool kSoA>
+__global__ void halo_pack(tsg::Coords<R, kSoA> cur, const int32_t* __restrict__ slots, int64_t n,
+                          double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const auto p = cur.load_mut(slots[i]);
+    out[2 * i] = static_cast<double>(p.x);
+    out[2 * i + 1] = static_cast<double>(p.y);
+  }
+}
+
+template <typename R, bool kSoA>
+__global__ void halo_unpack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1, const int32_t* __restrict__ slots,
+                            int64_t n, const double* __restrict__ in) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const auto p = tsg::Arith<R>::make(static_cast<R>(in[2 * i]), static_cast<R>(in[2 * i + 1]));
+    b0.store(slots[i], p);
+    b1.store(slots[i], p);
+  }
+}
+
 __global__ void scatter_i8(const int8_t* __restrict__ in, const int64_t* __restrict__ order,
                            int64_t n, int8_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -205,6 +229,11 @@ struct tsg_mesh {
   std::vector<tsg::Phase> fb_levels;
   int64_t fb_bytes = 0;
   GraphCache gc;
+  // Halo exchange plan (multi-GPU partitions): slots sent to / received from peers.
+  int32_t* d_send_slots = nullptr;
+  int32_t* d_recv_slots = nullptr;
+  int64_t n_send = 0, n_recv = 0;
+  double* d_halo_stage = nullptr;  // 2 * max(n_send, n_recv) doubles (host-pointer transfers)
 };
 
 namespace {
@@ -631,7 +660,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
-                  m->d_ext};
+                  m->d_ext, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
   for (void* p : ptrs) cudaFree(p);
   delete m;
   return TSG_OK;
@@ -927,6 +956,124 @@ tsg_status tsg_pass_lockstep(tsg_mesh* m, int32_t form, int32_t chunks, int8_t* 
   TSG_CUDA(cudaStreamSynchronize(s));
   if (accepted_out) *accepted_out = acc;
   if (max_disp_out) std::memcpy(max_disp_out, &md, sizeof(double));
+  return TSG_OK;
+}
+
+tsg_status tsg_pass(tsg_mesh* m, const tsg_smooth_cfg* c, int32_t* accepted_out, double* max_disp_out) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  tsg_status st = validate_cfg(c);
+  if (st) return st;
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  if (c->form == TSG_FORM_B && (st = ensure_form_b(m, c->chunks))) return st;
+  if ((st = ensure_stats_capacity(m, 2))) return st;
+  if (c->swap == TSG_SWAP_COPY) {
+    st = dispatch(m, [&](auto E) { return decltype(E)::normalize(m); });
+    if (st) return st;
+  }
+  const int32_t q = c->swap == TSG_SWAP_PINGPONG ? m->cur : 0;  // pass index = buffer parity
+  const tsg::PassState init{q, 0, 0, 0};
+  TSG_CUDA(cudaMemcpyAsync(m->d_state, &init, sizeof init, cudaMemcpyHostToDevice, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_sacc + q * tsg::kStatSlots, 0, sizeof(int32_t) * tsg::kStatSlots, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_smd + q * tsg::kStatSlots, 0, sizeof(unsigned long long) * tsg::kStatSlots, s));
+  tsg_smooth_cfg one = *c;
+  one.max_iters = q + 1;
+  one.driver = TSG_DRIVER_STREAM;
+  int64_t k = 0;
+  st = dispatch(m, [&](auto E) {
+    return decltype(E)::enqueue_pass(m, one, s, -1.0, cudaGraphConditionalHandle{}, 0, nullptr, nullptr,
+                                     nullptr, &k);
+  });
+  if (st) return st;
+  int32_t acc = 0;
+  unsigned long long md = 0;
+  TSG_CUDA(cudaMemcpyAsync(&acc, m->d_acc + q, sizeof acc, cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaMemcpyAsync(&md, m->d_md + q, sizeof md, cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  m->cur = c->swap == TSG_SWAP_PINGPONG ? (q ^ 1) : 0;
+  if (accepted_out) *accepted_out = acc;
+  if (max_disp_out) std::memcpy(max_disp_out, &md, sizeof(double));
+  return TSG_OK;
+}
+
+tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, const int64_t* recv_ids,
+                         int64_t n_recv) {
+  if (!m || n_send < 0 || n_recv < 0 || (n_send && !send_ids) || (n_recv && !recv_ids))
+    return fail(TSG_ERR_INVALID, "bad halo plan");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  std::vector<int32_t> ss(n_send), rs(n_recv);
+  for (int64_t i = 0; i < n_send; ++i) {
+    if (send_ids[i] < 0 || send_ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "send id out of range");
+    ss[i] = static_cast<int32_t>(m->hm.rank[send_ids[i]]);
+  }
+  for (int64_t i = 0; i < n_recv; ++i) {
+    if (recv_ids[i] < 0 || recv_ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "recv id out of range");
+    rs[i] = static_cast<int32_t>(m->hm.rank[recv_ids[i]]);
+  }
+  cudaFree(m->d_send_slots);
+  cudaFree(m->d_recv_slots);
+  cudaFree(m->d_halo_stage);
+  m->d_send_slots = m->d_recv_slots = nullptr;
+  m->d_halo_stage = nullptr;
+  int64_t b = 0;
+  tsg_status st;
+  if ((st = upload(&m->d_send_slots, ss, &b, m->ctx->stream))) return st;
+  if ((st = upload(&m->d_recv_slots, rs, &b, m->ctx->stream))) return st;
+  if ((st = dalloc(&m->d_halo_stage, 2 * std::max<int64_t>(1, std::max(n_send, n_recv)), &b))) return st;
+  TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  m->n_send = n_send;
+  m->n_recv = n_recv;
+  return TSG_OK;
+}
+
+tsg_status tsg_halo_pack(tsg_mesh* m, double* out, int32_t out_is_host) {
+  if (!m || (m->n_send && !out)) return fail(TSG_ERR_INVALID, "bad halo pack arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  if (m->n_send == 0) return TSG_OK;
+  double* dst = out_is_host ? m->d_halo_stage : out;
+  if (m->prec == TSG_F64) {
+    if (m->layout == TSG_LAYOUT_SOA)
+      halo_pack<double, true><<<grid_for(m->n_send, 256), 256, 0, s>>>(coords_of<double, true>(m, m->cur), m->d_send_slots, m->n_send, dst);
+    else
+      halo_pack<double, false><<<grid_for(m->n_send, 256), 256, 0, s>>>(coords_of<double, false>(m, m->cur), m->d_send_slots, m->n_send, dst);
+  } else {
+    if (m->layout == TSG_LAYOUT_SOA)
+      halo_pack<float, true><<<grid_for(m->n_send, 256), 256, 0, s>>>(coords_of<float, true>(m, m->cur), m->d_send_slots, m->n_send, dst);
+    else
+      halo_pack<float, false><<<grid_for(m->n_send, 256), 256, 0, s>>>(coords_of<float, false>(m, m->cur), m->d_send_slots, m->n_send, dst);
+  }
+  TSG_CUDA(cudaGetLastError());
+  if (out_is_host)
+    TSG_CUDA(cudaMemcpyAsync(out, dst, 2 * m->n_send * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  return TSG_OK;
+}
+
+tsg_status tsg_halo_unpack(tsg_mesh* m, const double* in, int32_t in_is_host) {
+  if (!m || (m->n_recv && !in)) return fail(TSG_ERR_INVALID, "bad halo unpack arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  if (m->n_recv == 0) return TSG_OK;
+  const double* src = in;
+  if (in_is_host) {
+    TSG_CUDA(cudaMemcpyAsync(m->d_halo_stage, in, 2 * m->n_recv * sizeof(double), cudaMemcpyHostToDevice, s));
+    src = m->d_halo_stage;
+  }
+  const unsigned g = grid_for(m->n_recv, 256);
+  if (m->prec == TSG_F64) {
+    if (m->layout == TSG_LAYOUT_SOA)
+      halo_unpack<double, true><<<g, 256, 0, s>>>(coords_of<double, true>(m, 0), coords_of<double, true>(m, 1), m->d_recv_slots, m->n_recv, src);
+    else
+      halo_unpack<double, false><<<g, 256, 0, s>>>(coords_of<double, false>(m, 0), coords_of<double, false>(m, 1), m->d_recv_slots, m->n_recv, src);
+  } else {
+    if (m->layout == TSG_LAYOUT_SOA)
+      halo_unpack<float, true><<<g, 256, 0, s>>>(coords_of<float, true>(m, 0), coords_of<float, true>(m, 1), m->d_recv_slots, m->n_recv, src);
+    else
+      halo_unpack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), m->d_recv_slots, m->n_recv, src);
+  }
+  TSG_CUDA(cudaGetLastError());
+  TSG_CUDA(cudaStreamSynchronize(s));
   return TSG_OK;
 }
 
