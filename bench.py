@@ -234,6 +234,79 @@ def run_reference_arm(args, cfg):
     print(json.dumps(out))
 
 
+def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
+    """N GPUs, one process each: the mesh is partitioned (Hilbert ranges + one-ring halos) and
+    every pass exchanges halos (NCCL all-to-all on device buffers) and all-reduces the stop
+    statistics — strong scaling of one mesh (paper_1502_00355_b200/distributed.py)."""
+    import paper_1502_00355_b200 as ts
+    from paper_1502_00355_b200 import capi, distributed as D
+
+    if cfg["form"] != "a":
+        raise SystemExit("partitioned multi-GPU runs support Form A (see DESIGN.md)")
+    xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
+    nv, nt = len(xy), len(tri)
+    t0 = time.time()
+    topo = ts.topology(nv, tri)
+    owner = D.owners_by_order(capi.hilbert_order(xy), world)
+    part = D.build_partition(rank, world, owner, xy, tri, topo)
+    ctx = capi.Context(dev_index)
+    eng = D.DeviceEngine(ctx, part, layout=cfg["layout"], precision=cfg["precision"])
+    device_buffers = args.transport == "nccl"
+    ex = D.Exchanger(part, device=device_buffers, torch_device=torch.device("cuda", dev_index))
+    prep_s = time.time() - t0
+    diag = ts.bbox_diagonal(xy)
+    passes = cfg["passes"]
+    scfg = capi.make_cfg(form="a", strategy=cfg["strategy"], swap=args.swap, max_iters=passes,
+                         move_tol=cfg["move_tol"], bbox_diag=diag)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev_index))
+
+    def step():
+        eng.mesh.restore_coords()
+        return D.smooth_partitioned(eng, ex, scfg, passes, cfg["move_tol"], diag)
+
+    for _ in range(args.warmup):
+        it, _, _, _ = step()
+    sampler = ClockSampler(dev_index)
+    sampler.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    updates = 0
+    for _ in range(args.steps):
+        it, _, _, _ = step()
+        updates += nv * it
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if device_buffers else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    value = updates / (elapsed_ms / 1000.0)  # whole-mesh node updates (every rank's share)
+    halo = torch.tensor([len(part.send_ids)], dtype=torch.int64, device="cuda" if device_buffers else "cpu")
+    dist.all_reduce(halo, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        out = {
+            "metric": "node-updates/sec (Smart Laplacian)", "value": value, "unit": "node-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": nt,
+                       "passes_per_step": passes, "form": "a", "layout": cfg["layout"],
+                       "parallelism": f"partitioned x{world} (Hilbert ranges, one-ring halo, "
+                                      f"{args.transport} all-to-all per pass)",
+                       "max_halo_vertices_per_rank": int(halo.item()), "generator_args": list(gargs)},
+            "ms_per_pass": elapsed_ms / max(1, args.steps * passes),
+            "roofline": None, "e2e": None, "cpu_baseline": None, "clocks": clocks,
+            "gpu_launches": None, "prep_s": prep_s,
+        }
+        print(json.dumps(out))
+    eng.mesh.free()
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -253,6 +326,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=2.0, help="reference arm: target seconds of passes per step")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no e2e / baseline")
+    ap.add_argument("--transport", choices=["nccl", "gloo"], default="nccl",
+                    help="N>1 halo exchange: NCCL device buffers (default) or gloo host buffers "
+                         "(lets N ranks share one GPU for testing)")
     args = ap.parse_args()
 
     cfg = dict(CONFIGS[args.config])
@@ -275,8 +351,16 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ndev = torch.cuda.device_count()
+        dev_index = local_rank % max(1, ndev)
+        torch.cuda.set_device(dev_index)
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
+        run_partitioned(args, cfg, rank, world, dev_index, dist, torch)
+        dist.destroy_process_group()
+        return
     import paper_1502_00355_b200 as ts
     from paper_1502_00355_b200 import capi
 
