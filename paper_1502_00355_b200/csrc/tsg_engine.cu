@@ -37,7 +37,7 @@ tsg_status fail(tsg_status code, const std::string& msg) {
 
 // Valence tiers: thread-per-vertex (<= 12, CTA of 128, every slot in Form A), thread-per-vertex
 // over a list (13..31, CTA of 64: larger per-thread ring), CTA-per-vertex hubs (>= 32).
-constexpr int kMaxSmallDeg = 12;
+constexpr int kMaxSmallDeg = 10;
 constexpr int kMaxMedDeg = 31;
 constexpr tsg::Tiers kTiers{kMaxSmallDeg, kMaxMedDeg};
 constexpr int kHubCap = 4096;     // hub entries staged in shared memory

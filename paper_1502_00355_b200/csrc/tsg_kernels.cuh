@@ -88,7 +88,7 @@ __device__ __forceinline__ void commit_stats_warp(int accepted, double disp, int
 // values whenever they are more than kGuard apart, and otherwise (rare: near-ties) every α of
 // the vertex is re-evaluated with IEEE division, exactly as the reference (quality.hpp:15-23).
 template <typename R, bool kSoA, bool kFormB, bool kTwoPhase, int kMaxDeg, int kBlock>
-__global__ void __launch_bounds__(kBlock, kBlock == 128 ? 7 : 4) node_update(PassArgs<R, kSoA> a) {
+__global__ void __launch_bounds__(kBlock, kBlock == 128 ? 8 : 4) node_update(PassArgs<R, kSoA> a) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr int kSelf = kMaxDeg;
