@@ -205,6 +205,7 @@ struct tsg_mesh {
   void* buf[2] = {nullptr, nullptr};
   void* init = nullptr;  // slot-ordered copy of the coordinates given at upload / set_coords
   uint16_t* d_fan16 = nullptr;
+  uint64_t* d_cyc = nullptr;
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
   int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr;
@@ -351,7 +352,15 @@ struct Engine {
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
-    if (ns > 0) {
+    if (ns > 0 && !kFormB && !kTwoPhase) {
+      Args a = base;
+      a.list = small;
+      a.count = ns;
+      tsg::ring_update<R, kSoA, kMaxSmallDeg, tsg::kNodeBlock>
+          <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a, m->d_cyc);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    } else if (ns > 0) {
       Args a = base;
       a.list = small;
       a.count = ns;
@@ -624,6 +633,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_nbr, hm.nbr, b, s))) return st;
   if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
   if ((st = upload(&m->d_fan16, hm.fan16, b, s))) return st;
+  if ((st = upload(&m->d_cyc, hm.cyc, b, s))) return st;
   if ((st = upload(&m->d_vinc_off, hm.vinc_off, b, s))) return st;
   if ((st = upload(&m->d_vinc, hm.vinc, b, s))) return st;
   if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
@@ -657,7 +667,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
   free_form_b(m);
-  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_vinc_off, m->d_vinc,
+  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_cyc, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};

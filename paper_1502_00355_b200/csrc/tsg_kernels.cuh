@@ -301,6 +301,215 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 8 : 4) node_update(Pas
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
 }
 
+// 1 / deg, the reference's reciprocal (smoothing.hpp:78), folded at compile time (IEEE, same
+// value as the run-time division) so the node kernels skip a division subroutine.
+struct InvDeg {
+  double d[kMaxInvDeg + 1];
+  float f[kMaxInvDeg + 1];
+};
+__constant__ constexpr InvDeg c_inv = [] {
+  InvDeg t{};
+  for (int i = 1; i <= kMaxInvDeg; ++i) {
+    t.d[i] = 1.0 / static_cast<double>(i);
+    t.f[i] = 1.0f / static_cast<float>(i);
+  }
+  return t;
+}();
+template <typename R>
+__device__ __forceinline__ R inv_deg(int deg) {
+  if constexpr (sizeof(R) == 8) {
+    return c_inv.d[deg];
+  } else {
+    return c_inv.f[deg];
+  }
+}
+
+// Per-neighbour quantities of the cycle sweep: q - v at the pass-start position and at the
+// candidate, and their squared lengths.
+template <typename R>
+struct RingEdge {
+  R qx, qy, px, py, cx, cy, lp, lc;
+};
+
+template <typename R>
+__device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typename Arith<R>::R2 pv,
+                                                 typename Arith<R>::R2 cand) {
+  RingEdge<R> e;
+  e.qx = q.x;
+  e.qy = q.y;
+  e.px = q.x - pv.x;
+  e.py = q.y - pv.y;
+  e.cx = q.x - cand.x;
+  e.cy = q.y - cand.y;
+  e.lp = fma(e.px, e.px, e.py * e.py);
+  e.lc = fma(e.cx, e.cx, e.cy * e.cy);
+  return e;
+}
+
+// Thread-per-vertex Form A fused update over the one-ring CYCLE (small tier).
+//
+// Every incident triangle of an interior manifold vertex is a rotation of (v, a, b) for
+// consecutive entries a -> b of its directed link cycle, so one sweep around the cycle visits
+// each triangle once while computing each neighbour's offsets from v (pass-start and
+// candidate) and their squared lengths once: α/K = ((a-v) x (b-v)) / (|a-v|^2 + |b-v|^2 +
+// |b-a|^2) for both positions of v, sharing |b-a|^2.  (The reference's triangle_alpha,
+// quality.hpp:15-23, is rotation invariant in exact arithmetic.)  This is the decision FILTER;
+// its error against the exact real value is < 6u (u = 2^-53) on α/K, the reference's own
+// evaluation differs from the real value by < 14u on α, so whenever the fast thr and hyp are
+// more than kGuard (>> 2 * 10u) apart the strict test hyp > thr has the reference's outcome.
+// Near-ties (and degenerate triangles) are settled with the reference's literal evaluation
+// over the fan records, exactly as node_update does.
+//
+// Neighbour coordinates are gathered in ascending ORIGINAL id (the summation order of
+// neighbor_mean, smoothing.hpp:72-80) into a per-thread shared-memory slice, then read back in
+// cycle order.  Vertices whose link is not a single directed cycle (cyc == kNoCycle) use the
+// fan records for the fast sweep as well.
+template <typename R, bool kSoA, int kMaxDeg, int kBlock>
+__global__ void __launch_bounds__(kBlock, 8) ring_update(PassArgs<R, kSoA> a, const uint64_t* __restrict__ cycw) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  constexpr int kSelf = kMaxDeg;
+  constexpr bool kExact = sizeof(R) == 8;
+  static_assert(kMaxDeg <= 15, "cycle words hold deg + 1 <= 16 nibbles");
+  __shared__ R2 ring[kMaxDeg * kBlock];
+  const int tid = threadIdx.x;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + tid;
+
+  int64_t s = 0;
+  uint32_t o0 = 0;
+  int deg = 0;
+  uint64_t cyc = ~0ull;
+  if (i < a.count) {
+    s = a.list ? static_cast<int64_t>(a.list[i]) : i;
+    o0 = __ldg(a.off + s);
+    deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
+    if (deg > kMaxDeg) deg = 0;  // medium / hub tiers
+    if (deg > 0) cyc = __ldg(cycw + s);
+  }
+  const int2 state = *reinterpret_cast<const int2*>(a.st);  // {pass, done}
+  if (state.y) return;  // stop rule fired (stream driver); uniform across the grid
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+  const uint32_t* nb = a.nbr + o0;
+
+  int accepted = 0;
+  double disp = 0.0;
+  if (deg > 0) {
+    const R2 pv = P.load(s);
+    R sx = R(0), sy = R(0);
+#pragma unroll
+    for (int base = 0; base < kMaxDeg; base += 8) {
+      if (base < deg) {
+        uint32_t u[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = (base + j < deg) ? __ldg(nb + base + j) : 0u;
+        R2 c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (base + j < deg) c[j] = P.load(u[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (base + j < deg) {
+            ring[(base + j) * kBlock + tid] = c[j];
+            sx = O::add(sx, c[j].x);
+            sy = O::add(sy, c[j].y);
+          }
+        }
+      }
+    }
+    auto at = [&](uint32_t idx) -> R2 { return ring[idx * kBlock + tid]; };
+    const uint16_t* fan = a.fan16 + o0;
+    const R inv = inv_deg<R>(deg);
+    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    // Exact tie (candidate == position; Form A reads only pass-start values): every
+    // hypothetical α equals its threshold α bit for bit, the strict test fails.
+    const bool tie = cand.x == pv.x && cand.y == pv.y;
+    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+    if (!tie) {
+      if (cyc != ~0ull) {
+        RingEdge<R> ea = ring_edge<R>(at(static_cast<uint32_t>(cyc & 15u)), pv, cand);
+#pragma unroll 2
+        for (int j = 1; j <= deg; ++j) {
+          const RingEdge<R> eb = ring_edge<R>(at(static_cast<uint32_t>((cyc >> (4 * j)) & 15u)), pv, cand);
+          const R ex = eb.qx - ea.qx, ey = eb.qy - ea.qy;
+          const R lab = fma(ex, ex, ey * ey);
+          const R cp = fma(ea.px, eb.py, -(ea.py * eb.px));
+          const R cc = fma(ea.cx, eb.cy, -(ea.cy * eb.cx));
+          R tp = cp * rcp_refined<2>(ea.lp + eb.lp + lab);
+          R tc = cc * rcp_refined<2>(ea.lc + eb.lc + lab);
+          if constexpr (!kExact) {
+            tp = isfinite(tp) ? tp : R(0);
+            tc = isfinite(tc) ? tc : R(0);
+          }
+          nan_acc = nan_acc + (tp + tc);
+          thr = fmin(thr, tp);
+          hyp = fmin(hyp, tc);
+          ea = eb;
+        }
+      } else {
+        // No single link cycle: literal triangles from the fan records (α/K scale as above).
+        constexpr R kInvK = R(1) / Arith<R>::kAlpha;
+        for (int j = 0; j < deg; ++j) {
+          const uint32_t f = __ldg(fan + j);
+          const uint32_t i0 = fan_p(f, 0), i1 = fan_p(f, 1), i2 = fan_p(f, 2);
+          const R2 q1 = i0 == kSelf ? pv : at(i0), q2 = i1 == kSelf ? pv : at(i1), q3 = i2 == kSelf ? pv : at(i2);
+          const R2 c1 = i0 == kSelf ? cand : q1, c2 = i1 == kSelf ? cand : q2, c3 = i2 == kSelf ? cand : q3;
+          R t = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y) * kInvK;
+          R h = alpha_fast<R>(c1.x, c1.y, c2.x, c2.y, c3.x, c3.y) * kInvK;
+          if constexpr (!kExact) {
+            t = isfinite(t) ? t : R(0);
+            h = isfinite(h) ? h : R(0);
+          }
+          nan_acc = nan_acc + (t + h);
+          thr = fmin(thr, t);
+          hyp = fmin(hyp, h);
+        }
+      }
+    }
+    const bool bad = !(fabs(nan_acc) < R(1e30));
+    bool acc;
+    if (tie) {
+      acc = false;
+    } else if constexpr (!kExact) {
+      acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
+    } else if (!bad && hyp > thr + R(kGuard)) {
+      acc = true;
+    } else if (!bad && hyp < thr - R(kGuard)) {
+      acc = false;
+    } else {
+      // Near-tie: the reference's literal evaluation (IEEE division, same operand order) of
+      // the triangles whose fast value lies within kGuard of the fast minimum (all of them when
+      // some fast value is not finite).
+      constexpr R kInvK = R(1) / Arith<R>::kAlpha;
+      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = __ldg(fan + j);
+        R2 q[3], c[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const uint32_t idx = fan_p(f, k);
+          q[k] = idx == kSelf ? pv : at(idx);
+          c[k] = idx == kSelf ? cand : q[k];
+        }
+        if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK <= thr + R(kGuard))
+          thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
+        if (bad || alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK <= hyp + R(kGuard))
+          hyp_e = min_ref(hyp_e, alpha_plain<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y));
+      }
+      acc = hyp_e > thr_e;
+    }
+    N.store(s, acc ? cand : pv);
+    if (acc) {
+      accepted = 1;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+    }
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+  }
+  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+}
+
 // CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)
 // by `cap` view pairs; entries beyond cap are read from global memory.
 template <typename R, bool kSoA, bool kFormB, bool kTwoPhase>

@@ -178,6 +178,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   hm.nbr.assign(total, 0);
   hm.fan.assign(total, 0);
   hm.fan16.assign(total, 0);
+  hm.cyc.assign(nv, kNoCycle);
 
   // Device triangle order: identity, or by the smallest slot among the corners (stable) so
   // that the triangle kernels stream coordinates in the same locality order as the vertices.
@@ -219,6 +220,11 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
       uint32_t* out_n = hm.nbr.data() + hm.off[s];
       uint32_t* out_f = hm.fan.data() + hm.off[s];
       for (int32_t j = 0; j < n; ++j) out_n[j] = static_cast<uint32_t>(hm.rank[row[j]]);
+      const bool want_cycle = tiers.tier(static_cast<uint32_t>(n)) == 0 && n <= kMaxCycleDeg;
+      int8_t succ[kMaxCycleDeg], indeg[kMaxCycleDeg];
+      bool cycle_ok = want_cycle;
+      if (want_cycle)
+        for (int32_t j = 0; j < n; ++j) succ[j] = -1, indeg[j] = 0;
       for (int64_t i = d.inc_off[v], j = 0; i < d.inc_off[v + 1]; ++i, ++j) {
         const int32_t* tv = d.tri + 3 * static_cast<int64_t>(d.inc[i]);
         const int k = tv[0] == v ? 0 : tv[1] == v ? 1 : 2;
@@ -230,6 +236,14 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
           return;
         }
         const uint32_t ia = static_cast<uint32_t>(pa - row), ic = static_cast<uint32_t>(pc - row);
+        if (cycle_ok) {  // triangle = rotation of (v, a, c): directed link edge ia -> ic
+          if (succ[ia] >= 0 || indeg[ic] > 0) {
+            cycle_ok = false;
+          } else {
+            succ[ia] = static_cast<int8_t>(ic);
+            indeg[ic] = 1;
+          }
+        }
         const int tier = tiers.tier(static_cast<uint32_t>(n));
         if (tier < 2) {
           // ring positions of (p1, p2, p3); v itself is the entry after the tier's last
@@ -241,6 +255,17 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
         } else {
           out_f[j] = fan_pack_h(ia, ic, static_cast<uint32_t>(k));
         }
+      }
+      if (cycle_ok) {
+        // Single directed cycle through all n positions, starting at position 0.
+        uint64_t w = 0;
+        int32_t p = 0, steps = 0;
+        do {
+          w |= static_cast<uint64_t>(p) << (4 * steps);
+          p = succ[p];
+          ++steps;
+        } while (p > 0 && steps < n);
+        if (p == 0 && steps == n) hm.cyc[s] = w;  // nibble n (= n_0 = 0) is already 0
       }
     }
   });

@@ -31,6 +31,9 @@ struct Tiers {
   }
 };
 
+constexpr uint64_t kNoCycle = ~uint64_t{0};
+constexpr int kMaxCycleDeg = 15;  // deg + 1 nibbles in 64 bits
+
 struct HostMesh {
   int64_t nv = 0, nt = 0;
   std::vector<int64_t> order;     // slot -> original vertex
@@ -40,6 +43,11 @@ struct HostMesh {
   std::vector<uint32_t> nbr;      // slots
   std::vector<uint32_t> fan;      // hub rows: (i1, i2, k) records; small rows unused
   std::vector<uint16_t> fan16;    // small rows: ring positions of (p1, p2, p3), 5 bits each
+  // Small rows: the one-ring as a directed cycle, 4-bit row positions n_0..n_deg (n_deg = n_0)
+  // such that every incident triangle is a rotation of (v, row[n_j], row[n_j+1]).  kNoCycle
+  // when the link of v is not a single directed cycle (bow-tie / inconsistent orientation) or
+  // the row is not in the small tier; those vertices use the fan records.
+  std::vector<uint64_t> cyc;
   std::vector<uint32_t> vinc_off; // nv+1, all vertices
   std::vector<uint32_t> vinc;     // device triangle ids
   std::vector<int32_t> tri;       // 3*nt device slots, device triangle order

@@ -142,6 +142,33 @@ def test_single_fan_hub_beyond_shared_memory(capi, gpu_ctx, ts, port, n):
         dm.free()
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mixed_orientation_and_bowtie_links_vs_oracle(capi, gpu_ctx, ts, port, seed):
+    """Vertices whose link is not one directed cycle (flipped triangles, a bow-tie vertex shared by
+    two fans) take the fan-record sweep of the small tier; the rest take the cycle sweep."""
+    rng = np.random.default_rng(seed)
+    xy, tri = ts.delaunay_arrays(6000, 70 + seed)
+    tri = tri.copy()
+    flip = rng.random(len(tri)) < 0.05
+    tri[flip] = tri[flip][:, [0, 2, 1]]
+    # bow-tie: two separate 4-fans glued at one centre vertex (interior: every edge twice)
+    c = len(xy)
+    ring = [(0.5 + 0.02 * np.cos(t), 2.5 + 0.02 * np.sin(t)) for t in np.linspace(0, 2 * np.pi, 5)[:-1]]
+    ring2 = [(0.501 + 0.03 * np.cos(t), 2.5 + 0.03 * np.sin(t)) for t in np.linspace(0.3, 2 * np.pi + 0.3, 5)[:-1]]
+    xy = np.vstack([xy, [[0.501, 2.499]], ring, ring2])
+    extra = [[c, c + 1 + k, c + 1 + (k + 1) % 4] for k in range(4)] + \
+            [[c, c + 5 + k, c + 5 + (k + 1) % 4] for k in range(4)]
+    tri = np.vstack([tri, np.array(extra, np.int32)]).astype(np.int32)
+    want = port.smooth(xy, tri, form="a", max_iters=25, move_tol=0.0)
+    assert want.accepted[0] > 0
+    for layout, reorder in (("aos", True), ("soa", False)):
+        dm, got = run_capi(capi, gpu_ctx, ts, xy, tri, "a", max_iters=25, layout=layout, reorder=reorder)
+        assert np.array_equal(got["accepted"], want.accepted)
+        assert np.array_equal(got["max_disp"].view(np.uint64), want.max_disp.view(np.uint64))
+        assert np.array_equal(got["xy"].view(np.uint64), want.xy.view(np.uint64))
+        dm.free()
+
+
 def test_edge_cases(capi, gpu_ctx, ts, port):
     # all-boundary meshes: one pass, no moves (proj/tests/test_smoothing.cpp:142-152)
     for xy, tri in ((np.array([[0, 0], [1, 0], [0, 1]], float), np.array([[0, 1, 2]], np.int32)),
