@@ -175,7 +175,9 @@ __device__ __forceinline__ int fan_k(uint32_t f) { return static_cast<int>(f >> 
 // Small-vertex fan record: ring positions of p1, p2, p3 (5 bits each; kMaxDeg = v itself).
 __device__ __forceinline__ uint32_t fan_p(uint32_t f, int c) { return (f >> (5 * c)) & 31u; }
 
-constexpr int kMaxInvDeg = 32;  // 1/deg table (thread-per-vertex tiers)
+constexpr int kMaxInvDeg = 32;
+constexpr int kTile = 1024;               // tile_update: slots per CTA (= tsg_prep.hpp kTile)
+constexpr uint32_t kNoLocalDev = 0xffffu;  // = tsg_prep.hpp kNoLocal  // 1/deg table (thread-per-vertex tiers)
 
 constexpr uint32_t kFreshBit = 0x80000000u;  // Form B: read this neighbour from N (live)
 

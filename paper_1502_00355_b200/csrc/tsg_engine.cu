@@ -41,6 +41,8 @@ constexpr int kMaxSmallDeg = 10;
 constexpr int kMaxMedDeg = 31;
 constexpr tsg::Tiers kTiers{kMaxSmallDeg, kMaxMedDeg};
 constexpr int kHubCap = 4096;     // hub entries staged in shared memory
+constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
+constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
 template <class T>
 tsg_status dalloc(T** p, size_t count, int64_t* bytes) {
@@ -208,7 +210,7 @@ struct tsg_mesh {
   uint64_t* d_cyc = nullptr;
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
-  int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr;
+  int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr, *d_cyc_mid = nullptr, *d_large = nullptr;
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   void* d_alpha = nullptr;
   double* d_xy_stage = nullptr;  // 2*nv original-order doubles
@@ -352,20 +354,66 @@ struct Engine {
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
-    if (ns > 0 && !kFormB && !kTwoPhase) {
-      Args a = base;
-      a.list = small;
-      a.count = ns;
-      tsg::ring_update<R, kSoA, kMaxSmallDeg, tsg::kNodeBlock>
-          <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a, m->d_cyc);
-      TSG_CUDA(cudaGetLastError());
-      ++*kernels;
-    } else if (ns > 0) {
+    if (ns > 0) {
       Args a = base;
       a.list = small;
       a.count = ns;
       tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock>
           <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    if (fork) {
+      cudaEvent_t e;
+      tsg_status st = next_event(ctx, &e);
+      if (st) return st;
+      TSG_CUDA(cudaEventRecord(e, ctx->side));
+      TSG_CUDA(cudaStreamWaitEvent(s, e, 0));
+    }
+    return TSG_OK;
+  }
+
+  // Form A, fused: cycle sweep (thread per vertex) over every slot with deg <= kMaxSmallDeg and
+  // over the 11..15 list, warp per vertex above.  The list tiers run on the side stream.
+  static tsg_status launch_form_a_fused(tsg_mesh* m, const Args& base, cudaStream_t s, int64_t* kernels) {
+    tsg_context* ctx = m->ctx;
+    const int64_t nv = m->hm.nv, nmid = static_cast<int64_t>(m->hm.cyc_mid.size()),
+                  nlarge = static_cast<int64_t>(m->hm.large.size());
+    const bool fork = nmid > 0 || nlarge > 0;
+    cudaStream_t t = s;
+    if (fork) {
+      cudaEvent_t e;
+      tsg_status st = next_event(ctx, &e);
+      if (st) return st;
+      TSG_CUDA(cudaEventRecord(e, s));
+      TSG_CUDA(cudaStreamWaitEvent(ctx->side, e, 0));
+      t = ctx->side;
+    }
+    if (nlarge > 0) {
+      Args a = base;
+      a.list = m->d_large;
+      a.count = nlarge;
+      tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>
+          <<<static_cast<unsigned>((nlarge + kWarpTierWarps - 1) / kWarpTierWarps), kWarpTierWarps * 32, 0, t>>>(a);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    if (nmid > 0) {
+      constexpr int kB = 64;
+      Args a = base;
+      a.list = m->d_cyc_mid;
+      a.count = nmid;
+      tsg::ring_update<R, kSoA, tsg::kMaxCycleDeg, kMaxMedDeg, kB>
+          <<<static_cast<unsigned>((nmid + kB - 1) / kB), kB, 0, t>>>(a, m->d_cyc);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    {
+      Args a = base;
+      a.list = nullptr;
+      a.count = nv;
+      tsg::ring_update<R, kSoA, kMaxSmallDeg, kMaxSmallDeg, tsg::kNodeBlock>
+          <<<static_cast<unsigned>((nv + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a, m->d_cyc);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
@@ -399,7 +447,10 @@ struct Engine {
     base.decision = decision;
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
     if (ev_begin) TSG_CUDA(cudaEventRecord(ev_begin, s));
-    if (!kFormB) {
+    if (!kFormB && !kTwoPhase) {
+      tsg_status st = launch_form_a_fused(m, base, s, kernels);
+      if (st) return st;
+    } else if (!kFormB) {
       tsg_status st = launch_phase<false, kTwoPhase>(m, base, nullptr, nv, m->d_medium,
                                                      static_cast<int64_t>(m->hm.medium.size()), m->d_hubs,
                                                      static_cast<int64_t>(m->hm.hubs.size()),
@@ -639,6 +690,8 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
   if ((st = upload(&m->d_hubs, hm.hubs, b, s))) return st;
   if ((st = upload(&m->d_medium, hm.medium, b, s))) return st;
+  if ((st = upload(&m->d_cyc_mid, hm.cyc_mid, b, s))) return st;
+  if ((st = upload(&m->d_large, hm.large, b, s))) return st;
   if (d->order) {
     if ((st = upload(&m->d_order, hm.order, b, s))) return st;
     if ((st = upload(&m->d_tri_order, hm.tri_order, b, s))) return st;
@@ -668,7 +721,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   m->gc.reset();
   free_form_b(m);
   void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_cyc, m->d_vinc_off, m->d_vinc,
-                  m->d_tri, m->d_hubs, m->d_medium, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
+                  m->d_tri, m->d_hubs, m->d_medium, m->d_cyc_mid, m->d_large, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
   for (void* p : ptrs) cudaFree(p);

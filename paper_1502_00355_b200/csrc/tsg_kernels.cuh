@@ -364,11 +364,13 @@ __device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typena
 // neighbor_mean, smoothing.hpp:72-80) into a per-thread shared-memory slice, then read back in
 // cycle order.  Vertices whose link is not a single directed cycle (cyc == kNoCycle) use the
 // fan records for the fast sweep as well.
-template <typename R, bool kSoA, int kMaxDeg, int kBlock>
-__global__ void __launch_bounds__(kBlock, 8) ring_update(PassArgs<R, kSoA> a, const uint64_t* __restrict__ cycw) {
+//
+// kSelf is v's position in the fan16 records of the rows this instance serves (the tier's
+// maximum valence, tsg_prep.cpp).
+template <typename R, bool kSoA, int kMaxDeg, int kSelf, int kBlock>
+__global__ void __launch_bounds__(kBlock, 1024 / kBlock) ring_update(PassArgs<R, kSoA> a, const uint64_t* __restrict__ cycw) {
   using O = Arith<R>;
   using R2 = typename O::R2;
-  constexpr int kSelf = kMaxDeg;
   constexpr bool kExact = sizeof(R) == 8;
   static_assert(kMaxDeg <= 15, "cycle words hold deg + 1 <= 16 nibbles");
   __shared__ R2 ring[kMaxDeg * kBlock];
@@ -506,6 +508,336 @@ __global__ void __launch_bounds__(kBlock, 8) ring_update(PassArgs<R, kSoA> a, co
       disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
     }
     if (a.decision) a.decision[s] = acc ? 1 : 0;
+  }
+  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+}
+
+// Tile arrays (tsg_prep.hpp build_tiles).
+struct TileArgs {
+  const uint32_t* meta;      // per slot: record offset in the tile (16-byte units) | deg << 16
+  const uint4* rec;          // records, 16-byte units
+  const uint32_t* tile_rec;  // ntiles + 1
+  const uint32_t* ext_off;   // ntiles + 1
+  const uint32_t* ext;       // external slots
+  int32_t ext_cap;           // external entries staged in shared memory per tile
+  int32_t rec_cap;           // record units staged in shared memory per tile
+  int64_t nv;
+};
+
+template <typename R>
+__host__ __device__ constexpr size_t tile_smem_bytes(int tile, int ext_cap, int rec_cap) {
+  return sizeof(typename Arith<R>::R2) * (tile + ext_cap) + 16 * static_cast<size_t>(rec_cap) +
+         4 * static_cast<size_t>(tile);
+}
+
+// Tile-staged thread-per-vertex Form A fused update (small tier, deg <= kMaxDeg).
+//
+// One CTA owns kTile consecutive slots (a Hilbert-compact patch, degree-sorted inside).  It
+// first stages, with coalesced loads, the patch's pass-start coordinates, the coordinates of
+// the external slots its rows reference, the rows' local-index records and the per-slot meta
+// words into shared memory; after one barrier every gather is a shared-memory read.  Record
+// word j of a row = (row[j], cycle[j]) local indices: row[] in ascending ORIGINAL id (the
+// summation order of neighbor_mean, smoothing.hpp:72-80), cycle[] the directed link cycle
+// (every incident triangle is a rotation of (v, cycle[j], cycle[j+1])).  The decision
+// arithmetic is ring_update's: fast α/K filter over the cycle, exact literal evaluation over
+// the fan records for near-ties and for rows without a link cycle.
+template <typename R, bool kSoA, int kThreads, int kMaxDeg>
+__global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  constexpr int kSelf = kMaxDeg;  // v's position in the small tier's fan16 records
+  constexpr bool kExact = sizeof(R) == 8;
+  constexpr int kWords = (kMaxDeg + 3) / 4 * 4;
+  static_assert(kTile % kThreads == 0, "whole vertices per thread");
+  extern __shared__ __align__(16) unsigned char tile_smem[];
+  R2* pts = reinterpret_cast<R2*>(tile_smem);
+  uint4* recs = reinterpret_cast<uint4*>(pts + kTile + t.ext_cap);
+  uint32_t* meta_s = reinterpret_cast<uint32_t*>(recs + t.rec_cap);
+
+  const int tid = threadIdx.x;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
+  const int n_in = static_cast<int>(t.nv - base < kTile ? t.nv - base : kTile);
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+
+  const uint32_t e0 = __ldg(t.ext_off + blockIdx.x), ne = __ldg(t.ext_off + blockIdx.x + 1) - e0;
+  const uint32_t r0 = __ldg(t.tile_rec + blockIdx.x), nr = __ldg(t.tile_rec + blockIdx.x + 1) - r0;
+  const int n_ext = static_cast<int>(ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
+  const int n_rec = static_cast<int>(nr < static_cast<uint32_t>(t.rec_cap) ? nr : t.rec_cap);
+  for (int i = tid; i < n_in; i += kThreads) {
+    pts[i] = P.load(base + i);
+    meta_s[i] = __ldg(t.meta + base + i);
+  }
+  for (int k = tid; k < n_ext; k += kThreads) pts[kTile + k] = P.load(__ldg(t.ext + e0 + k));
+  for (int k = tid; k < n_rec; k += kThreads) recs[k] = __ldg(t.rec + r0 + k);
+  __syncthreads();
+
+  auto get = [&](uint32_t l) -> R2 {
+    return l < static_cast<uint32_t>(kTile + t.ext_cap) ? pts[l] : P.load(__ldg(t.ext + e0 + l - kTile));
+  };
+  auto rec_word = [&](uint32_t unit, int j) -> uint32_t {  // any unit, any j (rare paths)
+    const uint32_t u = unit + static_cast<uint32_t>(j >> 2);
+    const uint4 v = u < static_cast<uint32_t>(t.rec_cap) ? recs[u] : __ldg(t.rec + r0 + u);
+    const int c = j & 3;
+    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+  };
+
+  int accepted = 0;
+  double disp = 0.0;
+#pragma unroll 1
+  for (int i = tid; i < n_in; i += kThreads) {
+    const uint32_t meta = meta_s[i];
+    const int deg = static_cast<int>(meta >> 16);
+    if (deg == 0) continue;  // pinned, or a medium / warp tier row
+    const uint32_t unit = meta & 0xffffu;
+    uint32_t w[kWords];
+#pragma unroll
+    for (int q = 0; q < kWords / 4; ++q) {
+      if (4 * q < deg) {
+        const uint32_t u = unit + q;
+        const uint4 v = u < static_cast<uint32_t>(t.rec_cap) ? recs[u] : __ldg(t.rec + r0 + u);
+        w[4 * q] = v.x;
+        w[4 * q + 1] = v.y;
+        w[4 * q + 2] = v.z;
+        w[4 * q + 3] = v.w;
+      } else {
+        w[4 * q] = w[4 * q + 1] = w[4 * q + 2] = w[4 * q + 3] = 0u;
+      }
+    }
+    const R2 pv = pts[i];
+    R sx = R(0), sy = R(0);
+#pragma unroll
+    for (int j = 0; j < kMaxDeg; ++j) {
+      if (j < deg) {
+        const R2 c = get(w[j] & 0xffffu);
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
+    }
+    const R inv = inv_deg<R>(deg);
+    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    const bool tie = cand.x == pv.x && cand.y == pv.y;
+    const int64_t s = base + i;
+    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+    if (!tie) {
+      if ((w[0] >> 16) != kNoLocalDev) {
+        RingEdge<R> ea = ring_edge<R>(get(w[0] >> 16), pv, cand);
+#pragma unroll
+        for (int j = 1; j <= kMaxDeg; ++j) {
+          if (j <= deg) {
+            const uint32_t l = (j < deg ? w[j < kMaxDeg ? j : 0] : w[0]) >> 16;
+            const RingEdge<R> eb = ring_edge<R>(get(l), pv, cand);
+            const R ex = eb.qx - ea.qx, ey = eb.qy - ea.qy;
+            const R lab = fma(ex, ex, ey * ey);
+            const R cp = fma(ea.px, eb.py, -(ea.py * eb.px));
+            const R cc = fma(ea.cx, eb.cy, -(ea.cy * eb.cx));
+            R tp = cp * rcp_refined<2>(ea.lp + eb.lp + lab);
+            R tc = cc * rcp_refined<2>(ea.lc + eb.lc + lab);
+            if constexpr (!kExact) {
+              tp = isfinite(tp) ? tp : R(0);
+              tc = isfinite(tc) ? tc : R(0);
+            }
+            nan_acc = nan_acc + (tp + tc);
+            thr = fmin(thr, tp);
+            hyp = fmin(hyp, tc);
+            ea = eb;
+          }
+        }
+      } else {
+        // No single link cycle: literal triangles from the fan records (α/K scale).
+        constexpr R kInvK = R(1) / Arith<R>::kAlpha;
+        const uint16_t* fan = a.fan16 + __ldg(a.off + s);
+        for (int j = 0; j < deg; ++j) {
+          const uint32_t f = __ldg(fan + j);
+          R2 q[3], c[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const uint32_t p = fan_p(f, k);
+            q[k] = p == kSelf ? pv : get(rec_word(unit, static_cast<int>(p)) & 0xffffu);
+            c[k] = p == kSelf ? cand : q[k];
+          }
+          R tq = alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK;
+          R th = alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK;
+          if constexpr (!kExact) {
+            tq = isfinite(tq) ? tq : R(0);
+            th = isfinite(th) ? th : R(0);
+          }
+          nan_acc = nan_acc + (tq + th);
+          thr = fmin(thr, tq);
+          hyp = fmin(hyp, th);
+        }
+      }
+    }
+    const bool bad = !(fabs(nan_acc) < R(1e30));
+    bool acc;
+    if (tie) {
+      acc = false;
+    } else if constexpr (!kExact) {
+      acc = hyp > thr;
+    } else if (!bad && hyp > thr + R(kGuard)) {
+      acc = true;
+    } else if (!bad && hyp < thr - R(kGuard)) {
+      acc = false;
+    } else {
+      constexpr R kInvK = R(1) / Arith<R>::kAlpha;
+      const uint16_t* fan = a.fan16 + __ldg(a.off + s);
+      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = __ldg(fan + j);
+        R2 q[3], c[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const uint32_t p = fan_p(f, k);
+          q[k] = p == kSelf ? pv : get(rec_word(unit, static_cast<int>(p)) & 0xffffu);
+          c[k] = p == kSelf ? cand : q[k];
+        }
+        if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK <= thr + R(kGuard))
+          thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
+        if (bad || alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK <= hyp + R(kGuard))
+          hyp_e = min_ref(hyp_e, alpha_plain<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y));
+      }
+      acc = hyp_e > thr_e;
+    }
+    N.store(s, acc ? cand : pv);
+    if (acc) {
+      ++accepted;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      disp = fmax(disp, static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy)))));
+    }
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+  }
+  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+}
+
+// Warp per vertex, Form A fused, for rows above the cycle tiers (valence 16 .. any): the
+// paper's CDP child launch for high-valence nodes becomes the 32 lanes of
+// one warp.  Lanes gather the row (ascending original id) into the warp's shared-memory slice
+// (entries beyond kCap are re-read from global memory / L2), every lane then forms the ordered
+// neighbour sum from the slice (broadcast reads, uniform control flow), lanes sweep the fan
+// records with the fast α/K filter for both positions of v, and a shuffle reduction gives the
+// warp-uniform decision.  Near-ties are settled with the reference's exact α (alpha_at).
+template <typename R, bool kSoA, int kWarps, int kCap>
+__global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  constexpr bool kExact = sizeof(R) == 8;
+  __shared__ R2 ring_s[kWarps * kCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * kWarps + w;
+  if (idx >= a.count) return;  // warp-uniform
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+  const int64_t s = a.list[idx];
+  const uint32_t o0 = __ldg(a.off + s);
+  const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
+  const uint32_t* nb = a.nbr + o0;
+  const uint32_t* fan = a.fan + o0;
+  R2* ring = ring_s + w * kCap;
+  const R2 pv = P.load(s);
+
+  // neighbor_mean (smoothing.hpp:72-80): one ordered chain, computed redundantly by all lanes
+  // from the shared-memory slice.  Rows longer than kCap are summed chunk by chunk (each chunk
+  // gathered in parallel); the first chunk stays resident for the fan sweep, entries beyond
+  // it are re-read from global memory there (parallel across lanes).
+  R sx = R(0), sy = R(0);
+  for (int c0 = 0; c0 < deg; c0 += kCap) {
+    const int n = deg - c0 < kCap ? deg - c0 : kCap;
+    if (c0 > 0) __syncwarp();
+#pragma unroll 4
+    for (int j = lane; j < n; j += 32) ring[j] = P.load(__ldg(nb + c0 + j));
+    __syncwarp();
+#pragma unroll 8
+    for (int j = 0; j < n; ++j) {
+      const R2 c = ring[j];
+      sx = O::add(sx, c.x);
+      sy = O::add(sy, c.y);
+    }
+  }
+  if (deg > kCap) {  // restore the first chunk for the sweep
+    __syncwarp();
+#pragma unroll 4
+    for (int j = lane; j < kCap; j += 32) ring[j] = P.load(__ldg(nb + j));
+    __syncwarp();
+  }
+  auto get = [&](int j) -> R2 { return j < kCap ? ring[j] : P.load(__ldg(nb + j)); };
+  const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
+  const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+  const bool tie = cand.x == pv.x && cand.y == pv.y;  // warp-uniform
+
+  bool acc = false;
+  if (!tie) {
+    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+#pragma unroll 2
+    for (int j = lane; j < deg; j += 32) {
+      const uint32_t f = __ldg(fan + j);
+      const R2 qa = get(fan_i1(f)), qb = get(fan_i2(f));
+      const R ex = qb.x - qa.x, ey = qb.y - qa.y;
+      const R lab = fma(ex, ex, ey * ey);
+      const R pax = qa.x - pv.x, pay = qa.y - pv.y, pbx = qb.x - pv.x, pby = qb.y - pv.y;
+      const R cax = qa.x - cand.x, cay = qa.y - cand.y, cbx = qb.x - cand.x, cby = qb.y - cand.y;
+      const R ep = fma(pax, pax, pay * pay) + fma(pbx, pbx, pby * pby) + lab;
+      const R ec = fma(cax, cax, cay * cay) + fma(cbx, cbx, cby * cby) + lab;
+      R tp = fma(pax, pby, -(pay * pbx)) * rcp_refined<2>(ep);
+      R tc = fma(cax, cby, -(cay * cbx)) * rcp_refined<2>(ec);
+      if constexpr (!kExact) {
+        tp = isfinite(tp) ? tp : R(0);
+        tc = isfinite(tc) ? tc : R(0);
+      }
+      nan_acc = nan_acc + (tp + tc);
+      thr = fmin(thr, tp);
+      hyp = fmin(hyp, tc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      thr = fmin(thr, __shfl_xor_sync(0xffffffffu, thr, o));
+      hyp = fmin(hyp, __shfl_xor_sync(0xffffffffu, hyp, o));
+    }
+    const bool bad = __any_sync(0xffffffffu, !(fabs(nan_acc) < R(1e30)));
+    if constexpr (!kExact) {
+      acc = hyp > thr;
+    } else if (!bad && hyp > thr + R(kGuard)) {
+      acc = true;
+    } else if (!bad && hyp < thr - R(kGuard)) {
+      acc = false;
+    } else {
+      // Near-tie: exact α of every triangle (alpha_at = triangle_alpha in the literal
+      // operand order; the minimum of finite values is order-free).
+      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+      for (int j = lane; j < deg; j += 32) {
+        const uint32_t f = __ldg(fan + j);
+        const R2 qa = get(fan_i1(f)), qb = get(fan_i2(f));
+        const int k = fan_k(f);
+        const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+        const R sabx = O::mul(dabx, dabx), saby = O::mul(daby, daby);
+        const R ep = alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby);
+        const R ec = alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby);
+        thr_e = min_ref(thr_e, ep);
+        hyp_e = min_ref(hyp_e, ec);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        thr_e = min_ref(thr_e, __shfl_xor_sync(0xffffffffu, thr_e, o));
+        hyp_e = min_ref(hyp_e, __shfl_xor_sync(0xffffffffu, hyp_e, o));
+      }
+      acc = hyp_e > thr_e;
+    }
+  }
+  int accepted = 0;
+  double disp = 0.0;
+  if (lane == 0) {
+    N.store(s, acc ? cand : pv);
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+    if (acc) {
+      accepted = 1;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+    }
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
 }

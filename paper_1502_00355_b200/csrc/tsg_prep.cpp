@@ -84,6 +84,76 @@ uint32_t hilbert_d(uint32_t x, uint32_t y) {
 
 }  // namespace
 
+// Tile records (see tsg_prep.hpp).  Per tile: the sorted external slots referenced by its
+// small rows, then per small row the interleaved (row, cycle) local indices.
+void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_max) {
+  const int64_t nv = hm.nv;
+  const int64_t ntiles = (nv + kTile - 1) / kTile;
+  hm.tmeta.assign(nv, 0);
+  hm.tile_rec.assign(ntiles + 1, 0);
+  hm.ext_off.assign(ntiles + 1, 0);
+  std::vector<std::vector<uint32_t>> ext(ntiles);
+  std::vector<uint32_t> units(ntiles, 0);
+  auto is_small = [&](int64_t s) { return deg[s] >= 1 && deg[s] <= static_cast<uint32_t>(small_max); };
+  parallel_ranges(ntiles, [&](int64_t tb, int64_t te) {
+    for (int64_t t = tb; t < te; ++t) {
+      const int64_t base = t * kTile, end = std::min(nv, base + kTile);
+      auto& E = ext[t];
+      uint32_t u16s = 0;
+      for (int64_t s = base; s < end; ++s) {
+        if (!is_small(s)) continue;
+        for (uint32_t j = hm.off[s]; j < hm.off[s + 1]; ++j) {
+          const int64_t u = hm.nbr[j];
+          if (u < base || u >= end) E.push_back(static_cast<uint32_t>(u));
+        }
+        hm.tmeta[s] = (u16s / 8) | (deg[s] << 16);
+        u16s += (2 * deg[s] + 7) / 8 * 8;
+      }
+      std::sort(E.begin(), E.end());
+      E.erase(std::unique(E.begin(), E.end()), E.end());
+      units[t] = u16s / 8;
+    }
+  });
+  uint64_t ru = 0, eu = 0;
+  int32_t max_ext = 0, max_units = 0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    hm.tile_rec[t] = static_cast<uint32_t>(ru);
+    hm.ext_off[t] = static_cast<uint32_t>(eu);
+    ru += units[t];
+    eu += ext[t].size();
+    max_ext = std::max<int32_t>(max_ext, static_cast<int32_t>(ext[t].size()));
+    max_units = std::max<int32_t>(max_units, static_cast<int32_t>(units[t]));
+  }
+  hm.tile_rec[ntiles] = static_cast<uint32_t>(ru);
+  hm.ext_off[ntiles] = static_cast<uint32_t>(eu);
+  hm.max_ext = max_ext;
+  hm.max_rec_units = max_units;
+  hm.ext.resize(eu);
+  hm.trec.assign(ru * 8, 0);
+  parallel_ranges(ntiles, [&](int64_t tb, int64_t te) {
+    for (int64_t t = tb; t < te; ++t) {
+      const int64_t base = t * kTile, end = std::min(nv, base + kTile);
+      const auto& E = ext[t];
+      std::copy(E.begin(), E.end(), hm.ext.begin() + hm.ext_off[t]);
+      auto local = [&](int64_t u) -> uint16_t {
+        if (u >= base && u < end) return static_cast<uint16_t>(u - base);
+        const auto it = std::lower_bound(E.begin(), E.end(), static_cast<uint32_t>(u));
+        return static_cast<uint16_t>(kTile + (it - E.begin()));
+      };
+      for (int64_t s = base; s < end; ++s) {
+        if (!is_small(s)) continue;
+        uint16_t* r = hm.trec.data() + (static_cast<uint64_t>(hm.tile_rec[t]) + (hm.tmeta[s] & 0xffffu)) * 8;
+        const uint32_t o0 = hm.off[s], n = deg[s];
+        const uint64_t cyc = hm.cyc[s];
+        for (uint32_t j = 0; j < n; ++j) {
+          r[2 * j] = local(hm.nbr[o0 + j]);
+          r[2 * j + 1] = cyc == kNoCycle ? kNoLocal : local(hm.nbr[o0 + ((cyc >> (4 * j)) & 15u)]);
+        }
+      }
+    }
+  });
+}
+
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
   double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
   for (int64_t v = 0; v < nv; ++v) {
@@ -127,7 +197,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     // Degree sort inside windows of kSigma consecutive slots of the locality order (SELL-C-σ
     // style): warps then see near-uniform valences (no divergent loop tails) while every
     // window stays spatially compact.  Results do not depend on the slot order.
-    constexpr int64_t kSigma = 1024;
+    constexpr int64_t kSigma = kTile;  // windows coincide with the tiles of tile_update
     auto degree_key = [&](int64_t v) -> int64_t {
       return d.boundary[v] ? 0 : d.nbr_off[v + 1] - d.nbr_off[v];
     };
@@ -220,7 +290,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
       uint32_t* out_n = hm.nbr.data() + hm.off[s];
       uint32_t* out_f = hm.fan.data() + hm.off[s];
       for (int32_t j = 0; j < n; ++j) out_n[j] = static_cast<uint32_t>(hm.rank[row[j]]);
-      const bool want_cycle = tiers.tier(static_cast<uint32_t>(n)) == 0 && n <= kMaxCycleDeg;
+      const bool want_cycle = n <= kMaxCycleDeg;
       int8_t succ[kMaxCycleDeg], indeg[kMaxCycleDeg];
       bool cycle_ok = want_cycle;
       if (want_cycle)
@@ -252,9 +322,8 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
           p[(k + 1) % 3] = ia;
           p[(k + 2) % 3] = ic;
           hm.fan16[hm.off[s] + j] = static_cast<uint16_t>(p[0] | (p[1] << 5) | (p[2] << 10));
-        } else {
-          out_f[j] = fan_pack_h(ia, ic, static_cast<uint32_t>(k));
         }
+        out_f[j] = fan_pack_h(ia, ic, static_cast<uint32_t>(k));
       }
       if (cycle_ok) {
         // Single directed cycle through all n positions, starting at position 0.
@@ -295,12 +364,23 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
 
   hm.hubs.clear();
   hm.medium.clear();
+  hm.cyc_mid.clear();
+  hm.large.clear();
   for (int64_t s = 0; s < nv; ++s) {
     if (deg[s] == 0) continue;
     const int tier = tiers.tier(deg[s]);
     if (tier == 1) hm.medium.push_back(static_cast<int32_t>(s));
     if (tier == 2) hm.hubs.push_back(static_cast<int32_t>(s));
+    if (tier > 0) {
+      if (deg[s] <= static_cast<uint32_t>(kMaxCycleDeg))
+        hm.cyc_mid.push_back(static_cast<int32_t>(s));
+      else
+        hm.large.push_back(static_cast<int32_t>(s));
+    }
   }
+  build_tiles(hm, deg, tiers.small_max);
+  // Longest rows first: the warp tier's tail is its largest hubs.
+  std::stable_sort(hm.large.begin(), hm.large.end(), [&](int32_t x, int32_t y) { return deg[x] > deg[y]; });
   return "";
 }
 

@@ -32,6 +32,11 @@ struct Tiers {
 };
 
 constexpr uint64_t kNoCycle = ~uint64_t{0};
+// Tiles of tile_update: kTile consecutive slots (the degree-sort windows of the locality
+// order).  A tile's small rows address their neighbours by LOCAL index: slot - tile base for
+// in-tile slots, kTile + position in the tile's sorted external-slot list otherwise.
+constexpr int kTile = 1024;
+constexpr uint16_t kNoLocal = 0xffffu;  // cycle entry of a row without a single link cycle
 constexpr int kMaxCycleDeg = 15;  // deg + 1 nibbles in 64 bits
 
 struct HostMesh {
@@ -41,7 +46,7 @@ struct HostMesh {
   std::vector<int64_t> tri_order; // device triangle -> original triangle
   std::vector<uint32_t> off;      // nv+1
   std::vector<uint32_t> nbr;      // slots
-  std::vector<uint32_t> fan;      // hub rows: (i1, i2, k) records; small rows unused
+  std::vector<uint32_t> fan;      // every row: (i1, i2, k) records
   std::vector<uint16_t> fan16;    // small rows: ring positions of (p1, p2, p3), 5 bits each
   // Small rows: the one-ring as a directed cycle, 4-bit row positions n_0..n_deg (n_deg = n_0)
   // such that every incident triangle is a rotation of (v, row[n_j], row[n_j+1]).  kNoCycle
@@ -53,6 +58,19 @@ struct HostMesh {
   std::vector<int32_t> tri;       // 3*nt device slots, device triangle order
   std::vector<int32_t> medium;    // slots of the medium tier
   std::vector<int32_t> hubs;      // slots of the hub tier
+  // Form A fused lists: rows above the small tier with deg <= kMaxCycleDeg (cycle sweep,
+  // thread per vertex) and the rest (warp per vertex).
+  std::vector<int32_t> cyc_mid;
+  std::vector<int32_t> large;
+  // Tiles (small rows only; other rows have tmeta == 0):
+  //   tmeta[s]     record offset of row s inside its tile (16-byte units) | deg << 16
+  //   tile_rec[t]  first 16-byte unit of tile t's records (ntiles + 1)
+  //   trec         u16 records: (row[j], cycle[j]) local indices interleaved for j < deg,
+  //                padded to 16 bytes; cycle[j] = kNoLocal when the row has no link cycle
+  //   ext_off/ext  per tile: sorted external slots (ntiles + 1 offsets)
+  std::vector<uint32_t> tmeta, tile_rec, ext_off, ext;
+  std::vector<uint16_t> trec;
+  int32_t max_ext = 0, max_rec_units = 0;
   int32_t max_deg = 0;
 };
 
@@ -75,5 +93,6 @@ struct FormBSchedule {
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
 std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
+void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_max);
 
 }  // namespace tsg
