@@ -29,11 +29,11 @@ tsg: $(TSG_SO)
 host: $(TS_SO)
 module: $(MOD_SO)
 
-build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp include/tsg.h
+build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp include/tsg.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas.log || (cat build/ptxas.log; false)
 
-build/tsg_prep.o: $(CSRC)/tsg_prep.cpp $(CSRC)/tsg_prep.hpp include/tsg.h
+build/tsg_prep.o: $(CSRC)/tsg_prep.cpp $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp include/tsg.h
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tsg_layout.hpp"
+
 namespace tsg {
 
 template <typename R>
@@ -176,8 +178,7 @@ __device__ __forceinline__ int fan_k(uint32_t f) { return static_cast<int>(f >> 
 __device__ __forceinline__ uint32_t fan_p(uint32_t f, int c) { return (f >> (5 * c)) & 31u; }
 
 constexpr int kMaxInvDeg = 32;
-constexpr int kTile = 1024;               // tile_update: slots per CTA (= tsg_prep.hpp kTile)
-constexpr uint32_t kNoLocalDev = 0xffffu;  // = tsg_prep.hpp kNoLocal  // 1/deg table (thread-per-vertex tiers)
+  // 1/deg table (thread-per-vertex tiers)
 
 constexpr uint32_t kFreshBit = 0x80000000u;  // Form B: read this neighbour from N (live)
 

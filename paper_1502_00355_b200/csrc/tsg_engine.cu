@@ -41,6 +41,9 @@ constexpr int kMaxSmallDeg = 10;
 constexpr int kMaxMedDeg = 31;
 constexpr tsg::Tiers kTiers{kMaxSmallDeg, kMaxMedDeg};
 constexpr int kHubCap = 4096;     // hub entries staged in shared memory
+constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
+constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
+constexpr int kTileRecCap = 8192;  // ... row words staged in shared memory (multiple of 4)
 constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
@@ -208,6 +211,8 @@ struct tsg_mesh {
   void* init = nullptr;  // slot-ordered copy of the coordinates given at upload / set_coords
   uint16_t* d_fan16 = nullptr;
   uint64_t* d_cyc = nullptr;
+  uint32_t *d_tmeta = nullptr, *d_tile_rec = nullptr, *d_ext_off = nullptr, *d_tile_ext = nullptr;
+  uint32_t* d_trec = nullptr;
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
   int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr, *d_cyc_mid = nullptr, *d_large = nullptr;
@@ -412,8 +417,13 @@ struct Engine {
       Args a = base;
       a.list = nullptr;
       a.count = nv;
-      tsg::ring_update<R, kSoA, kMaxSmallDeg, kMaxSmallDeg, tsg::kNodeBlock>
-          <<<static_cast<unsigned>((nv + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a, m->d_cyc);
+      const tsg::TileArgs ta = tile_args(m);
+      const unsigned ntiles = static_cast<unsigned>((nv + tsg::kTile - 1) / tsg::kTile);
+      const size_t smem = tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap);
+      if (tiles_staged(m))
+        tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, true><<<ntiles, kTileThreads, smem, s>>>(a, ta);
+      else
+        tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
@@ -473,8 +483,33 @@ struct Engine {
     return TSG_OK;
   }
 
+  static bool tiles_staged(const tsg_mesh* m) {
+    return m->hm.max_ext <= kTileExtCap && m->hm.max_rec_words <= kTileRecCap;
+  }
+
+  static tsg::TileArgs tile_args(const tsg_mesh* m) {
+    tsg::TileArgs t{};
+    t.meta = m->d_tmeta;
+    t.rec = m->d_trec;
+    t.tile_rec = m->d_tile_rec;
+    t.ext_off = m->d_ext_off;
+    t.ext = m->d_tile_ext;
+    t.ext_cap = std::min(m->hm.max_ext, kTileExtCap);
+    t.rec_cap = std::min(m->hm.max_rec_words, kTileRecCap);
+    t.nv = m->hm.nv;
+    return t;
+  }
+
   // Opt-in shared memory for the hub kernels (done outside any stream capture).
   static tsg_status prepare(tsg_mesh* m) {
+    {
+      const tsg::TileArgs ta = tile_args(m);
+      const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap));
+      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
     const int smem1 = static_cast<int>(hub_cap * sizeof(R2)), smem2 = 2 * smem1;
     TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
@@ -685,6 +720,11 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
   if ((st = upload(&m->d_fan16, hm.fan16, b, s))) return st;
   if ((st = upload(&m->d_cyc, hm.cyc, b, s))) return st;
+  if ((st = upload(&m->d_tmeta, hm.tmeta, b, s))) return st;
+  if ((st = upload(&m->d_tile_rec, hm.tile_rec, b, s))) return st;
+  if ((st = upload(&m->d_ext_off, hm.ext_off, b, s))) return st;
+  if ((st = upload(&m->d_tile_ext, hm.ext, b, s))) return st;
+  if ((st = upload(&m->d_trec, hm.trec, b, s))) return st;
   if ((st = upload(&m->d_vinc_off, hm.vinc_off, b, s))) return st;
   if ((st = upload(&m->d_vinc, hm.vinc, b, s))) return st;
   if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
@@ -720,7 +760,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
   free_form_b(m);
-  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_cyc, m->d_vinc_off, m->d_vinc,
+  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_cyc, m->d_tmeta, m->d_tile_rec, m->d_ext_off, m->d_tile_ext, m->d_trec, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_cyc_mid, m->d_large, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};

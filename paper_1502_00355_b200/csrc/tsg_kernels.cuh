@@ -325,18 +325,17 @@ __device__ __forceinline__ R inv_deg(int deg) {
 }
 
 // Per-neighbour quantities of the cycle sweep: q - v at the pass-start position and at the
-// candidate, and their squared lengths.
+// candidate, and their squared lengths.  (The outer edge b - a of a triangle is formed from
+// the pass-start offsets; its rounding error is bounded like the others', see ring_update.)
 template <typename R>
 struct RingEdge {
-  R qx, qy, px, py, cx, cy, lp, lc;
+  R px, py, cx, cy, lp, lc;
 };
 
 template <typename R>
 __device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typename Arith<R>::R2 pv,
                                                  typename Arith<R>::R2 cand) {
   RingEdge<R> e;
-  e.qx = q.x;
-  e.qy = q.y;
   e.px = q.x - pv.x;
   e.py = q.y - pv.y;
   e.cx = q.x - cand.x;
@@ -434,7 +433,7 @@ __global__ void __launch_bounds__(kBlock, 1024 / kBlock) ring_update(PassArgs<R,
 #pragma unroll 2
         for (int j = 1; j <= deg; ++j) {
           const RingEdge<R> eb = ring_edge<R>(at(static_cast<uint32_t>((cyc >> (4 * j)) & 15u)), pv, cand);
-          const R ex = eb.qx - ea.qx, ey = eb.qy - ea.qy;
+          const R ex = eb.px - ea.px, ey = eb.py - ea.py;
           const R lab = fma(ex, ex, ey * ey);
           const R cp = fma(ea.px, eb.py, -(ea.py * eb.px));
           const R cc = fma(ea.cx, eb.cy, -(ea.cy * eb.cx));
@@ -514,45 +513,46 @@ __global__ void __launch_bounds__(kBlock, 1024 / kBlock) ring_update(PassArgs<R,
 
 // Tile arrays (tsg_prep.hpp build_tiles).
 struct TileArgs {
-  const uint32_t* meta;      // per slot: record offset in the tile (16-byte units) | deg << 16
-  const uint4* rec;          // records, 16-byte units
-  const uint32_t* tile_rec;  // ntiles + 1
+  const uint32_t* meta;      // per slot: first word | deg << 16 | group stride << 20
+  const uint32_t* rec;       // words: row[j] | cycle[j] << 16 (local indices)
+  const uint32_t* tile_rec;  // ntiles + 1 (first word of each tile, multiples of 4)
   const uint32_t* ext_off;   // ntiles + 1
   const uint32_t* ext;       // external slots
-  int32_t ext_cap;           // external entries staged in shared memory per tile
-  int32_t rec_cap;           // record units staged in shared memory per tile
+  int32_t ext_cap;           // external coordinates staged in shared memory per tile
+  int32_t rec_cap;           // words staged in shared memory per tile (multiple of 4)
   int64_t nv;
 };
 
 template <typename R>
-__host__ __device__ constexpr size_t tile_smem_bytes(int tile, int ext_cap, int rec_cap) {
-  return sizeof(typename Arith<R>::R2) * (tile + ext_cap) + 16 * static_cast<size_t>(rec_cap) +
-         4 * static_cast<size_t>(tile);
+__host__ __device__ constexpr size_t tile_smem_bytes(int ext_cap, int rec_cap) {
+  return sizeof(typename Arith<R>::R2) * (kTile + ext_cap) + 4 * static_cast<size_t>(rec_cap) +
+         4 * static_cast<size_t>(kTile);
 }
 
 // Tile-staged thread-per-vertex Form A fused update (small tier, deg <= kMaxDeg).
 //
 // One CTA owns kTile consecutive slots (a Hilbert-compact patch, degree-sorted inside).  It
 // first stages, with coalesced loads, the patch's pass-start coordinates, the coordinates of
-// the external slots its rows reference, the rows' local-index records and the per-slot meta
-// words into shared memory; after one barrier every gather is a shared-memory read.  Record
-// word j of a row = (row[j], cycle[j]) local indices: row[] in ascending ORIGINAL id (the
-// summation order of neighbor_mean, smoothing.hpp:72-80), cycle[] the directed link cycle
-// (every incident triangle is a rotation of (v, cycle[j], cycle[j+1])).  The decision
-// arithmetic is ring_update's: fast α/K filter over the cycle, exact literal evaluation over
-// the fan records for near-ties and for rows without a link cycle.
-template <typename R, bool kSoA, int kThreads, int kMaxDeg>
+// the external slots its rows reference, the rows' words and the per-slot meta words in
+// shared memory; after one barrier every gather is a shared-memory read.  Word j of a row =
+// (row[j], cycle[j]) local indices: row[] in ascending ORIGINAL id (the summation order of
+// neighbor_mean, smoothing.hpp:72-80), cycle[] the directed link cycle (every incident triangle
+// is a rotation of (v, cycle[j], cycle[j+1])).  Rows of one valence are stored entry-major, so
+// the lanes of a (degree-uniform) warp read word j of consecutive rows without bank conflicts.
+// The decision arithmetic is ring_update's: fast α/K filter over the cycle, exact literal
+// evaluation over the fan records for near-ties and for rows without a link cycle.
+// kStaged: every tile's external coordinates and words fit the shared-memory caps.
+template <typename R, bool kSoA, int kThreads, int kMaxDeg, bool kStaged>
 __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr int kSelf = kMaxDeg;  // v's position in the small tier's fan16 records
   constexpr bool kExact = sizeof(R) == 8;
-  constexpr int kWords = (kMaxDeg + 3) / 4 * 4;
   static_assert(kTile % kThreads == 0, "whole vertices per thread");
   extern __shared__ __align__(16) unsigned char tile_smem[];
   R2* pts = reinterpret_cast<R2*>(tile_smem);
-  uint4* recs = reinterpret_cast<uint4*>(pts + kTile + t.ext_cap);
-  uint32_t* meta_s = reinterpret_cast<uint32_t*>(recs + t.rec_cap);
+  uint32_t* words = reinterpret_cast<uint32_t*>(pts + kTile + t.ext_cap);
+  uint32_t* meta_s = words + t.rec_cap;
 
   const int tid = threadIdx.x;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
@@ -565,24 +565,33 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
 
   const uint32_t e0 = __ldg(t.ext_off + blockIdx.x), ne = __ldg(t.ext_off + blockIdx.x + 1) - e0;
   const uint32_t r0 = __ldg(t.tile_rec + blockIdx.x), nr = __ldg(t.tile_rec + blockIdx.x + 1) - r0;
-  const int n_ext = static_cast<int>(ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
-  const int n_rec = static_cast<int>(nr < static_cast<uint32_t>(t.rec_cap) ? nr : t.rec_cap);
+  const int n_ext = static_cast<int>(kStaged || ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
+  const int n_rec = static_cast<int>(kStaged || nr < static_cast<uint32_t>(t.rec_cap) ? nr : t.rec_cap);
   for (int i = tid; i < n_in; i += kThreads) {
     pts[i] = P.load(base + i);
     meta_s[i] = __ldg(t.meta + base + i);
   }
   for (int k = tid; k < n_ext; k += kThreads) pts[kTile + k] = P.load(__ldg(t.ext + e0 + k));
-  for (int k = tid; k < n_rec; k += kThreads) recs[k] = __ldg(t.rec + r0 + k);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(t.rec + r0);
+    uint4* dst = reinterpret_cast<uint4*>(words);
+    for (int k = tid; k < n_rec / 4; k += kThreads) dst[k] = __ldg(src + k);
+  }
   __syncthreads();
 
   auto get = [&](uint32_t l) -> R2 {
-    return l < static_cast<uint32_t>(kTile + t.ext_cap) ? pts[l] : P.load(__ldg(t.ext + e0 + l - kTile));
+    if constexpr (kStaged) {
+      return pts[l];
+    } else {
+      return l < static_cast<uint32_t>(kTile + t.ext_cap) ? pts[l] : P.load(__ldg(t.ext + e0 + l - kTile));
+    }
   };
-  auto rec_word = [&](uint32_t unit, int j) -> uint32_t {  // any unit, any j (rare paths)
-    const uint32_t u = unit + static_cast<uint32_t>(j >> 2);
-    const uint4 v = u < static_cast<uint32_t>(t.rec_cap) ? recs[u] : __ldg(t.rec + r0 + u);
-    const int c = j & 3;
-    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+  auto word = [&](uint32_t w) -> uint32_t {
+    if constexpr (kStaged) {
+      return words[w];
+    } else {
+      return w < static_cast<uint32_t>(t.rec_cap) ? words[w] : __ldg(t.rec + r0 + w);
+    }
   };
 
   int accepted = 0;
@@ -590,32 +599,16 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
 #pragma unroll 1
   for (int i = tid; i < n_in; i += kThreads) {
     const uint32_t meta = meta_s[i];
-    const int deg = static_cast<int>(meta >> 16);
+    const int deg = static_cast<int>((meta >> kMetaDegShift) & 15u);
     if (deg == 0) continue;  // pinned, or a medium / warp tier row
-    const uint32_t unit = meta & 0xffffu;
-    uint32_t w[kWords];
-#pragma unroll
-    for (int q = 0; q < kWords / 4; ++q) {
-      if (4 * q < deg) {
-        const uint32_t u = unit + q;
-        const uint4 v = u < static_cast<uint32_t>(t.rec_cap) ? recs[u] : __ldg(t.rec + r0 + u);
-        w[4 * q] = v.x;
-        w[4 * q + 1] = v.y;
-        w[4 * q + 2] = v.z;
-        w[4 * q + 3] = v.w;
-      } else {
-        w[4 * q] = w[4 * q + 1] = w[4 * q + 2] = w[4 * q + 3] = 0u;
-      }
-    }
+    const uint32_t w0 = meta & kMetaBaseMask, stride = meta >> kMetaStrideShift;
     const R2 pv = pts[i];
     R sx = R(0), sy = R(0);
-#pragma unroll
-    for (int j = 0; j < kMaxDeg; ++j) {
-      if (j < deg) {
-        const R2 c = get(w[j] & 0xffffu);
-        sx = O::add(sx, c.x);
-        sy = O::add(sy, c.y);
-      }
+#pragma unroll 2
+    for (int j = 0; j < deg; ++j) {
+      const R2 c = get(word(w0 + j * stride) & 0xffffu);
+      sx = O::add(sx, c.x);
+      sy = O::add(sy, c.y);
     }
     const R inv = inv_deg<R>(deg);
     const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
@@ -623,29 +616,31 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
     const int64_t s = base + i;
     R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
     if (!tie) {
-      if ((w[0] >> 16) != kNoLocalDev) {
-        RingEdge<R> ea = ring_edge<R>(get(w[0] >> 16), pv, cand);
-#pragma unroll
-        for (int j = 1; j <= kMaxDeg; ++j) {
-          if (j <= deg) {
-            const uint32_t l = (j < deg ? w[j < kMaxDeg ? j : 0] : w[0]) >> 16;
-            const RingEdge<R> eb = ring_edge<R>(get(l), pv, cand);
-            const R ex = eb.qx - ea.qx, ey = eb.qy - ea.qy;
-            const R lab = fma(ex, ex, ey * ey);
-            const R cp = fma(ea.px, eb.py, -(ea.py * eb.px));
-            const R cc = fma(ea.cx, eb.cy, -(ea.cy * eb.cx));
-            R tp = cp * rcp_refined<2>(ea.lp + eb.lp + lab);
-            R tc = cc * rcp_refined<2>(ea.lc + eb.lc + lab);
-            if constexpr (!kExact) {
-              tp = isfinite(tp) ? tp : R(0);
-              tc = isfinite(tc) ? tc : R(0);
-            }
-            nan_acc = nan_acc + (tp + tc);
-            thr = fmin(thr, tp);
-            hyp = fmin(hyp, tc);
-            ea = eb;
+      const uint32_t l0 = word(w0) >> 16;
+      if (l0 != kNoLocal) {
+        RingEdge<R> ea = ring_edge<R>(get(l0), pv, cand);
+        auto tri = [&](const RingEdge<R>& x, const RingEdge<R>& y) {
+          const R ex = y.px - x.px, ey = y.py - x.py;
+          const R lab = fma(ex, ex, ey * ey);
+          const R cp = fma(x.px, y.py, -(x.py * y.px));
+          const R cc = fma(x.cx, y.cy, -(x.cy * y.cx));
+          R tp = cp * rcp_refined<2>(x.lp + y.lp + lab);
+          R tc = cc * rcp_refined<2>(x.lc + y.lc + lab);
+          if constexpr (!kExact) {
+            tp = isfinite(tp) ? tp : R(0);
+            tc = isfinite(tc) ? tc : R(0);
           }
+          nan_acc = fma(tp, tc, nan_acc);  // any non-finite value poisons the accumulator
+          thr = min_ref(thr, tp);
+          hyp = min_ref(hyp, tc);
+        };
+#pragma unroll 2
+        for (int j = 1; j < deg; ++j) {
+          const RingEdge<R> eb = ring_edge<R>(get(word(w0 + j * stride) >> 16), pv, cand);
+          tri(ea, eb);
+          ea = eb;
         }
+        tri(ea, ring_edge<R>(get(l0), pv, cand));  // closing triangle (recomputed, saves registers)
       } else {
         // No single link cycle: literal triangles from the fan records (α/K scale).
         constexpr R kInvK = R(1) / Arith<R>::kAlpha;
@@ -656,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
             const uint32_t p = fan_p(f, k);
-            q[k] = p == kSelf ? pv : get(rec_word(unit, static_cast<int>(p)) & 0xffffu);
+            q[k] = p == kSelf ? pv : get(word(w0 + p * stride) & 0xffffu);
             c[k] = p == kSelf ? cand : q[k];
           }
           R tq = alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK;
@@ -665,9 +660,9 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
             tq = isfinite(tq) ? tq : R(0);
             th = isfinite(th) ? th : R(0);
           }
-          nan_acc = nan_acc + (tq + th);
-          thr = fmin(thr, tq);
-          hyp = fmin(hyp, th);
+          nan_acc = fma(tq, th, nan_acc);
+          thr = min_ref(thr, tq);
+          hyp = min_ref(hyp, th);
         }
       }
     }
@@ -691,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const uint32_t p = fan_p(f, k);
-          q[k] = p == kSelf ? pv : get(rec_word(unit, static_cast<int>(p)) & 0xffffu);
+          q[k] = p == kSelf ? pv : get(word(w0 + p * stride) & 0xffffu);
           c[k] = p == kSelf ? cand : q[k];
         }
         if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK <= thr + R(kGuard))
@@ -705,7 +700,8 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
     if (acc) {
       ++accepted;
       const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
-      disp = fmax(disp, static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy)))));
+      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      disp = d > disp ? d : disp;
     }
     if (a.decision) a.decision[s] = acc ? 1 : 0;
   }

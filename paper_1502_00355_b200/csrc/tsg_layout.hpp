@@ -1,0 +1,20 @@
+// Layout constants shared by the host preparation (tsg_prep.cpp) and the kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace tsg {
+
+constexpr uint64_t kNoCycle = ~uint64_t{0};  // cycle word of a row without a single link cycle
+constexpr int kMaxCycleDeg = 15;             // deg + 1 nibbles in 64 bits
+// Tiles of tile_update: kTile consecutive slots (the degree-sort windows of the locality
+// order).  A tile's small rows address their neighbours by LOCAL index: slot - tile base for
+// in-tile slots, kTile + position in the tile's sorted external-slot list otherwise.
+constexpr int kTile = 1024;
+constexpr uint16_t kNoLocal = 0xffffu;  // cycle entry of a row without a single link cycle
+// Tile meta word: first-word offset | valence | group stride (tsg_prep.hpp HostMesh::tmeta).
+constexpr uint32_t kMetaBaseMask = 0xffffu;
+constexpr int kMetaDegShift = 16;     // 4 bits
+constexpr int kMetaStrideShift = 20;  // 11 bits (<= kTile)
+
+}  // namespace tsg

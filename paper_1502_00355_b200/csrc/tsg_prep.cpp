@@ -85,7 +85,8 @@ uint32_t hilbert_d(uint32_t x, uint32_t y) {
 }  // namespace
 
 // Tile records (see tsg_prep.hpp).  Per tile: the sorted external slots referenced by its
-// small rows, then per small row the interleaved (row, cycle) local indices.
+// small rows; the small rows grouped by valence (slot order inside a group), each group's
+// words stored entry-major: word j of the k-th row of a group of n rows at group base + j*n + k.
 void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_max) {
   const int64_t nv = hm.nv;
   const int64_t ntiles = (nv + kTile - 1) / kTile;
@@ -93,61 +94,73 @@ void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_m
   hm.tile_rec.assign(ntiles + 1, 0);
   hm.ext_off.assign(ntiles + 1, 0);
   std::vector<std::vector<uint32_t>> ext(ntiles);
-  std::vector<uint32_t> units(ntiles, 0);
+  std::vector<uint32_t> words(ntiles, 0);
   auto is_small = [&](int64_t s) { return deg[s] >= 1 && deg[s] <= static_cast<uint32_t>(small_max); };
   parallel_ranges(ntiles, [&](int64_t tb, int64_t te) {
     for (int64_t t = tb; t < te; ++t) {
       const int64_t base = t * kTile, end = std::min(nv, base + kTile);
       auto& E = ext[t];
-      uint32_t u16s = 0;
+      uint32_t count[kMaxCycleDeg + 1] = {};
       for (int64_t s = base; s < end; ++s) {
         if (!is_small(s)) continue;
+        ++count[deg[s]];
         for (uint32_t j = hm.off[s]; j < hm.off[s + 1]; ++j) {
           const int64_t u = hm.nbr[j];
           if (u < base || u >= end) E.push_back(static_cast<uint32_t>(u));
         }
-        hm.tmeta[s] = (u16s / 8) | (deg[s] << 16);
-        u16s += (2 * deg[s] + 7) / 8 * 8;
+      }
+      uint32_t gbase[kMaxCycleDeg + 1], fill[kMaxCycleDeg + 1] = {}, w = 0;
+      for (int d = 1; d <= small_max; ++d) {
+        gbase[d] = w;
+        w += static_cast<uint32_t>(d) * count[d];
+      }
+      for (int64_t s = base; s < end; ++s) {
+        if (!is_small(s)) continue;
+        const uint32_t d = deg[s], k = fill[d]++;
+        hm.tmeta[s] = (gbase[d] + k) | (d << kMetaDegShift) | (count[d] << kMetaStrideShift);
       }
       std::sort(E.begin(), E.end());
       E.erase(std::unique(E.begin(), E.end()), E.end());
-      units[t] = u16s / 8;
+      words[t] = (w + 3) / 4 * 4;  // tiles start 16-byte aligned
     }
   });
-  uint64_t ru = 0, eu = 0;
-  int32_t max_ext = 0, max_units = 0;
+  uint64_t wu = 0, eu = 0;
+  int32_t max_ext = 0, max_words = 0;
   for (int64_t t = 0; t < ntiles; ++t) {
-    hm.tile_rec[t] = static_cast<uint32_t>(ru);
+    hm.tile_rec[t] = static_cast<uint32_t>(wu);
     hm.ext_off[t] = static_cast<uint32_t>(eu);
-    ru += units[t];
+    wu += words[t];
     eu += ext[t].size();
     max_ext = std::max<int32_t>(max_ext, static_cast<int32_t>(ext[t].size()));
-    max_units = std::max<int32_t>(max_units, static_cast<int32_t>(units[t]));
+    max_words = std::max<int32_t>(max_words, static_cast<int32_t>(words[t]));
   }
-  hm.tile_rec[ntiles] = static_cast<uint32_t>(ru);
+  hm.tile_rec[ntiles] = static_cast<uint32_t>(wu);
   hm.ext_off[ntiles] = static_cast<uint32_t>(eu);
   hm.max_ext = max_ext;
-  hm.max_rec_units = max_units;
+  hm.max_rec_words = max_words;
   hm.ext.resize(eu);
-  hm.trec.assign(ru * 8, 0);
+  hm.trec.assign(wu, 0);
   parallel_ranges(ntiles, [&](int64_t tb, int64_t te) {
     for (int64_t t = tb; t < te; ++t) {
       const int64_t base = t * kTile, end = std::min(nv, base + kTile);
       const auto& E = ext[t];
       std::copy(E.begin(), E.end(), hm.ext.begin() + hm.ext_off[t]);
-      auto local = [&](int64_t u) -> uint16_t {
-        if (u >= base && u < end) return static_cast<uint16_t>(u - base);
+      auto local = [&](int64_t u) -> uint32_t {
+        if (u >= base && u < end) return static_cast<uint32_t>(u - base);
         const auto it = std::lower_bound(E.begin(), E.end(), static_cast<uint32_t>(u));
-        return static_cast<uint16_t>(kTile + (it - E.begin()));
+        return static_cast<uint32_t>(kTile + (it - E.begin()));
       };
       for (int64_t s = base; s < end; ++s) {
         if (!is_small(s)) continue;
-        uint16_t* r = hm.trec.data() + (static_cast<uint64_t>(hm.tile_rec[t]) + (hm.tmeta[s] & 0xffffu)) * 8;
+        const uint32_t meta = hm.tmeta[s];
+        uint32_t* r = hm.trec.data() + hm.tile_rec[t] + (meta & kMetaBaseMask);
+        const uint32_t stride = meta >> kMetaStrideShift;
         const uint32_t o0 = hm.off[s], n = deg[s];
         const uint64_t cyc = hm.cyc[s];
         for (uint32_t j = 0; j < n; ++j) {
-          r[2 * j] = local(hm.nbr[o0 + j]);
-          r[2 * j + 1] = cyc == kNoCycle ? kNoLocal : local(hm.nbr[o0 + ((cyc >> (4 * j)) & 15u)]);
+          const uint32_t row = local(hm.nbr[o0 + j]);
+          const uint32_t cy = cyc == kNoCycle ? kNoLocal : local(hm.nbr[o0 + ((cyc >> (4 * j)) & 15u)]);
+          r[j * stride] = row | (cy << 16);
         }
       }
     }

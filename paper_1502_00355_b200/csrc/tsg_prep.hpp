@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "tsg.h"
+#include "tsg_layout.hpp"
 
 namespace tsg {
 
@@ -30,14 +31,6 @@ struct Tiers {
     return deg <= static_cast<uint32_t>(small_max) ? 0 : deg <= static_cast<uint32_t>(medium_max) ? 1 : 2;
   }
 };
-
-constexpr uint64_t kNoCycle = ~uint64_t{0};
-// Tiles of tile_update: kTile consecutive slots (the degree-sort windows of the locality
-// order).  A tile's small rows address their neighbours by LOCAL index: slot - tile base for
-// in-tile slots, kTile + position in the tile's sorted external-slot list otherwise.
-constexpr int kTile = 1024;
-constexpr uint16_t kNoLocal = 0xffffu;  // cycle entry of a row without a single link cycle
-constexpr int kMaxCycleDeg = 15;  // deg + 1 nibbles in 64 bits
 
 struct HostMesh {
   int64_t nv = 0, nt = 0;
@@ -63,14 +56,14 @@ struct HostMesh {
   std::vector<int32_t> cyc_mid;
   std::vector<int32_t> large;
   // Tiles (small rows only; other rows have tmeta == 0):
-  //   tmeta[s]     record offset of row s inside its tile (16-byte units) | deg << 16
-  //   tile_rec[t]  first 16-byte unit of tile t's records (ntiles + 1)
-  //   trec         u16 records: (row[j], cycle[j]) local indices interleaved for j < deg,
-  //                padded to 16 bytes; cycle[j] = kNoLocal when the row has no link cycle
+  //   tmeta[s]     word offset of row s's first word inside its tile's words (bits 0-15) |
+  //                deg << kMetaDegShift | stride << kMetaStrideShift (word j at offset + j*stride)
+  //   tile_rec[t]  first word of tile t (ntiles + 1; multiples of 4)
+  //   trec         u32 words: row[j] local index | cycle[j] local index << 16, cycle[j] =
+  //                kNoLocal when the row has no single link cycle
   //   ext_off/ext  per tile: sorted external slots (ntiles + 1 offsets)
-  std::vector<uint32_t> tmeta, tile_rec, ext_off, ext;
-  std::vector<uint16_t> trec;
-  int32_t max_ext = 0, max_rec_units = 0;
+  std::vector<uint32_t> tmeta, tile_rec, ext_off, ext, trec;
+  int32_t max_ext = 0, max_rec_words = 0;
   int32_t max_deg = 0;
 };
 
