@@ -187,7 +187,7 @@ struct PassState {
   int32_t pass;  // index of the pass being executed
   int32_t done;  // 1 once a stop rule fired
   int32_t stop;  // TSG_STOP_*
-  int32_t pad;
+  int32_t queued;  // near-tie vertices queued by tile_update this pass (reset by finalize_pass)
 };
 
 }  // namespace tsg

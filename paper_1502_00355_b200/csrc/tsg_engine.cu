@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -44,6 +46,7 @@ constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
 constexpr int kTileRecCap = 8192;  // ... row words staged in shared memory (multiple of 4)
+constexpr int kTieBlocks = 148 * 4;  // tie_update: persistent grid over the near-tie queue
 constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
@@ -226,6 +229,8 @@ struct tsg_mesh {
   unsigned long long* d_md = nullptr;
   int32_t* d_sacc = nullptr;           // per-pass stat slots (kStatSlots each)
   unsigned long long* d_smd = nullptr;
+  unsigned long long* d_rare = nullptr;  // diagnostics: rare-path decisions per pass
+  int32_t* d_queue = nullptr;            // near-tie queue (nv)
   unsigned long long* d_ext = nullptr;  // extrema scratch (3)
   int32_t cap = 0;
   int cur = 0;
@@ -287,6 +292,13 @@ tsg::Coords<R, kSoA> coords_of(const tsg_mesh* m, int i) {
   return tsg::Coords<R, kSoA>{static_cast<R*>(m->buf[i]), m->hm.nv};
 }
 
+// Diagnostics (TSG_DIAG=1): per-pass rare-path counts and node-kernel times printed by the
+// stream driver to stderr.  Not part of the ABI; used to tune the fast-path guard.
+bool diag_enabled() {
+  static const bool on = std::getenv("TSG_DIAG") != nullptr;
+  return on;
+}
+
 // Everything templated on the coordinate type and layout.
 template <typename R, bool kSoA>
 struct Engine {
@@ -309,6 +321,8 @@ struct Engine {
     a.slot_acc = m->d_sacc;
     a.slot_md = m->d_smd;
     a.decision = nullptr;
+    a.rare = diag_enabled() ? m->d_rare : nullptr;
+    a.queue = m->d_queue;
     return a;
   }
 
@@ -384,7 +398,8 @@ struct Engine {
     tsg_context* ctx = m->ctx;
     const int64_t nv = m->hm.nv, nmid = static_cast<int64_t>(m->hm.cyc_mid.size()),
                   nlarge = static_cast<int64_t>(m->hm.large.size());
-    const bool fork = nmid > 0 || nlarge > 0;
+    static const bool serial = std::getenv("TSG_SERIAL_TIERS") != nullptr;  // experiment knob
+    const bool fork = !serial && (nmid > 0 || nlarge > 0);
     cudaStream_t t = s;
     if (fork) {
       cudaEvent_t e;
@@ -426,6 +441,11 @@ struct Engine {
         tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
+      if constexpr (sizeof(R) == 8) {  // fp64: exact decisions of the queued near-ties
+        tsg::tie_update<R, kSoA><<<kTieBlocks, 128, 0, s>>>(a);
+        TSG_CUDA(cudaGetLastError());
+        ++*kernels;
+      }
     }
     if (fork) {
       cudaEvent_t e;
@@ -612,6 +632,9 @@ tsg_status ensure_stats_capacity(tsg_mesh* m, int32_t n) {
   TSG_CUDA(cudaMalloc(&m->d_md, sizeof(unsigned long long) * n));
   TSG_CUDA(cudaMalloc(&m->d_sacc, sizeof(int32_t) * n * tsg::kStatSlots));
   TSG_CUDA(cudaMalloc(&m->d_smd, sizeof(unsigned long long) * n * tsg::kStatSlots));
+  cudaFree(m->d_rare);
+  m->d_rare = nullptr;
+  TSG_CUDA(cudaMalloc(&m->d_rare, sizeof(unsigned long long) * n));
   m->cap = n;
   m->gc.reset();  // graph captured old pointers
   return TSG_OK;
@@ -743,6 +766,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = dalloc(&m->d_decision, nv, b))) return st;
   if ((st = dalloc(&m->d_decision_orig, nv, b))) return st;
   if ((st = dalloc(&m->d_state, 1, b))) return st;
+  if ((st = dalloc(&m->d_queue, nv, b))) return st;
   if ((st = dalloc(&m->d_ext, 3, b))) return st;
   for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
   if ((st = ensure_stats_capacity(m.get(), 128))) return st;
@@ -763,7 +787,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_cyc, m->d_tmeta, m->d_tile_rec, m->d_ext_off, m->d_tile_ext, m->d_trec, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_cyc_mid, m->d_large, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
-                  m->d_ext, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
+                  m->d_ext, m->d_rare, m->d_queue, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
   for (void* p : ptrs) cudaFree(p);
   delete m;
   return TSG_OK;
@@ -894,6 +918,7 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
   TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * c->max_iters, s));
   TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
+  if (diag_enabled()) TSG_CUDA(cudaMemsetAsync(m->d_rare, 0, sizeof(unsigned long long) * c->max_iters, s));
 
   int64_t kernels_per_pass = 0;
   double node_ms = -1.0;
@@ -982,6 +1007,17 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
       float ms = 0.f;
       TSG_CUDA(cudaEventElapsedTime(&ms, ctx->pass_events[2 * p], ctx->pass_events[2 * p + 1]));
       node_ms += ms;
+    }
+    if (diag_enabled()) {
+      std::vector<unsigned long long> rare(it);
+      std::vector<int32_t> accd(it);
+      TSG_CUDA(cudaMemcpy(rare.data(), m->d_rare, sizeof(unsigned long long) * it, cudaMemcpyDeviceToHost));
+      TSG_CUDA(cudaMemcpy(accd.data(), m->d_acc, sizeof(int32_t) * it, cudaMemcpyDeviceToHost));
+      for (int p = 0; p < it; ++p) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->pass_events[2 * p], ctx->pass_events[2 * p + 1]);
+        std::fprintf(stderr, "[tsg diag] pass %d node_ms %.4f accepted %d rare %llu\n", p, ms, accd[p], rare[p]);
+      }
     }
   }
   if (c->swap == TSG_SWAP_PINGPONG) m->cur = it & 1;

@@ -44,6 +44,8 @@ struct PassArgs {
   unsigned long long* slot_md;  // [pass][kStatSlots] partial max displacement bits
                                 // (non-negative doubles order as u64)
   int8_t* decision;             // optional: 1 accept / 0 reject per slot
+  unsigned long long* rare;     // optional diagnostics: [pass] rare-path decisions (tile_update)
+  int32_t* queue;               // near-tie slots queued for tie_update (capacity nv)
 };
 
 template <typename R, bool kSoA>
@@ -512,6 +514,8 @@ __global__ void __launch_bounds__(kBlock, 1024 / kBlock) ring_update(PassArgs<R,
 }
 
 // Tile arrays (tsg_prep.hpp build_tiles).
+constexpr int kTileMinBlocks = 3;  // 256-thread CTAs per SM the register budget is sized for
+
 struct TileArgs {
   const uint32_t* meta;      // per slot: first word | deg << 16 | group stride << 20
   const uint32_t* rec;       // words: row[j] | cycle[j] << 16 (local indices)
@@ -529,27 +533,145 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int ext_cap, int rec_cap) {
          4 * static_cast<size_t>(kTile);
 }
 
+// ---- bulk-copy (TMA) staging helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+// Global -> shared bulk copy (16-byte aligned, size a multiple of 16), completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+// 16-byte (8-byte) asynchronous global -> shared copy (LDGSTS), completed by cp_async_wait_all.
+template <int kBytes>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  if constexpr (kBytes == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_addr(dst)), "l"(src), "n"(kBytes) : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Shared-memory view of one staged tile.
+template <typename R, bool kSoA, bool kStaged>
+struct TileView {
+  using R2 = typename Arith<R>::R2;
+  const R2* pts;
+  const uint32_t* words;
+  Coords<R, kSoA> P;
+  const uint32_t* ext;    // this tile's external slots (global)
+  const uint32_t* recg;   // this tile's words (global)
+  int32_t ext_cap, rec_cap;
+  __device__ __forceinline__ R2 get(uint32_t l) const {
+    if constexpr (kStaged) {
+      return pts[l];
+    } else {
+      return l < static_cast<uint32_t>(kTile + ext_cap) ? pts[l] : P.load(__ldg(ext + l - kTile));
+    }
+  }
+  __device__ __forceinline__ uint32_t word(uint32_t w) const {
+    if constexpr (kStaged) {
+      return words[w];
+    } else {
+      return w < static_cast<uint32_t>(rec_cap) ? words[w] : __ldg(recg + w);
+    }
+  }
+};
+
+// Rare paths of tile_update, kept out of line so that their register needs do not shape the
+// main loop: the fan-record sweep of rows without a single link cycle (need_fast) and the
+// exact near-tie decision (quality.hpp:15-23 literal evaluation of the triangles whose fast
+// value lies within kGuard of the fast minimum; all of them when a fast value is not finite).
+template <typename R, bool kSoA, bool kStaged, int kSelf>
+__device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& tv, const uint16_t* fan, uint32_t w0,
+                                              uint32_t stride, int deg, typename Arith<R>::R2 pv,
+                                              typename Arith<R>::R2 cand, R thr, R hyp, bool bad, bool need_fast) {
+  using R2 = typename Arith<R>::R2;
+  constexpr bool kExact = sizeof(R) == 8;
+  constexpr R kInvK = R(1) / Arith<R>::kAlpha;
+  auto corners = [&](uint32_t f, R2* q, R2* c) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t p = fan_p(f, k);
+      q[k] = p == kSelf ? pv : tv.get(tv.word(w0 + p * stride) & 0xffffu);
+      c[k] = p == kSelf ? cand : q[k];
+    }
+  };
+  if (need_fast) {
+    R nan_acc = R(0);
+    thr = hyp = R(INFINITY);
+    for (int j = 0; j < deg; ++j) {
+      R2 q[3], c[3];
+      corners(__ldg(fan + j), q, c);
+      R tq = alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK;
+      R th = alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK;
+      if constexpr (!kExact) {
+        tq = isfinite(tq) ? tq : R(0);
+        th = isfinite(th) ? th : R(0);
+      }
+      nan_acc = fma(tq, th, nan_acc);
+      thr = min_ref(thr, tq);
+      hyp = min_ref(hyp, th);
+    }
+    bad = !(fabs(nan_acc) < R(1e30));
+    if constexpr (!kExact) return hyp > thr;
+    if (!bad && hyp > thr + R(kGuard)) return true;
+    if (!bad && hyp < thr - R(kGuard)) return false;
+  }
+  R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+  for (int j = 0; j < deg; ++j) {
+    R2 q[3], c[3];
+    corners(__ldg(fan + j), q, c);
+    if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK <= thr + R(kGuard))
+      thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
+    if (bad || alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK <= hyp + R(kGuard))
+      hyp_e = min_ref(hyp_e, alpha_plain<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y));
+  }
+  return hyp_e > thr_e;
+}
+
 // Tile-staged thread-per-vertex Form A fused update (small tier, deg <= kMaxDeg).
 //
 // One CTA owns kTile consecutive slots (a Hilbert-compact patch, degree-sorted inside).  It
-// first stages, with coalesced loads, the patch's pass-start coordinates, the coordinates of
-// the external slots its rows reference, the rows' words and the per-slot meta words in
-// shared memory; after one barrier every gather is a shared-memory read.  Word j of a row =
-// (row[j], cycle[j]) local indices: row[] in ascending ORIGINAL id (the summation order of
-// neighbor_mean, smoothing.hpp:72-80), cycle[] the directed link cycle (every incident triangle
-// is a rotation of (v, cycle[j], cycle[j+1])).  Rows of one valence are stored entry-major, so
-// the lanes of a (degree-uniform) warp read word j of consecutive rows without bank conflicts.
-// The decision arithmetic is ring_update's: fast α/K filter over the cycle, exact literal
-// evaluation over the fan records for near-ties and for rows without a link cycle.
+// stages in shared memory the patch's pass-start coordinates, the rows' words and the per-slot
+// meta words with bulk copies (TMA, one mbarrier), and the coordinates of the external slots
+// its rows reference with asynchronous 16-byte copies; after one barrier every gather is a
+// shared-memory read.  Word j of a row = (row[j], cycle[j]) local indices: row[] in ascending
+// ORIGINAL id (the summation order of neighbor_mean, smoothing.hpp:72-80), cycle[] the directed
+// link cycle (every incident triangle is a rotation of (v, cycle[j], cycle[j+1])).  Rows of one
+// valence are stored entry-major, so the lanes of a (degree-uniform) warp read word j of
+// consecutive rows without bank conflicts.  The decision arithmetic is ring_update's: fast α/K
+// filter over the cycle; rows without a link cycle and near-ties go to tile_decide_rare.
 // kStaged: every tile's external coordinates and words fit the shared-memory caps.
 template <typename R, bool kSoA, int kThreads, int kMaxDeg, bool kStaged>
-__global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
+__global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
   using O = Arith<R>;
   using R2 = typename O::R2;
-  constexpr int kSelf = kMaxDeg;  // v's position in the small tier's fan16 records
   constexpr bool kExact = sizeof(R) == 8;
   static_assert(kTile % kThreads == 0, "whole vertices per thread");
   extern __shared__ __align__(16) unsigned char tile_smem[];
+  __shared__ uint64_t bar;
   R2* pts = reinterpret_cast<R2*>(tile_smem);
   uint32_t* words = reinterpret_cast<uint32_t*>(pts + kTile + t.ext_cap);
   uint32_t* meta_s = words + t.rec_cap;
@@ -567,33 +689,39 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
   const uint32_t r0 = __ldg(t.tile_rec + blockIdx.x), nr = __ldg(t.tile_rec + blockIdx.x + 1) - r0;
   const int n_ext = static_cast<int>(kStaged || ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
   const int n_rec = static_cast<int>(kStaged || nr < static_cast<uint32_t>(t.rec_cap) ? nr : t.rec_cap);
-  for (int i = tid; i < n_in; i += kThreads) {
-    pts[i] = P.load(base + i);
-    meta_s[i] = __ldg(t.meta + base + i);
+  // Bulk copies: full AoS tiles (coordinates and meta are then 16-byte multiples); the rest
+  // (SoA, the partial last tile) goes through the load/store units.
+  const bool bulk = !kSoA && n_in == kTile;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    if (bulk) {
+      const uint32_t bytes = kTile * sizeof(R2) + kTile * 4u + 4u * n_rec;
+      mbar_expect_tx(&bar, bytes);
+      bulk_g2s(pts, P.base + 2 * base, kTile * sizeof(R2), &bar);
+      bulk_g2s(meta_s, t.meta + base, kTile * 4u, &bar);
+      if (n_rec > 0) bulk_g2s(words, t.rec + r0, 4u * n_rec, &bar);
+    }
   }
-  for (int k = tid; k < n_ext; k += kThreads) pts[kTile + k] = P.load(__ldg(t.ext + e0 + k));
-  {
+  if (!bulk) {
+    for (int i = tid; i < n_in; i += kThreads) {
+      pts[i] = P.load(base + i);
+      meta_s[i] = __ldg(t.meta + base + i);
+    }
     const uint4* src = reinterpret_cast<const uint4*>(t.rec + r0);
     uint4* dst = reinterpret_cast<uint4*>(words);
     for (int k = tid; k < n_rec / 4; k += kThreads) dst[k] = __ldg(src + k);
   }
-  __syncthreads();
+  if constexpr (kSoA) {
+    for (int k = tid; k < n_ext; k += kThreads) pts[kTile + k] = P.load(__ldg(t.ext + e0 + k));
+  } else {
+    for (int k = tid; k < n_ext; k += kThreads)
+      cp_async<sizeof(R2)>(pts + kTile + k, reinterpret_cast<const R2*>(P.base) + __ldg(t.ext + e0 + k));
+    cp_async_wait_all();
+  }
+  __syncthreads();  // also publishes the mbarrier initialisation
+  if (bulk) mbar_wait(&bar, 0);
 
-  auto get = [&](uint32_t l) -> R2 {
-    if constexpr (kStaged) {
-      return pts[l];
-    } else {
-      return l < static_cast<uint32_t>(kTile + t.ext_cap) ? pts[l] : P.load(__ldg(t.ext + e0 + l - kTile));
-    }
-  };
-  auto word = [&](uint32_t w) -> uint32_t {
-    if constexpr (kStaged) {
-      return words[w];
-    } else {
-      return w < static_cast<uint32_t>(t.rec_cap) ? words[w] : __ldg(t.rec + r0 + w);
-    }
-  };
-
+  const TileView<R, kSoA, kStaged> tv{pts, words, P, t.ext + e0, t.rec + r0, t.ext_cap, t.rec_cap};
   int accepted = 0;
   double disp = 0.0;
 #pragma unroll 1
@@ -606,19 +734,22 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
     R sx = R(0), sy = R(0);
 #pragma unroll 2
     for (int j = 0; j < deg; ++j) {
-      const R2 c = get(word(w0 + j * stride) & 0xffffu);
+      const R2 c = tv.get(tv.word(w0 + j * stride) & 0xffffu);
       sx = O::add(sx, c.x);
       sy = O::add(sy, c.y);
     }
     const R inv = inv_deg<R>(deg);
     const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-    const bool tie = cand.x == pv.x && cand.y == pv.y;
     const int64_t s = base + i;
-    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
-    if (!tie) {
-      const uint32_t l0 = word(w0) >> 16;
-      if (l0 != kNoLocal) {
-        RingEdge<R> ea = ring_edge<R>(get(l0), pv, cand);
+    bool acc = false;
+    // Exact tie (candidate == position; Form A reads only pass-start values): every
+    // hypothetical α equals its threshold α bit for bit, the strict test fails.
+    if (!(cand.x == pv.x && cand.y == pv.y)) {
+      const uint32_t l0 = tv.word(w0) >> 16;
+      R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+      const bool cyc = l0 != kNoLocal;
+      if (cyc) {
+        RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
         auto tri = [&](const RingEdge<R>& x, const RingEdge<R>& y) {
           const R ex = y.px - x.px, ey = y.py - x.py;
           const R lab = fma(ex, ex, ey * ey);
@@ -636,65 +767,34 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
         };
 #pragma unroll 2
         for (int j = 1; j < deg; ++j) {
-          const RingEdge<R> eb = ring_edge<R>(get(word(w0 + j * stride) >> 16), pv, cand);
+          const RingEdge<R> eb = ring_edge<R>(tv.get(tv.word(w0 + j * stride) >> 16), pv, cand);
           tri(ea, eb);
           ea = eb;
         }
-        tri(ea, ring_edge<R>(get(l0), pv, cand));  // closing triangle (recomputed, saves registers)
+        tri(ea, ring_edge<R>(tv.get(l0), pv, cand));  // closing triangle (recomputed: registers)
+      }
+      const bool bad = !(fabs(nan_acc) < R(1e30));
+      if (cyc && !kExact) {
+        acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
+      } else if (cyc && !bad && hyp > thr + R(kGuard)) {
+        acc = true;
+      } else if (cyc && !bad && hyp < thr - R(kGuard)) {
+        acc = false;
+      } else if (cyc) {
+        // Near-tie (or a degenerate triangle): decided exactly by tie_update, which runs over
+        // the queue after this kernel with full warps instead of one divergent lane here.
+        if (a.rare) atomicAdd(a.rare + pass, 1ull);
+        const unsigned mask = __activemask();
+        const int leader = __ffs(mask) - 1, lane = threadIdx.x & 31;
+        int slot0 = 0;
+        if (lane == leader) slot0 = atomicAdd(&a.st->queued, __popc(mask));
+        slot0 = __shfl_sync(mask, slot0, leader);
+        a.queue[slot0 + __popc(mask & ((1u << lane) - 1u))] = static_cast<int32_t>(s);
+        continue;
       } else {
-        // No single link cycle: literal triangles from the fan records (α/K scale).
-        constexpr R kInvK = R(1) / Arith<R>::kAlpha;
-        const uint16_t* fan = a.fan16 + __ldg(a.off + s);
-        for (int j = 0; j < deg; ++j) {
-          const uint32_t f = __ldg(fan + j);
-          R2 q[3], c[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const uint32_t p = fan_p(f, k);
-            q[k] = p == kSelf ? pv : get(word(w0 + p * stride) & 0xffffu);
-            c[k] = p == kSelf ? cand : q[k];
-          }
-          R tq = alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK;
-          R th = alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK;
-          if constexpr (!kExact) {
-            tq = isfinite(tq) ? tq : R(0);
-            th = isfinite(th) ? th : R(0);
-          }
-          nan_acc = fma(tq, th, nan_acc);
-          thr = min_ref(thr, tq);
-          hyp = min_ref(hyp, th);
-        }
+        acc = tile_decide_rare<R, kSoA, kStaged, kMaxDeg>(tv, a.fan16 + __ldg(a.off + s), w0, stride, deg, pv, cand,
+                                                          thr, hyp, bad, true);
       }
-    }
-    const bool bad = !(fabs(nan_acc) < R(1e30));
-    bool acc;
-    if (tie) {
-      acc = false;
-    } else if constexpr (!kExact) {
-      acc = hyp > thr;
-    } else if (!bad && hyp > thr + R(kGuard)) {
-      acc = true;
-    } else if (!bad && hyp < thr - R(kGuard)) {
-      acc = false;
-    } else {
-      constexpr R kInvK = R(1) / Arith<R>::kAlpha;
-      const uint16_t* fan = a.fan16 + __ldg(a.off + s);
-      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
-      for (int j = 0; j < deg; ++j) {
-        const uint32_t f = __ldg(fan + j);
-        R2 q[3], c[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const uint32_t p = fan_p(f, k);
-          q[k] = p == kSelf ? pv : get(word(w0 + p * stride) & 0xffffu);
-          c[k] = p == kSelf ? cand : q[k];
-        }
-        if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK <= thr + R(kGuard))
-          thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
-        if (bad || alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK <= hyp + R(kGuard))
-          hyp_e = min_ref(hyp_e, alpha_plain<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y));
-      }
-      acc = hyp_e > thr_e;
     }
     N.store(s, acc ? cand : pv);
     if (acc) {
@@ -704,6 +804,65 @@ __global__ void __launch_bounds__(kThreads, 2048 / kThreads / 2) tile_update(Pas
       disp = d > disp ? d : disp;
     }
     if (a.decision) a.decision[s] = acc ? 1 : 0;
+  }
+  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+}
+
+// Exact decisions of the near-tie vertices queued by tile_update (Form A fused, fp64): thread
+// per queued slot, the reference's arithmetic throughout — ordered neighbour sum, literal
+// triangle_alpha with IEEE division for every incident triangle at the pass-start position and
+// at the candidate (quality.hpp:15-23, :54-64), strict test (smoothing.hpp:99).
+template <typename R, bool kSoA>
+__global__ void __launch_bounds__(128) tie_update(PassArgs<R, kSoA> a) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+  const int64_t count = a.st->queued;
+  int accepted = 0;
+  double disp = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  // Warp-uniform trip count (commit_stats_warp needs the whole warp).
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t w = first; w < count; w += stride) {
+    const int64_t k = w + (threadIdx.x & 31);
+    if (k >= count) continue;
+    const int64_t s = a.queue[k];
+    const uint32_t o0 = __ldg(a.off + s);
+    const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
+    const uint32_t* nb = a.nbr + o0;
+    const uint32_t* fan = a.fan + o0;
+    const R2 pv = P.load(s);
+    R sx = R(0), sy = R(0);
+    for (int j = 0; j < deg; ++j) {
+      const R2 c = P.load(__ldg(nb + j));
+      sx = O::add(sx, c.x);
+      sy = O::add(sy, c.y);
+    }
+    const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
+    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    R thr = R(INFINITY), hyp = R(INFINITY);
+    for (int j = 0; j < deg; ++j) {
+      const uint32_t f = __ldg(fan + j);
+      const R2 qa = P.load(__ldg(nb + fan_i1(f))), qb = P.load(__ldg(nb + fan_i2(f)));
+      const int kk = fan_k(f);
+      const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+      const R sabx = O::mul(dabx, dabx), saby = O::mul(daby, daby);
+      thr = min_ref(thr, alpha_at<R>(kk, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby));
+      hyp = min_ref(hyp, alpha_at<R>(kk, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby));
+    }
+    const bool acc = hyp > thr;
+    N.store(s, acc ? cand : pv);
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+    if (acc) {
+      ++accepted;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      disp = d > disp ? d : disp;
+    }
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
 }
@@ -1036,6 +1195,7 @@ __global__ void finalize_pass(PassState* st, const int32_t* slot_acc, const unsi
     mdb = other > mdb ? other : mdb;
   }
   if (lane != 0) return;
+  st->queued = 0;  // tile_update's near-tie queue has been drained by tie_update
   if (!done) {
     pass_acc[q] = acc;
     pass_md[q] = mdb;
