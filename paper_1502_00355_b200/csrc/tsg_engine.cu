@@ -45,7 +45,7 @@ constexpr tsg::Tiers kTiers{kMaxSmallDeg, kMaxMedDeg};
 constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
-constexpr int kTileRecCap = 8192;  // ... row words staged in shared memory (multiple of 4)
+constexpr int kTileRecCap = 12288;  // ... row words staged in shared memory (multiple of 4)
 constexpr int kTieBlocks = 148 * 4;  // tie_update: persistent grid over the near-tie queue
 constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
@@ -392,14 +392,13 @@ struct Engine {
     return TSG_OK;
   }
 
-  // Form A, fused: cycle sweep (thread per vertex) over every slot with deg <= kMaxSmallDeg and
-  // over the 11..15 list, warp per vertex above.  The list tiers run on the side stream.
+  // Form A, fused: tile-staged cycle sweep (thread per vertex) over every slot with deg <=
+  // kMaxCycleDeg, then the exact near-tie queue; warp per vertex above, on the side stream.
   static tsg_status launch_form_a_fused(tsg_mesh* m, const Args& base, cudaStream_t s, int64_t* kernels) {
     tsg_context* ctx = m->ctx;
-    const int64_t nv = m->hm.nv, nmid = static_cast<int64_t>(m->hm.cyc_mid.size()),
-                  nlarge = static_cast<int64_t>(m->hm.large.size());
+    const int64_t nv = m->hm.nv, nlarge = static_cast<int64_t>(m->hm.large.size());
     static const bool serial = std::getenv("TSG_SERIAL_TIERS") != nullptr;  // experiment knob
-    const bool fork = !serial && (nmid > 0 || nlarge > 0);
+    const bool fork = !serial && nlarge > 0;
     cudaStream_t t = s;
     if (fork) {
       cudaEvent_t e;
@@ -418,16 +417,6 @@ struct Engine {
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
-    if (nmid > 0) {
-      constexpr int kB = 64;
-      Args a = base;
-      a.list = m->d_cyc_mid;
-      a.count = nmid;
-      tsg::ring_update<R, kSoA, tsg::kMaxCycleDeg, kMaxMedDeg, kB>
-          <<<static_cast<unsigned>((nmid + kB - 1) / kB), kB, 0, t>>>(a, m->d_cyc);
-      TSG_CUDA(cudaGetLastError());
-      ++*kernels;
-    }
     {
       Args a = base;
       a.list = nullptr;
@@ -436,9 +425,9 @@ struct Engine {
       const unsigned ntiles = static_cast<unsigned>((nv + tsg::kTile - 1) / tsg::kTile);
       const size_t smem = tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap);
       if (tiles_staged(m))
-        tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, true><<<ntiles, kTileThreads, smem, s>>>(a, ta);
+        tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       else
-        tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
+        tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
       if constexpr (sizeof(R) == 8) {  // fp64: exact decisions of the queued near-ties
@@ -516,6 +505,8 @@ struct Engine {
     t.ext = m->d_tile_ext;
     t.ext_cap = std::min(m->hm.max_ext, kTileExtCap);
     t.rec_cap = std::min(m->hm.max_rec_words, kTileRecCap);
+    t.small_max = kMaxSmallDeg;
+    t.medium_max = kMaxMedDeg;
     t.nv = m->hm.nv;
     return t;
   }
@@ -525,9 +516,9 @@ struct Engine {
     {
       const tsg::TileArgs ta = tile_args(m);
       const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap));
-      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, true>,
+      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, kMaxSmallDeg, false>,
+      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));

@@ -524,6 +524,8 @@ struct TileArgs {
   const uint32_t* ext;       // external slots
   int32_t ext_cap;           // external coordinates staged in shared memory per tile
   int32_t rec_cap;           // words staged in shared memory per tile (multiple of 4)
+  int32_t small_max;         // rows with deg <= small_max have v at fan16 position small_max,
+  int32_t medium_max;        // the others at medium_max (tsg_prep.cpp)
   int64_t nv;
 };
 
@@ -603,9 +605,9 @@ struct TileView {
 // main loop: the fan-record sweep of rows without a single link cycle (need_fast) and the
 // exact near-tie decision (quality.hpp:15-23 literal evaluation of the triangles whose fast
 // value lies within kGuard of the fast minimum; all of them when a fast value is not finite).
-template <typename R, bool kSoA, bool kStaged, int kSelf>
-__device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& tv, const uint16_t* fan, uint32_t w0,
-                                              uint32_t stride, int deg, typename Arith<R>::R2 pv,
+template <typename R, bool kSoA, bool kStaged>
+__device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& tv, const uint16_t* fan, uint32_t kSelf,
+                                              uint32_t w0, uint32_t stride, int deg, typename Arith<R>::R2 pv,
                                               typename Arith<R>::R2 cand, R thr, R hyp, bool bad, bool need_fast) {
   using R2 = typename Arith<R>::R2;
   constexpr bool kExact = sizeof(R) == 8;
@@ -792,8 +794,9 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
         a.queue[slot0 + __popc(mask & ((1u << lane) - 1u))] = static_cast<int32_t>(s);
         continue;
       } else {
-        acc = tile_decide_rare<R, kSoA, kStaged, kMaxDeg>(tv, a.fan16 + __ldg(a.off + s), w0, stride, deg, pv, cand,
-                                                          thr, hyp, bad, true);
+        const uint32_t self = static_cast<uint32_t>(deg <= t.small_max ? t.small_max : t.medium_max);
+        acc = tile_decide_rare<R, kSoA, kStaged>(tv, a.fan16 + __ldg(a.off + s), self, w0, stride, deg, pv, cand, thr,
+                                                 hyp, bad, true);
       }
     }
     N.store(s, acc ? cand : pv);

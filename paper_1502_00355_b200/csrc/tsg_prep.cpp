@@ -87,7 +87,7 @@ uint32_t hilbert_d(uint32_t x, uint32_t y) {
 // Tile records (see tsg_prep.hpp).  Per tile: the sorted external slots referenced by its
 // small rows; the small rows grouped by valence (slot order inside a group), each group's
 // words stored entry-major: word j of the k-th row of a group of n rows at group base + j*n + k.
-void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_max) {
+void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg) {
   const int64_t nv = hm.nv;
   const int64_t ntiles = (nv + kTile - 1) / kTile;
   hm.tmeta.assign(nv, 0);
@@ -95,7 +95,7 @@ void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_m
   hm.ext_off.assign(ntiles + 1, 0);
   std::vector<std::vector<uint32_t>> ext(ntiles);
   std::vector<uint32_t> words(ntiles, 0);
-  auto is_small = [&](int64_t s) { return deg[s] >= 1 && deg[s] <= static_cast<uint32_t>(small_max); };
+  auto is_small = [&](int64_t s) { return deg[s] >= 1 && deg[s] <= static_cast<uint32_t>(max_deg); };
   parallel_ranges(ntiles, [&](int64_t tb, int64_t te) {
     for (int64_t t = tb; t < te; ++t) {
       const int64_t base = t * kTile, end = std::min(nv, base + kTile);
@@ -110,7 +110,7 @@ void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_m
         }
       }
       uint32_t gbase[kMaxCycleDeg + 1], fill[kMaxCycleDeg + 1] = {}, w = 0;
-      for (int d = 1; d <= small_max; ++d) {
+      for (int d = 1; d <= max_deg; ++d) {
         gbase[d] = w;
         w += static_cast<uint32_t>(d) * count[d];
       }
@@ -391,7 +391,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
         hm.large.push_back(static_cast<int32_t>(s));
     }
   }
-  build_tiles(hm, deg, tiers.small_max);
+  build_tiles(hm, deg, kMaxCycleDeg);
   // Longest rows first: the warp tier's tail is its largest hubs.
   std::stable_sort(hm.large.begin(), hm.large.end(), [&](int32_t x, int32_t y) { return deg[x] > deg[y]; });
   return "";

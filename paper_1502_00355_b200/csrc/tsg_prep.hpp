@@ -55,7 +55,7 @@ struct HostMesh {
   // thread per vertex) and the rest (warp per vertex).
   std::vector<int32_t> cyc_mid;
   std::vector<int32_t> large;
-  // Tiles (small rows only; other rows have tmeta == 0):
+  // Tiles (rows with 1 <= deg <= kMaxCycleDeg; other rows have tmeta == 0):
   //   tmeta[s]     word offset of row s's first word inside its tile's words (bits 0-15) |
   //                deg << kMetaDegShift | stride << kMetaStrideShift (word j at offset + j*stride)
   //   tile_rec[t]  first word of tile t (ntiles + 1; multiples of 4)
@@ -86,6 +86,6 @@ struct FormBSchedule {
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
 std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
-void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t small_max);
+void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg);
 
 }  // namespace tsg
