@@ -176,6 +176,11 @@ tsg_status tsg_halo_unpack(tsg_mesh* mesh, const double* in, int32_t in_is_host)
  * fast path is only trusted outside a 2^-45 guard band (tsg_device.cuh). */
 tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_t newton_steps,
                               double* max_abs_err_out, int64_t* nonfinite_out);
+/* The same for the rotation (cycle) fast path of the Form A fused kernels: the maximum
+ * |t - alpha_ref / K| in alpha/K units, K = 2*sqrt(3) as the reference rounds it.  Its guard
+ * band is 2^-47 in those units (derivation in tsg_device.cuh, kGuardCycle). */
+tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, double* max_abs_err_out,
+                                    int64_t* nonfinite_out);
 
 /* ---- locality ordering (host prep helper) ---- */
 /* order_out[s] = original id for slot s: vertices sorted along a Hilbert curve over the

@@ -31,7 +31,7 @@ EXPORTS = (
     "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_mesh_restore_coords",
     "tsg_tri_alpha",
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
-    "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_pass", "tsg_halo_plan",
+    "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
     "tsg_halo_pack", "tsg_halo_unpack",
 )
 
@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
             "tsg_pass_lockstep": (i32, [P, i32, i32, P, P, P]),
             "tsg_hilbert_order": (i32, [i64, P, P]),
             "tsg_selftest_alpha": (i32, [P, i64, C.c_uint64, i32, P, P]),
+            "tsg_selftest_alpha_cycle": (i32, [P, i64, C.c_uint64, P, P]),
             "tsg_pass": (i32, [P, C.POINTER(SmoothCfg), P, P]),
             "tsg_halo_plan": (i32, [P, P, i64, P, i64]),
             "tsg_halo_pack": (i32, [P, C.c_void_p, i32]),
@@ -127,6 +128,12 @@ class Context:
         err, bad = C.c_double(), C.c_int64()
         check(lib().tsg_selftest_alpha(self.h, n, seed, newton_steps, C.byref(err), C.byref(bad)),
               "tsg_selftest_alpha")
+        return err.value, bad.value
+
+    def selftest_alpha_cycle(self, n=1 << 22, seed=1):
+        err, bad = C.c_double(), C.c_int64()
+        check(lib().tsg_selftest_alpha_cycle(self.h, n, seed, C.byref(err), C.byref(bad)),
+              "tsg_selftest_alpha_cycle")
         return err.value, bad.value
 
     def close(self):

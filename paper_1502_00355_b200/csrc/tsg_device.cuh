@@ -143,6 +143,17 @@ __device__ __forceinline__ float rcp_refined(float x) {
 
 // Decisions whose fast-path margin is within kGuard (absolute; |α| <= 1) are settled exactly.
 constexpr double kGuard = 0x1p-45;
+// Guard of the rotation (cycle) fast path, in α/K units.  With u = 2^-53, per triangle the fast
+// value t = ((a-v) x (b-v)) * rcp(|a-v|^2 + |b-v|^2 + |b-a|^2) (FMA, refined reciprocal with
+// relative error <= 3u) is within 6.7u of the real τ = X/S (numerator error <= 2.01u·S,
+// denominator <= 12u·S, |τ| <= 1/K), and the reference's α/K is within 5u of τ (numerator
+// 2.01u·S, edge-square sum 8u·S, two final roundings); the minima over the fan are 1-Lipschitz,
+// so hyp - thr is known to within 2 x 11.7u = 23.4u < 2^-48.5.  kGuardCycle = 64u leaves a
+// factor 2.7; tsg_selftest_alpha (formula 1) measures the per-triangle error on the device.
+// Valid while every coordinate magnitude is below 2^500 (no overflow / flushed reciprocal);
+// beyond that the engine sets PassArgs::exact_only.
+constexpr double kGuardCycle = 0x1p-47;
+constexpr double kExactOnlyAbove = 0x1p500;
 
 // triangle_alpha with the division replaced by the refined reciprocal; everything before the
 // division is the reference's exact operation sequence.  A degenerate triangle (es == 0 or a
@@ -187,7 +198,7 @@ struct PassState {
   int32_t pass;  // index of the pass being executed
   int32_t done;  // 1 once a stop rule fired
   int32_t stop;  // TSG_STOP_*
-  int32_t queued;  // near-tie vertices queued by tile_update this pass (reset by finalize_pass)
+  int32_t pad;
 };
 
 }  // namespace tsg

@@ -46,7 +46,6 @@ constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
 constexpr int kTileRecCap = 12288;  // ... row words staged in shared memory (multiple of 4)
-constexpr int kTieBlocks = 148 * 4;  // tie_update: persistent grid over the near-tie queue
 constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
@@ -71,16 +70,36 @@ tsg_status upload(T** p, const std::vector<T>& v, int64_t* bytes, cudaStream_t s
 }
 
 // Gather original-order f64 pairs into slot order (both buffers) and back.
+// Largest coordinate magnitude as ordered u64 bits (NaN counts as +inf): per-thread maximum,
+// then one warp reduction and one atomic per warp at the end of the grid-stride loop.
+__device__ __forceinline__ double abs_max2(double x, double y) {
+  return (x != x || y != y) ? INFINITY : fmax(fabs(x), fabs(y));
+}
+__device__ __forceinline__ void commit_maxabs(double m, unsigned long long* maxabs) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(m));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long c = __shfl_xor_sync(0xffffffffu, b, o);
+    b = c > b ? c : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(maxabs, b);
+}
+
 template <typename R, bool kSoA>
 __global__ void coords_from_orig(const double* __restrict__ xy, const int64_t* __restrict__ order,
-                                 int64_t nv, tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1) {
+                                 int64_t nv, tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1,
+                                 unsigned long long* maxabs) {
+  double m = 0.0;
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t v = order ? order[s] : s;
-    const auto p = tsg::Arith<R>::make(static_cast<R>(xy[2 * v]), static_cast<R>(xy[2 * v + 1]));
+    const double x = xy[2 * v], y = xy[2 * v + 1];
+    const auto p = tsg::Arith<R>::make(static_cast<R>(x), static_cast<R>(y));
     b0.store(s, p);
     b1.store(s, p);
+    m = fmax(m, abs_max2(x, y));
   }
+  commit_maxabs(m, maxabs);
 }
 
 template <typename R, bool kSoA>
@@ -118,13 +137,17 @@ __global__ void halo_pack(tsg::Coords<R, kSoA> cur, const int32_t* __restrict__ 
 
 template <typename R, bool kSoA>
 __global__ void halo_unpack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1, const int32_t* __restrict__ slots,
-                            int64_t n, const double* __restrict__ in) {
+                            int64_t n, const double* __restrict__ in, unsigned long long* maxabs) {
+  double m = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const auto p = tsg::Arith<R>::make(static_cast<R>(in[2 * i]), static_cast<R>(in[2 * i + 1]));
+    const double x = in[2 * i], y = in[2 * i + 1];
+    const auto p = tsg::Arith<R>::make(static_cast<R>(x), static_cast<R>(y));
     b0.store(slots[i], p);
     b1.store(slots[i], p);
+    m = fmax(m, abs_max2(x, y));
   }
+  commit_maxabs(m, maxabs);
 }
 
 __global__ void scatter_i8(const int8_t* __restrict__ in, const int64_t* __restrict__ order,
@@ -174,6 +197,42 @@ unsigned grid_for(int64_t n, int block) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 64)));
 }
 
+// The cycle path's fast α/K (ring_pair, v at a random rotation of the triangle) against the
+// reference's literal α / K: max |t - α_ref/K| in α/K units (error analysis: kGuardCycle).
+__global__ void selftest_alpha_cycle(int64_t n, uint64_t seed, unsigned long long* max_err,
+                                     unsigned long long* nonfinite) {
+  constexpr double K = tsg::Arith<double>::kAlpha;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double c[6];
+    const uint64_t h = mix64(seed ^ static_cast<uint64_t>(i));
+    const double scale = __longlong_as_double(static_cast<long long>((1023ULL + (h % 61) - 30) << 52));
+    const double off = (h >> 40) & 1 ? 0.0 : scale * 37.0;  // also away from the origin
+    for (int k = 0; k < 6; ++k)
+      c[k] = off + (static_cast<double>(mix64(h + 7 * k + 1) >> 11) * 0x1.0p-53 - 0.5) * scale;
+    if ((h >> 60) == 0) {  // near-degenerate: third corner almost on the first edge
+      const double t = static_cast<double>(mix64(h + 99) >> 11) * 0x1.0p-53;
+      c[4] = c[0] + t * (c[2] - c[0]) + 1e-9 * scale;
+      c[5] = c[1] + t * (c[3] - c[1]);
+    }
+    const double e = tsg::alpha_plain<double>(c[0], c[1], c[2], c[3], c[4], c[5]);
+    const int r = static_cast<int>((h >> 20) % 3);  // v = p_r, then the cyclic successors
+    const double2 v = make_double2(c[2 * r], c[2 * r + 1]);
+    const double2 a = make_double2(c[2 * ((r + 1) % 3)], c[2 * ((r + 1) % 3) + 1]);
+    const double2 b = make_double2(c[2 * ((r + 2) % 3)], c[2 * ((r + 2) % 3) + 1]);
+    double tp, tc;
+    tsg::ring_pair<double>(tsg::ring_edge<double>(a, v, v), tsg::ring_edge<double>(b, v, v), tp, tc);
+    if (!(fabs(tp) <= 1.0)) {
+      atomicAdd(nonfinite, 1ULL);
+      continue;
+    }
+    if (fabs(e) <= 1.0) {
+      const double d = fabs(fma(tp, K, -e)) / K;
+      atomicMax(max_err, static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
+  }
+}
+
 struct GraphCache {
   bool valid = false;
   int32_t form = -1, strategy = -1, chunks = -1, swap = -1, max_iters = -1;
@@ -213,12 +272,12 @@ struct tsg_mesh {
   void* buf[2] = {nullptr, nullptr};
   void* init = nullptr;  // slot-ordered copy of the coordinates given at upload / set_coords
   uint16_t* d_fan16 = nullptr;
-  uint64_t* d_cyc = nullptr;
   uint32_t *d_tmeta = nullptr, *d_tile_rec = nullptr, *d_ext_off = nullptr, *d_tile_ext = nullptr;
   uint32_t* d_trec = nullptr;
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
-  int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr, *d_cyc_mid = nullptr, *d_large = nullptr;
+  int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr, *d_large = nullptr;
+  unsigned long long* d_maxabs = nullptr;  // bits of max |coordinate|
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   void* d_alpha = nullptr;
   double* d_xy_stage = nullptr;  // 2*nv original-order doubles
@@ -230,7 +289,6 @@ struct tsg_mesh {
   int32_t* d_sacc = nullptr;           // per-pass stat slots (kStatSlots each)
   unsigned long long* d_smd = nullptr;
   unsigned long long* d_rare = nullptr;  // diagnostics: rare-path decisions per pass
-  int32_t* d_queue = nullptr;            // near-tie queue (nv)
   unsigned long long* d_ext = nullptr;  // extrema scratch (3)
   int32_t cap = 0;
   int cur = 0;
@@ -322,7 +380,7 @@ struct Engine {
     a.slot_md = m->d_smd;
     a.decision = nullptr;
     a.rare = diag_enabled() ? m->d_rare : nullptr;
-    a.queue = m->d_queue;
+    a.maxabs = m->d_maxabs;
     return a;
   }
 
@@ -393,7 +451,7 @@ struct Engine {
   }
 
   // Form A, fused: tile-staged cycle sweep (thread per vertex) over every slot with deg <=
-  // kMaxCycleDeg, then the exact near-tie queue; warp per vertex above, on the side stream.
+  // kMaxCycleDeg; warp per vertex above, on the side stream.
   static tsg_status launch_form_a_fused(tsg_mesh* m, const Args& base, cudaStream_t s, int64_t* kernels) {
     tsg_context* ctx = m->ctx;
     const int64_t nv = m->hm.nv, nlarge = static_cast<int64_t>(m->hm.large.size());
@@ -430,11 +488,7 @@ struct Engine {
         tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
-      if constexpr (sizeof(R) == 8) {  // fp64: exact decisions of the queued near-ties
-        tsg::tie_update<R, kSoA><<<kTieBlocks, 128, 0, s>>>(a);
-        TSG_CUDA(cudaGetLastError());
-        ++*kernels;
-      }
+
     }
     if (fork) {
       cudaEvent_t e;
@@ -544,9 +598,10 @@ struct Engine {
     cudaStream_t s = m->ctx->stream;
     const int64_t nv = m->hm.nv;
     TSG_CUDA(cudaMemcpyAsync(m->d_xy_stage, xy_host, 2 * nv * sizeof(double), cudaMemcpyHostToDevice, s));
+    TSG_CUDA(cudaMemsetAsync(m->d_maxabs, 0, sizeof(unsigned long long), s));
     coords_from_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(m->d_xy_stage, m->d_order, nv,
                                                                 coords_of<R, kSoA>(m, 0),
-                                                                coords_of<R, kSoA>(m, 1));
+                                                                coords_of<R, kSoA>(m, 1), m->d_maxabs);
     TSG_CUDA(cudaGetLastError());
     TSG_CUDA(cudaMemcpyAsync(m->init, m->buf[0], 2 * nv * sizeof(R), cudaMemcpyDeviceToDevice, s));
     m->cur = 0;
@@ -625,7 +680,7 @@ tsg_status ensure_stats_capacity(tsg_mesh* m, int32_t n) {
   TSG_CUDA(cudaMalloc(&m->d_smd, sizeof(unsigned long long) * n * tsg::kStatSlots));
   cudaFree(m->d_rare);
   m->d_rare = nullptr;
-  TSG_CUDA(cudaMalloc(&m->d_rare, sizeof(unsigned long long) * n));
+  TSG_CUDA(cudaMalloc(&m->d_rare, sizeof(unsigned long long) * (n + 16)));
   m->cap = n;
   m->gc.reset();  // graph captured old pointers
   return TSG_OK;
@@ -704,6 +759,24 @@ tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_
   return TSG_OK;
 }
 
+tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, double* max_abs_err_out,
+                                    int64_t* nonfinite_out) {
+  if (!ctx || n < 0) return fail(TSG_ERR_INVALID, "bad arguments");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  unsigned long long* d = nullptr;
+  TSG_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+  TSG_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  selftest_alpha_cycle<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, seed, d, d + 1);
+  TSG_CUDA(cudaGetLastError());
+  unsigned long long h[2];
+  TSG_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d);
+  if (max_abs_err_out) std::memcpy(max_abs_err_out, &h[0], sizeof(double));
+  if (nonfinite_out) *nonfinite_out = static_cast<int64_t>(h[1]);
+  return TSG_OK;
+}
+
 tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** out) {
   if (!ctx || !d || !out) return fail(TSG_ERR_INVALID, "null argument");
   if (!d->xy || !d->tri || !d->nbr_off || !d->nbr || !d->inc_off || !d->inc || !d->boundary)
@@ -733,7 +806,6 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_nbr, hm.nbr, b, s))) return st;
   if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
   if ((st = upload(&m->d_fan16, hm.fan16, b, s))) return st;
-  if ((st = upload(&m->d_cyc, hm.cyc, b, s))) return st;
   if ((st = upload(&m->d_tmeta, hm.tmeta, b, s))) return st;
   if ((st = upload(&m->d_tile_rec, hm.tile_rec, b, s))) return st;
   if ((st = upload(&m->d_ext_off, hm.ext_off, b, s))) return st;
@@ -744,7 +816,6 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
   if ((st = upload(&m->d_hubs, hm.hubs, b, s))) return st;
   if ((st = upload(&m->d_medium, hm.medium, b, s))) return st;
-  if ((st = upload(&m->d_cyc_mid, hm.cyc_mid, b, s))) return st;
   if ((st = upload(&m->d_large, hm.large, b, s))) return st;
   if (d->order) {
     if ((st = upload(&m->d_order, hm.order, b, s))) return st;
@@ -757,7 +828,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = dalloc(&m->d_decision, nv, b))) return st;
   if ((st = dalloc(&m->d_decision_orig, nv, b))) return st;
   if ((st = dalloc(&m->d_state, 1, b))) return st;
-  if ((st = dalloc(&m->d_queue, nv, b))) return st;
+  if ((st = dalloc(&m->d_maxabs, 1, b))) return st;
   if ((st = dalloc(&m->d_ext, 3, b))) return st;
   for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
   if ((st = ensure_stats_capacity(m.get(), 128))) return st;
@@ -775,10 +846,10 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
   free_form_b(m);
-  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_cyc, m->d_tmeta, m->d_tile_rec, m->d_ext_off, m->d_tile_ext, m->d_trec, m->d_vinc_off, m->d_vinc,
-                  m->d_tri, m->d_hubs, m->d_medium, m->d_cyc_mid, m->d_large, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
+  void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_tmeta, m->d_tile_rec, m->d_ext_off, m->d_tile_ext, m->d_trec, m->d_vinc_off, m->d_vinc,
+                  m->d_tri, m->d_hubs, m->d_medium, m->d_large, m->d_maxabs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
-                  m->d_ext, m->d_rare, m->d_queue, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
+                  m->d_ext, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
   for (void* p : ptrs) cudaFree(p);
   delete m;
   return TSG_OK;
@@ -909,7 +980,7 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
   TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * c->max_iters, s));
   TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
-  if (diag_enabled()) TSG_CUDA(cudaMemsetAsync(m->d_rare, 0, sizeof(unsigned long long) * c->max_iters, s));
+  if (diag_enabled()) TSG_CUDA(cudaMemsetAsync(m->d_rare, 0, sizeof(unsigned long long) * (m->cap + 16), s));
 
   int64_t kernels_per_pass = 0;
   double node_ms = -1.0;
@@ -1002,13 +1073,16 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
     if (diag_enabled()) {
       std::vector<unsigned long long> rare(it);
       std::vector<int32_t> accd(it);
-      TSG_CUDA(cudaMemcpy(rare.data(), m->d_rare, sizeof(unsigned long long) * it, cudaMemcpyDeviceToHost));
+      TSG_CUDA(cudaMemcpy(rare.data(), m->d_rare + 16, sizeof(unsigned long long) * it, cudaMemcpyDeviceToHost));
       TSG_CUDA(cudaMemcpy(accd.data(), m->d_acc, sizeof(int32_t) * it, cudaMemcpyDeviceToHost));
       for (int p = 0; p < it; ++p) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->pass_events[2 * p], ctx->pass_events[2 * p + 1]);
         std::fprintf(stderr, "[tsg diag] pass %d node_ms %.4f accepted %d rare %llu\n", p, ms, accd[p], rare[p]);
       }
+      unsigned long long hist[16];
+      TSG_CUDA(cudaMemcpy(hist, m->d_rare, sizeof hist, cudaMemcpyDeviceToHost));
+      for (int b = 0; b < 16; ++b) std::fprintf(stderr, "[tsg diag] |hyp-thr| 2^%d: %llu\n", b - 60, hist[b]);
     }
   }
   if (c->swap == TSG_SWAP_PINGPONG) m->cur = it & 1;
@@ -1193,14 +1267,14 @@ tsg_status tsg_halo_unpack(tsg_mesh* m, const double* in, int32_t in_is_host) {
   const unsigned g = grid_for(m->n_recv, 256);
   if (m->prec == TSG_F64) {
     if (m->layout == TSG_LAYOUT_SOA)
-      halo_unpack<double, true><<<g, 256, 0, s>>>(coords_of<double, true>(m, 0), coords_of<double, true>(m, 1), m->d_recv_slots, m->n_recv, src);
+      halo_unpack<double, true><<<g, 256, 0, s>>>(coords_of<double, true>(m, 0), coords_of<double, true>(m, 1), m->d_recv_slots, m->n_recv, src, m->d_maxabs);
     else
-      halo_unpack<double, false><<<g, 256, 0, s>>>(coords_of<double, false>(m, 0), coords_of<double, false>(m, 1), m->d_recv_slots, m->n_recv, src);
+      halo_unpack<double, false><<<g, 256, 0, s>>>(coords_of<double, false>(m, 0), coords_of<double, false>(m, 1), m->d_recv_slots, m->n_recv, src, m->d_maxabs);
   } else {
     if (m->layout == TSG_LAYOUT_SOA)
-      halo_unpack<float, true><<<g, 256, 0, s>>>(coords_of<float, true>(m, 0), coords_of<float, true>(m, 1), m->d_recv_slots, m->n_recv, src);
+      halo_unpack<float, true><<<g, 256, 0, s>>>(coords_of<float, true>(m, 0), coords_of<float, true>(m, 1), m->d_recv_slots, m->n_recv, src, m->d_maxabs);
     else
-      halo_unpack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), m->d_recv_slots, m->n_recv, src);
+      halo_unpack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), m->d_recv_slots, m->n_recv, src, m->d_maxabs);
   }
   TSG_CUDA(cudaGetLastError());
   TSG_CUDA(cudaStreamSynchronize(s));

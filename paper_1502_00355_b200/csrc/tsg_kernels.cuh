@@ -44,8 +44,9 @@ struct PassArgs {
   unsigned long long* slot_md;  // [pass][kStatSlots] partial max displacement bits
                                 // (non-negative doubles order as u64)
   int8_t* decision;             // optional: 1 accept / 0 reject per slot
-  unsigned long long* rare;     // optional diagnostics: [pass] rare-path decisions (tile_update)
-  int32_t* queue;               // near-tie slots queued for tie_update (capacity nv)
+  unsigned long long* rare;     // optional diagnostics: [16] |hyp-thr| histogram, [16 + pass] near-ties
+  const unsigned long long* maxabs;  // bits of max |coordinate| (set_coords / halo_unpack); at or
+                                     // above kExactOnlyAbove every decision is taken exactly
 };
 
 template <typename R, bool kSoA>
@@ -58,6 +59,10 @@ __device__ __forceinline__ void select_buffers(const PassArgs<R, kSoA>& a, int p
     P = a.buf0;
     N = a.buf1;
   }
+}
+
+__device__ __forceinline__ bool exact_only(const unsigned long long* maxabs) {
+  return *maxabs >= static_cast<unsigned long long>(__double_as_longlong(kExactOnlyAbove));
 }
 
 // Per-pass statistics are accumulated into kStatSlots spread slots (one pair per warp, slot
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(kBlock, kBlock == 128 ? 8 : 4) node_update(Pas
         hyp = fmin(hyp, q);
       }
     }
-    const bool bad = !(fabs(nan_acc) < R(1e30));
+    const bool bad = exact_only(a.maxabs) || !(fabs(nan_acc) < R(1e30));
     bool acc;
     if (tie) {
       acc = false;
@@ -328,11 +333,23 @@ __device__ __forceinline__ R inv_deg(int deg) {
 
 // Per-neighbour quantities of the cycle sweep: q - v at the pass-start position and at the
 // candidate, and their squared lengths.  (The outer edge b - a of a triangle is formed from
-// the pass-start offsets; its rounding error is bounded like the others', see ring_update.)
+// the pass-start offsets; its rounding error is covered by kGuardCycle, tsg_device.cuh.)
 template <typename R>
 struct RingEdge {
   R px, py, cx, cy, lp, lc;
 };
+
+// Fast α/K of the triangle (v, a, b) at the pass-start position (first) and at the candidate
+// (second) from the two neighbours' ring edges.
+template <typename R>
+__device__ __forceinline__ void ring_pair(const RingEdge<R>& x, const RingEdge<R>& y, R& tp, R& tc) {
+  const R ex = y.px - x.px, ey = y.py - x.py;
+  const R lab = fma(ex, ex, ey * ey);
+  const R cp = fma(x.px, y.py, -(x.py * y.px));
+  const R cc = fma(x.cx, y.cy, -(x.cy * y.cx));
+  tp = cp * rcp_refined<2>(x.lp + y.lp + lab);
+  tc = cc * rcp_refined<2>(x.lc + y.lc + lab);
+}
 
 template <typename R>
 __device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typename Arith<R>::R2 pv,
@@ -345,172 +362,6 @@ __device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typena
   e.lp = fma(e.px, e.px, e.py * e.py);
   e.lc = fma(e.cx, e.cx, e.cy * e.cy);
   return e;
-}
-
-// Thread-per-vertex Form A fused update over the one-ring CYCLE (small tier).
-//
-// Every incident triangle of an interior manifold vertex is a rotation of (v, a, b) for
-// consecutive entries a -> b of its directed link cycle, so one sweep around the cycle visits
-// each triangle once while computing each neighbour's offsets from v (pass-start and
-// candidate) and their squared lengths once: α/K = ((a-v) x (b-v)) / (|a-v|^2 + |b-v|^2 +
-// |b-a|^2) for both positions of v, sharing |b-a|^2.  (The reference's triangle_alpha,
-// quality.hpp:15-23, is rotation invariant in exact arithmetic.)  This is the decision FILTER;
-// its error against the exact real value is < 6u (u = 2^-53) on α/K, the reference's own
-// evaluation differs from the real value by < 14u on α, so whenever the fast thr and hyp are
-// more than kGuard (>> 2 * 10u) apart the strict test hyp > thr has the reference's outcome.
-// Near-ties (and degenerate triangles) are settled with the reference's literal evaluation
-// over the fan records, exactly as node_update does.
-//
-// Neighbour coordinates are gathered in ascending ORIGINAL id (the summation order of
-// neighbor_mean, smoothing.hpp:72-80) into a per-thread shared-memory slice, then read back in
-// cycle order.  Vertices whose link is not a single directed cycle (cyc == kNoCycle) use the
-// fan records for the fast sweep as well.
-//
-// kSelf is v's position in the fan16 records of the rows this instance serves (the tier's
-// maximum valence, tsg_prep.cpp).
-template <typename R, bool kSoA, int kMaxDeg, int kSelf, int kBlock>
-__global__ void __launch_bounds__(kBlock, 1024 / kBlock) ring_update(PassArgs<R, kSoA> a, const uint64_t* __restrict__ cycw) {
-  using O = Arith<R>;
-  using R2 = typename O::R2;
-  constexpr bool kExact = sizeof(R) == 8;
-  static_assert(kMaxDeg <= 15, "cycle words hold deg + 1 <= 16 nibbles");
-  __shared__ R2 ring[kMaxDeg * kBlock];
-  const int tid = threadIdx.x;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * kBlock + tid;
-
-  int64_t s = 0;
-  uint32_t o0 = 0;
-  int deg = 0;
-  uint64_t cyc = ~0ull;
-  if (i < a.count) {
-    s = a.list ? static_cast<int64_t>(a.list[i]) : i;
-    o0 = __ldg(a.off + s);
-    deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
-    if (deg > kMaxDeg) deg = 0;  // medium / hub tiers
-    if (deg > 0) cyc = __ldg(cycw + s);
-  }
-  const int2 state = *reinterpret_cast<const int2*>(a.st);  // {pass, done}
-  if (state.y) return;  // stop rule fired (stream driver); uniform across the grid
-  Coords<R, kSoA> P, N;
-  select_buffers(a, state.x, P, N);
-  const int pass = state.x;
-  const uint32_t* nb = a.nbr + o0;
-
-  int accepted = 0;
-  double disp = 0.0;
-  if (deg > 0) {
-    const R2 pv = P.load(s);
-    R sx = R(0), sy = R(0);
-#pragma unroll
-    for (int base = 0; base < kMaxDeg; base += 8) {
-      if (base < deg) {
-        uint32_t u[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) u[j] = (base + j < deg) ? __ldg(nb + base + j) : 0u;
-        R2 c[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (base + j < deg) c[j] = P.load(u[j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (base + j < deg) {
-            ring[(base + j) * kBlock + tid] = c[j];
-            sx = O::add(sx, c[j].x);
-            sy = O::add(sy, c[j].y);
-          }
-        }
-      }
-    }
-    auto at = [&](uint32_t idx) -> R2 { return ring[idx * kBlock + tid]; };
-    const uint16_t* fan = a.fan16 + o0;
-    const R inv = inv_deg<R>(deg);
-    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-    // Exact tie (candidate == position; Form A reads only pass-start values): every
-    // hypothetical α equals its threshold α bit for bit, the strict test fails.
-    const bool tie = cand.x == pv.x && cand.y == pv.y;
-    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
-    if (!tie) {
-      if (cyc != ~0ull) {
-        RingEdge<R> ea = ring_edge<R>(at(static_cast<uint32_t>(cyc & 15u)), pv, cand);
-#pragma unroll 2
-        for (int j = 1; j <= deg; ++j) {
-          const RingEdge<R> eb = ring_edge<R>(at(static_cast<uint32_t>((cyc >> (4 * j)) & 15u)), pv, cand);
-          const R ex = eb.px - ea.px, ey = eb.py - ea.py;
-          const R lab = fma(ex, ex, ey * ey);
-          const R cp = fma(ea.px, eb.py, -(ea.py * eb.px));
-          const R cc = fma(ea.cx, eb.cy, -(ea.cy * eb.cx));
-          R tp = cp * rcp_refined<2>(ea.lp + eb.lp + lab);
-          R tc = cc * rcp_refined<2>(ea.lc + eb.lc + lab);
-          if constexpr (!kExact) {
-            tp = isfinite(tp) ? tp : R(0);
-            tc = isfinite(tc) ? tc : R(0);
-          }
-          nan_acc = nan_acc + (tp + tc);
-          thr = fmin(thr, tp);
-          hyp = fmin(hyp, tc);
-          ea = eb;
-        }
-      } else {
-        // No single link cycle: literal triangles from the fan records (α/K scale as above).
-        constexpr R kInvK = R(1) / Arith<R>::kAlpha;
-        for (int j = 0; j < deg; ++j) {
-          const uint32_t f = __ldg(fan + j);
-          const uint32_t i0 = fan_p(f, 0), i1 = fan_p(f, 1), i2 = fan_p(f, 2);
-          const R2 q1 = i0 == kSelf ? pv : at(i0), q2 = i1 == kSelf ? pv : at(i1), q3 = i2 == kSelf ? pv : at(i2);
-          const R2 c1 = i0 == kSelf ? cand : q1, c2 = i1 == kSelf ? cand : q2, c3 = i2 == kSelf ? cand : q3;
-          R t = alpha_fast<R>(q1.x, q1.y, q2.x, q2.y, q3.x, q3.y) * kInvK;
-          R h = alpha_fast<R>(c1.x, c1.y, c2.x, c2.y, c3.x, c3.y) * kInvK;
-          if constexpr (!kExact) {
-            t = isfinite(t) ? t : R(0);
-            h = isfinite(h) ? h : R(0);
-          }
-          nan_acc = nan_acc + (t + h);
-          thr = fmin(thr, t);
-          hyp = fmin(hyp, h);
-        }
-      }
-    }
-    const bool bad = !(fabs(nan_acc) < R(1e30));
-    bool acc;
-    if (tie) {
-      acc = false;
-    } else if constexpr (!kExact) {
-      acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
-    } else if (!bad && hyp > thr + R(kGuard)) {
-      acc = true;
-    } else if (!bad && hyp < thr - R(kGuard)) {
-      acc = false;
-    } else {
-      // Near-tie: the reference's literal evaluation (IEEE division, same operand order) of
-      // the triangles whose fast value lies within kGuard of the fast minimum (all of them when
-      // some fast value is not finite).
-      constexpr R kInvK = R(1) / Arith<R>::kAlpha;
-      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
-      for (int j = 0; j < deg; ++j) {
-        const uint32_t f = __ldg(fan + j);
-        R2 q[3], c[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const uint32_t idx = fan_p(f, k);
-          q[k] = idx == kSelf ? pv : at(idx);
-          c[k] = idx == kSelf ? cand : q[k];
-        }
-        if (bad || alpha_fast<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y) * kInvK <= thr + R(kGuard))
-          thr_e = min_ref(thr_e, alpha_plain<R>(q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y));
-        if (bad || alpha_fast<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y) * kInvK <= hyp + R(kGuard))
-          hyp_e = min_ref(hyp_e, alpha_plain<R>(c[0].x, c[0].y, c[1].x, c[1].y, c[2].x, c[2].y));
-      }
-      acc = hyp_e > thr_e;
-    }
-    N.store(s, acc ? cand : pv);
-    if (acc) {
-      accepted = 1;
-      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
-      disp = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-    }
-    if (a.decision) a.decision[s] = acc ? 1 : 0;
-  }
-  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
 }
 
 // Tile arrays (tsg_prep.hpp build_tiles).
@@ -616,7 +467,7 @@ __device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& 
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const uint32_t p = fan_p(f, k);
-      q[k] = p == kSelf ? pv : tv.get(tv.word(w0 + p * stride) & 0xffffu);
+      q[k] = p == kSelf ? pv : tv.get(tv.word(w0 + p * stride) & kLocalMask);
       c[k] = p == kSelf ? cand : q[k];
     }
   };
@@ -636,7 +487,7 @@ __device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& 
       thr = min_ref(thr, tq);
       hyp = min_ref(hyp, th);
     }
-    bad = !(fabs(nan_acc) < R(1e30));
+    bad = bad || !(fabs(nan_acc) < R(1e30));
     if constexpr (!kExact) return hyp > thr;
     if (!bad && hyp > thr + R(kGuard)) return true;
     if (!bad && hyp < thr - R(kGuard)) return false;
@@ -663,8 +514,17 @@ __device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& 
 // ORIGINAL id (the summation order of neighbor_mean, smoothing.hpp:72-80), cycle[] the directed
 // link cycle (every incident triangle is a rotation of (v, cycle[j], cycle[j+1])).  Rows of one
 // valence are stored entry-major, so the lanes of a (degree-uniform) warp read word j of
-// consecutive rows without bank conflicts.  The decision arithmetic is ring_update's: fast α/K
-// filter over the cycle; rows without a link cycle and near-ties go to tile_decide_rare.
+// consecutive rows without bank conflicts.
+//
+// Decisions: every incident triangle of an interior manifold vertex is a rotation of (v, a, b)
+// for consecutive entries a -> b of its link cycle, so one sweep around the cycle visits each
+// triangle once and computes each neighbour's offsets from v (pass-start and candidate) and
+// their squared lengths once: α/K = ((a-v) x (b-v)) / (|a-v|^2 + |b-v|^2 + |b-a|^2) for both
+// positions of v (the reference's triangle_alpha, quality.hpp:15-23, is rotation invariant in
+// exact arithmetic).  This fast filter settles hyp > thr whenever the two minima are more than
+// kGuardCycle apart (error analysis in tsg_device.cuh); near-ties are collected per tile and
+// decided afterwards with the reference's literal arithmetic, one warp per vertex; rows without
+// a single link cycle take tile_decide_rare (fan records).
 // kStaged: every tile's external coordinates and words fit the shared-memory caps.
 template <typename R, bool kSoA, int kThreads, int kMaxDeg, bool kStaged>
 __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
@@ -674,6 +534,8 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   static_assert(kTile % kThreads == 0, "whole vertices per thread");
   extern __shared__ __align__(16) unsigned char tile_smem[];
   __shared__ uint64_t bar;
+  __shared__ int16_t q_s[kTile];  // this tile's near-tie vertices (tile-local index)
+  __shared__ int qn_s;
   R2* pts = reinterpret_cast<R2*>(tile_smem);
   uint32_t* words = reinterpret_cast<uint32_t*>(pts + kTile + t.ext_cap);
   uint32_t* meta_s = words + t.rec_cap;
@@ -695,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   // (SoA, the partial last tile) goes through the load/store units.
   const bool bulk = !kSoA && n_in == kTile;
   if (tid == 0) {
+    qn_s = 0;
     mbar_init(&bar, 1);
     if (bulk) {
       const uint32_t bytes = kTile * sizeof(R2) + kTile * 4u + 4u * n_rec;
@@ -736,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     R sx = R(0), sy = R(0);
 #pragma unroll 2
     for (int j = 0; j < deg; ++j) {
-      const R2 c = tv.get(tv.word(w0 + j * stride) & 0xffffu);
+      const R2 c = tv.get(tv.word(w0 + j * stride) & kLocalMask);
       sx = O::add(sx, c.x);
       sy = O::add(sy, c.y);
     }
@@ -747,18 +610,14 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     // Exact tie (candidate == position; Form A reads only pass-start values): every
     // hypothetical α equals its threshold α bit for bit, the strict test fails.
     if (!(cand.x == pv.x && cand.y == pv.y)) {
-      const uint32_t l0 = tv.word(w0) >> 16;
+      const uint32_t l0 = (tv.word(w0) >> kWordCycleShift) & kLocalMask;
       R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
       const bool cyc = l0 != kNoLocal;
       if (cyc) {
         RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
         auto tri = [&](const RingEdge<R>& x, const RingEdge<R>& y) {
-          const R ex = y.px - x.px, ey = y.py - x.py;
-          const R lab = fma(ex, ex, ey * ey);
-          const R cp = fma(x.px, y.py, -(x.py * y.px));
-          const R cc = fma(x.cx, y.cy, -(x.cy * y.cx));
-          R tp = cp * rcp_refined<2>(x.lp + y.lp + lab);
-          R tc = cc * rcp_refined<2>(x.lc + y.lc + lab);
+          R tp, tc;
+          ring_pair<R>(x, y, tp, tc);
           if constexpr (!kExact) {
             tp = isfinite(tp) ? tp : R(0);
             tc = isfinite(tc) ? tc : R(0);
@@ -769,29 +628,30 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
         };
 #pragma unroll 2
         for (int j = 1; j < deg; ++j) {
-          const RingEdge<R> eb = ring_edge<R>(tv.get(tv.word(w0 + j * stride) >> 16), pv, cand);
+          const RingEdge<R> eb =
+              ring_edge<R>(tv.get((tv.word(w0 + j * stride) >> kWordCycleShift) & kLocalMask), pv, cand);
           tri(ea, eb);
           ea = eb;
         }
         tri(ea, ring_edge<R>(tv.get(l0), pv, cand));  // closing triangle (recomputed: registers)
       }
-      const bool bad = !(fabs(nan_acc) < R(1e30));
+      const bool bad = exact_only(a.maxabs) || !(fabs(nan_acc) < R(1e30));
       if (cyc && !kExact) {
         acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
-      } else if (cyc && !bad && hyp > thr + R(kGuard)) {
+      } else if (cyc && !bad && hyp > thr + R(kGuardCycle)) {
         acc = true;
-      } else if (cyc && !bad && hyp < thr - R(kGuard)) {
+      } else if (cyc && !bad && hyp < thr - R(kGuardCycle)) {
         acc = false;
       } else if (cyc) {
-        // Near-tie (or a degenerate triangle): decided exactly by tie_update, which runs over
-        // the queue after this kernel with full warps instead of one divergent lane here.
-        if (a.rare) atomicAdd(a.rare + pass, 1ull);
-        const unsigned mask = __activemask();
-        const int leader = __ffs(mask) - 1, lane = threadIdx.x & 31;
-        int slot0 = 0;
-        if (lane == leader) slot0 = atomicAdd(&a.st->queued, __popc(mask));
-        slot0 = __shfl_sync(mask, slot0, leader);
-        a.queue[slot0 + __popc(mask & ((1u << lane) - 1u))] = static_cast<int32_t>(s);
+        // Near-tie (or a degenerate triangle): decided exactly after the sweep of the whole
+        // tile, by full warps instead of one divergent lane here.
+        q_s[atomicAdd(&qn_s, 1)] = static_cast<int16_t>(i);
+        if (a.rare) {  // diagnostics: histogram of log2 |hyp - thr| (bins 0..15 = 2^-60..2^-45)
+          const double dd = fabs(static_cast<double>(hyp - thr));
+          int b = dd > 0.0 ? ilogb(dd) + 60 : 0;
+          b = b < 0 ? 0 : b > 15 ? 15 : b;
+          atomicAdd(a.rare + b, 1ull);
+        }
         continue;
       } else {
         const uint32_t self = static_cast<uint32_t>(deg <= t.small_max ? t.small_max : t.medium_max);
@@ -808,63 +668,58 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     }
     if (a.decision) a.decision[s] = acc ? 1 : 0;
   }
-  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
-}
-
-// Exact decisions of the near-tie vertices queued by tile_update (Form A fused, fp64): thread
-// per queued slot, the reference's arithmetic throughout — ordered neighbour sum, literal
-// triangle_alpha with IEEE division for every incident triangle at the pass-start position and
-// at the candidate (quality.hpp:15-23, :54-64), strict test (smoothing.hpp:99).
-template <typename R, bool kSoA>
-__global__ void __launch_bounds__(128) tie_update(PassArgs<R, kSoA> a) {
-  using O = Arith<R>;
-  using R2 = typename O::R2;
-  const int2 state = *reinterpret_cast<const int2*>(a.st);
-  if (state.y) return;
-  Coords<R, kSoA> P, N;
-  select_buffers(a, state.x, P, N);
-  const int pass = state.x;
-  const int64_t count = a.st->queued;
-  int accepted = 0;
-  double disp = 0.0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  // Warp-uniform trip count (commit_stats_warp needs the whole warp).
-  const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
-  for (int64_t w = first; w < count; w += stride) {
-    const int64_t k = w + (threadIdx.x & 31);
-    if (k >= count) continue;
-    const int64_t s = a.queue[k];
-    const uint32_t o0 = __ldg(a.off + s);
-    const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
-    const uint32_t* nb = a.nbr + o0;
-    const uint32_t* fan = a.fan + o0;
-    const R2 pv = P.load(s);
+  // Exact decisions of the tile's near-ties, from the staged tile, one warp per vertex (lane j
+  // evaluates triangle j): the reference's arithmetic throughout — ordered neighbour sum,
+  // literal triangle_alpha with IEEE division for every incident triangle at the pass-start
+  // position and at the candidate (quality.hpp:15-23, :54-64, through alpha_at with the
+  // triangle's rotation k from the row words), strict test.  The minimum of finite values is
+  // order-free, so the shuffle reduction equals the reference's sequential std::min.
+  __syncthreads();
+  const int qn = qn_s;
+  if (qn > 0 && tid == 0 && a.rare) atomicAdd(a.rare + 16 + pass, static_cast<unsigned long long>(qn));
+  const int lane = tid & 31;
+#pragma unroll 1
+  for (int e = tid >> 5; e < qn; e += kThreads / 32) {
+    const int i = q_s[e];
+    const uint32_t meta = meta_s[i];
+    const int deg = static_cast<int>((meta >> kMetaDegShift) & 15u);
+    const uint32_t w0 = meta & kMetaBaseMask, stride = meta >> kMetaStrideShift;
+    const R2 pv = pts[i];
     R sx = R(0), sy = R(0);
     for (int j = 0; j < deg; ++j) {
-      const R2 c = P.load(__ldg(nb + j));
+      const R2 c = tv.get(tv.word(w0 + j * stride) & kLocalMask);
       sx = O::add(sx, c.x);
       sy = O::add(sy, c.y);
     }
-    const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
+    const R inv = inv_deg<R>(deg);
     const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
     R thr = R(INFINITY), hyp = R(INFINITY);
-    for (int j = 0; j < deg; ++j) {
-      const uint32_t f = __ldg(fan + j);
-      const R2 qa = P.load(__ldg(nb + fan_i1(f))), qb = P.load(__ldg(nb + fan_i2(f)));
-      const int kk = fan_k(f);
+    if (lane < deg) {
+      const uint32_t wa = tv.word(w0 + lane * stride);
+      const uint32_t wb = tv.word(w0 + (lane + 1 < deg ? lane + 1 : 0) * stride);
+      const R2 qa = tv.get((wa >> kWordCycleShift) & kLocalMask), qb = tv.get((wb >> kWordCycleShift) & kLocalMask);
+      const int k = static_cast<int>(wa >> kWordRotShift);
       const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
       const R sabx = O::mul(dabx, dabx), saby = O::mul(daby, daby);
-      thr = min_ref(thr, alpha_at<R>(kk, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby));
-      hyp = min_ref(hyp, alpha_at<R>(kk, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby));
+      thr = alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby);
+      hyp = alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby);
     }
-    const bool acc = hyp > thr;
-    N.store(s, acc ? cand : pv);
-    if (a.decision) a.decision[s] = acc ? 1 : 0;
-    if (acc) {
-      ++accepted;
-      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
-      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-      disp = d > disp ? d : disp;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      thr = min_ref(thr, __shfl_xor_sync(0xffffffffu, thr, o));
+      hyp = min_ref(hyp, __shfl_xor_sync(0xffffffffu, hyp, o));
+    }
+    if (lane == 0) {
+      const bool acc = hyp > thr;
+      const int64_t s = base + i;
+      N.store(s, acc ? cand : pv);
+      if (acc) {
+        ++accepted;
+        const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+        const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+        disp = d > disp ? d : disp;
+      }
+      if (a.decision) a.decision[s] = acc ? 1 : 0;
     }
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
@@ -956,12 +811,12 @@ __global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) 
       thr = fmin(thr, __shfl_xor_sync(0xffffffffu, thr, o));
       hyp = fmin(hyp, __shfl_xor_sync(0xffffffffu, hyp, o));
     }
-    const bool bad = __any_sync(0xffffffffu, !(fabs(nan_acc) < R(1e30)));
+    const bool bad = exact_only(a.maxabs) || __any_sync(0xffffffffu, !(fabs(nan_acc) < R(1e30)));
     if constexpr (!kExact) {
       acc = hyp > thr;
-    } else if (!bad && hyp > thr + R(kGuard)) {
+    } else if (!bad && hyp > thr + R(kGuardCycle)) {
       acc = true;
-    } else if (!bad && hyp < thr - R(kGuard)) {
+    } else if (!bad && hyp < thr - R(kGuardCycle)) {
       acc = false;
     } else {
       // Near-tie: exact α of every triangle (alpha_at = triangle_alpha in the literal
@@ -1198,7 +1053,6 @@ __global__ void finalize_pass(PassState* st, const int32_t* slot_acc, const unsi
     mdb = other > mdb ? other : mdb;
   }
   if (lane != 0) return;
-  st->queued = 0;  // tile_update's near-tie queue has been drained by tie_update
   if (!done) {
     pass_acc[q] = acc;
     pass_md[q] = mdb;

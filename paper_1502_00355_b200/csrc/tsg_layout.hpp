@@ -11,7 +11,11 @@ constexpr int kMaxCycleDeg = 15;             // deg + 1 nibbles in 64 bits
 // order).  A tile's small rows address their neighbours by LOCAL index: slot - tile base for
 // in-tile slots, kTile + position in the tile's sorted external-slot list otherwise.
 constexpr int kTile = 1024;
-constexpr uint16_t kNoLocal = 0xffffu;  // cycle entry of a row without a single link cycle
+constexpr uint32_t kNoLocal = 0x3fffu;  // cycle entry of a row without a single link cycle
+// Tile row word: row[j] (bits 0-13) | cycle[j] (bits 16-29) | k[j] (bits 30-31).
+constexpr uint32_t kLocalMask = 0x3fffu;
+constexpr int kWordCycleShift = 16;
+constexpr int kWordRotShift = 30;
 // Tile meta word: first-word offset | valence | group stride (tsg_prep.hpp HostMesh::tmeta).
 constexpr uint32_t kMetaBaseMask = 0xffffu;
 constexpr int kMetaDegShift = 16;     // 4 bits

@@ -87,7 +87,7 @@ uint32_t hilbert_d(uint32_t x, uint32_t y) {
 // Tile records (see tsg_prep.hpp).  Per tile: the sorted external slots referenced by its
 // small rows; the small rows grouped by valence (slot order inside a group), each group's
 // words stored entry-major: word j of the k-th row of a group of n rows at group base + j*n + k.
-void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg) {
+std::string build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg) {
   const int64_t nv = hm.nv;
   const int64_t ntiles = (nv + kTile - 1) / kTile;
   hm.tmeta.assign(nv, 0);
@@ -136,6 +136,9 @@ void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg
   }
   hm.tile_rec[ntiles] = static_cast<uint32_t>(wu);
   hm.ext_off[ntiles] = static_cast<uint32_t>(eu);
+  if (kTile + max_ext >= static_cast<int64_t>(kNoLocal))
+    return "a tile references more than " + std::to_string(kNoLocal - kTile - 1) + " external vertices";
+  if (wu >= 0xffffffffULL) return "tile records exceed 2^32 words";
   hm.max_ext = max_ext;
   hm.max_rec_words = max_words;
   hm.ext.resize(eu);
@@ -160,11 +163,13 @@ void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg
         for (uint32_t j = 0; j < n; ++j) {
           const uint32_t row = local(hm.nbr[o0 + j]);
           const uint32_t cy = cyc == kNoCycle ? kNoLocal : local(hm.nbr[o0 + ((cyc >> (4 * j)) & 15u)]);
-          r[j * stride] = row | (cy << 16);
+          const uint32_t k = cyc == kNoCycle ? 0u : (hm.cyck[s] >> (2 * j)) & 3u;
+          r[j * stride] = row | (cy << kWordCycleShift) | (k << kWordRotShift);
         }
       }
     }
   });
+  return "";
 }
 
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
@@ -262,6 +267,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   hm.fan.assign(total, 0);
   hm.fan16.assign(total, 0);
   hm.cyc.assign(nv, kNoCycle);
+  hm.cyck.assign(nv, 0);
 
   // Device triangle order: identity, or by the smallest slot among the corners (stable) so
   // that the triangle kernels stream coordinates in the same locality order as the vertices.
@@ -304,7 +310,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
       uint32_t* out_f = hm.fan.data() + hm.off[s];
       for (int32_t j = 0; j < n; ++j) out_n[j] = static_cast<uint32_t>(hm.rank[row[j]]);
       const bool want_cycle = n <= kMaxCycleDeg;
-      int8_t succ[kMaxCycleDeg], indeg[kMaxCycleDeg];
+      int8_t succ[kMaxCycleDeg], indeg[kMaxCycleDeg], rot[kMaxCycleDeg];
       bool cycle_ok = want_cycle;
       if (want_cycle)
         for (int32_t j = 0; j < n; ++j) succ[j] = -1, indeg[j] = 0;
@@ -325,6 +331,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
           } else {
             succ[ia] = static_cast<int8_t>(ic);
             indeg[ic] = 1;
+            rot[ia] = static_cast<int8_t>(k);
           }
         }
         const int tier = tiers.tier(static_cast<uint32_t>(n));
@@ -341,13 +348,18 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
       if (cycle_ok) {
         // Single directed cycle through all n positions, starting at position 0.
         uint64_t w = 0;
+        uint32_t kw = 0;
         int32_t p = 0, steps = 0;
         do {
           w |= static_cast<uint64_t>(p) << (4 * steps);
+          kw |= static_cast<uint32_t>(rot[p]) << (2 * steps);
           p = succ[p];
           ++steps;
         } while (p > 0 && steps < n);
-        if (p == 0 && steps == n) hm.cyc[s] = w;  // nibble n (= n_0 = 0) is already 0
+        if (p == 0 && steps == n) {  // nibble n (= n_0 = 0) is already 0
+          hm.cyc[s] = w;
+          hm.cyck[s] = kw;
+        }
       }
     }
   });
@@ -377,21 +389,18 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
 
   hm.hubs.clear();
   hm.medium.clear();
-  hm.cyc_mid.clear();
   hm.large.clear();
   for (int64_t s = 0; s < nv; ++s) {
     if (deg[s] == 0) continue;
     const int tier = tiers.tier(deg[s]);
     if (tier == 1) hm.medium.push_back(static_cast<int32_t>(s));
     if (tier == 2) hm.hubs.push_back(static_cast<int32_t>(s));
-    if (tier > 0) {
-      if (deg[s] <= static_cast<uint32_t>(kMaxCycleDeg))
-        hm.cyc_mid.push_back(static_cast<int32_t>(s));
-      else
-        hm.large.push_back(static_cast<int32_t>(s));
-    }
+    if (deg[s] > static_cast<uint32_t>(kMaxCycleDeg)) hm.large.push_back(static_cast<int32_t>(s));
   }
-  build_tiles(hm, deg, kMaxCycleDeg);
+  {
+    const std::string terr = build_tiles(hm, deg, kMaxCycleDeg);
+    if (!terr.empty()) return terr;
+  }
   // Longest rows first: the warp tier's tail is its largest hubs.
   std::stable_sort(hm.large.begin(), hm.large.end(), [&](int32_t x, int32_t y) { return deg[x] > deg[y]; });
   return "";

@@ -46,21 +46,21 @@ struct HostMesh {
   // when the link of v is not a single directed cycle (bow-tie / inconsistent orientation) or
   // the row is not in the small tier; those vertices use the fan records.
   std::vector<uint64_t> cyc;
+  std::vector<uint32_t> cyck;     // 2 bits per cycle step j: v's position k in triangle j
   std::vector<uint32_t> vinc_off; // nv+1, all vertices
   std::vector<uint32_t> vinc;     // device triangle ids
   std::vector<int32_t> tri;       // 3*nt device slots, device triangle order
   std::vector<int32_t> medium;    // slots of the medium tier
   std::vector<int32_t> hubs;      // slots of the hub tier
-  // Form A fused lists: rows above the small tier with deg <= kMaxCycleDeg (cycle sweep,
-  // thread per vertex) and the rest (warp per vertex).
-  std::vector<int32_t> cyc_mid;
+  // Form A fused: rows with deg > kMaxCycleDeg (warp per vertex; longest first).
   std::vector<int32_t> large;
   // Tiles (rows with 1 <= deg <= kMaxCycleDeg; other rows have tmeta == 0):
   //   tmeta[s]     word offset of row s's first word inside its tile's words (bits 0-15) |
   //                deg << kMetaDegShift | stride << kMetaStrideShift (word j at offset + j*stride)
   //   tile_rec[t]  first word of tile t (ntiles + 1; multiples of 4)
-  //   trec         u32 words: row[j] local index | cycle[j] local index << 16, cycle[j] =
-  //                kNoLocal when the row has no single link cycle
+  //   trec         u32 words: row[j] local index | cycle[j] local index << 16 | k[j] << 30
+  //                (v's position in the literal triangle (v, cycle[j], cycle[j+1]) rotated;
+  //                local indices < 2^14); cycle[j] = kNoLocal when the row has no link cycle
   //   ext_off/ext  per tile: sorted external slots (ntiles + 1 offsets)
   std::vector<uint32_t> tmeta, tile_rec, ext_off, ext, trec;
   int32_t max_ext = 0, max_rec_words = 0;
@@ -86,6 +86,6 @@ struct FormBSchedule {
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
 std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
-void build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg);
+std::string build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg);
 
 }  // namespace tsg
