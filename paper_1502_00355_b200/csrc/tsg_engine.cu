@@ -293,6 +293,7 @@ struct tsg_mesh {
   int32_t cap = 0;
   int cur = 0;
   int32_t hub_max_deg = 0;
+  int64_t n_hub_fast = 0;  // leading entries of hm.large with deg > kWarpTierCap
   // Form B schedule cache
   int32_t fb_chunks = 0;
   uint32_t* d_nbr_fresh = nullptr;
@@ -466,12 +467,22 @@ struct Engine {
       TSG_CUDA(cudaStreamWaitEvent(ctx->side, e, 0));
       t = ctx->side;
     }
-    if (nlarge > 0) {
+    const int64_t nhub = m->n_hub_fast, nwarp = nlarge - nhub;
+    if (nhub > 0) {  // the longest rows (a prefix of the degree-descending list): CTA per hub
       Args a = base;
       a.list = m->d_large;
-      a.count = nlarge;
+      a.count = nhub;
+      const int32_t cap = hub_fast_cap(m);
+      tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(nhub), tsg::kHubBlock, cap * sizeof(R2), t>>>(a, cap);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    if (nwarp > 0) {
+      Args a = base;
+      a.list = m->d_large + nhub;
+      a.count = nwarp;
       tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>
-          <<<static_cast<unsigned>((nlarge + kWarpTierWarps - 1) / kWarpTierWarps), kWarpTierWarps * 32, 0, t>>>(a);
+          <<<static_cast<unsigned>((nwarp + kWarpTierWarps - 1) / kWarpTierWarps), kWarpTierWarps * 32, 0, t>>>(a);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
@@ -546,6 +557,10 @@ struct Engine {
     return TSG_OK;
   }
 
+  static int32_t hub_fast_cap(const tsg_mesh* m) {
+    return std::max(1, std::min(m->hm.max_deg, kHubCap));
+  }
+
   static bool tiles_staged(const tsg_mesh* m) {
     return m->hm.max_ext <= kTileExtCap && m->hm.max_rec_words <= kTileRecCap;
   }
@@ -567,6 +582,8 @@ struct Engine {
 
   // Opt-in shared memory for the hub kernels (done outside any stream capture).
   static tsg_status prepare(tsg_mesh* m) {
+    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_fast_update<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(hub_fast_cap(m) * sizeof(R2))));
     {
       const tsg::TileArgs ta = tile_args(m);
       const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap));
@@ -831,6 +848,9 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = dalloc(&m->d_maxabs, 1, b))) return st;
   if ((st = dalloc(&m->d_ext, 3, b))) return st;
   for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
+  while (m->n_hub_fast < static_cast<int64_t>(hm.large.size()) &&
+         hm.off[hm.large[m->n_hub_fast] + 1] - hm.off[hm.large[m->n_hub_fast]] > static_cast<uint32_t>(kWarpTierCap))
+    ++m->n_hub_fast;
   if ((st = ensure_stats_capacity(m.get(), 128))) return st;
   st = dispatch(m.get(), [&](auto E) { return decltype(E)::set_coords(m.get(), d->xy); });
   if (st) return st;

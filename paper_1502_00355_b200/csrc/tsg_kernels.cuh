@@ -855,6 +855,166 @@ __global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) 
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
 }
 
+// Fast α/K of the triangle (v, a, b) for one position of v: the rotation formula of the cycle
+// sweep (ring_edge / ring_pair, same operation sequence, same error bound).
+template <typename R>
+__device__ __forceinline__ R rot_fast(typename Arith<R>::R2 qa, typename Arith<R>::R2 qb, typename Arith<R>::R2 v) {
+  const R ax = qa.x - v.x, ay = qa.y - v.y, bx = qb.x - v.x, by = qb.y - v.y;
+  const R ex = bx - ax, ey = by - ay;
+  const R lab = fma(ex, ex, ey * ey);
+  const R la = fma(ax, ax, ay * ay), lb = fma(bx, bx, by * by);
+  return fma(ax, by, -(ay * bx)) * rcp_refined<2>(la + lb + lab);
+}
+
+// CTA per hub (Form A fused, valence above the warp tier's staging cap): the paper's CDP child
+// launch becomes one CTA.  The row is staged in dynamic shared memory (up to
+// `cap` entries, the rest re-read from global memory); warp 0 forms the ordered neighbour sum
+// (smoothing.hpp:72-80) while warps 1.. sweep the fan at the pass-start position; then every
+// warp sweeps the fan at the candidate; block min-reductions give the decision, near-ties are
+// re-evaluated exactly (alpha_at) by the whole CTA.
+template <typename R, bool kSoA>
+__global__ void __launch_bounds__(kHubBlock) hub_fast_update(PassArgs<R, kSoA> a, int cap) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  constexpr bool kExact = sizeof(R) == 8;
+  constexpr int kWarps = kHubBlock / 32;
+  extern __shared__ __align__(16) unsigned char hub_smem[];
+  R2* ring = reinterpret_cast<R2*>(hub_smem);
+  __shared__ R2 s_cand;
+  __shared__ R s_min[2][kWarps];
+  __shared__ int s_bad;
+
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t s = a.list[blockIdx.x];
+  const uint32_t o0 = __ldg(a.off + s);
+  const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
+  const uint32_t* nb = a.nbr + o0;
+  const uint32_t* fan = a.fan + o0;
+  const int staged = deg < cap ? deg : cap;
+  if (tid == 0) s_bad = 0;
+#pragma unroll 4
+  for (int j = tid; j < staged; j += kHubBlock) ring[j] = P.load(__ldg(nb + j));
+  __syncthreads();
+  auto get = [&](int j) -> R2 { return j < cap ? ring[j] : P.load(__ldg(nb + j)); };
+  const R2 pv = P.load(s);
+
+  R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+  if (warp == 0) {
+    if (lane == 0) {
+      R sx = R(0), sy = R(0);
+#pragma unroll 8
+      for (int j = 0; j < staged; ++j) {
+        const R2 c = ring[j];
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
+      for (int j = staged; j < deg; ++j) {
+        const R2 c = P.load(__ldg(nb + j));
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
+      const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
+      s_cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    }
+  } else {
+    for (int j = tid - 32; j < deg; j += kHubBlock - 32) {
+      const uint32_t f = __ldg(fan + j);
+      R tp = rot_fast<R>(get(fan_i1(f)), get(fan_i2(f)), pv);
+      if constexpr (!kExact) tp = isfinite(tp) ? tp : R(0);
+      nan_acc = fma(tp, tp, nan_acc);
+      thr = min_ref(thr, tp);
+    }
+  }
+  __syncthreads();
+  const R2 cand = s_cand;
+  const bool tie = cand.x == pv.x && cand.y == pv.y;
+  if (!tie) {
+    for (int j = tid; j < deg; j += kHubBlock) {
+      const uint32_t f = __ldg(fan + j);
+      R tc = rot_fast<R>(get(fan_i1(f)), get(fan_i2(f)), cand);
+      if constexpr (!kExact) tc = isfinite(tc) ? tc : R(0);
+      nan_acc = fma(tc, tc, nan_acc);
+      hyp = min_ref(hyp, tc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    thr = min_ref(thr, __shfl_xor_sync(0xffffffffu, thr, o));
+    hyp = min_ref(hyp, __shfl_xor_sync(0xffffffffu, hyp, o));
+  }
+  if (__any_sync(0xffffffffu, !(fabs(nan_acc) < R(1e30))) && lane == 0) s_bad = 1;
+  if (lane == 0) {
+    s_min[0][warp] = thr;
+    s_min[1][warp] = hyp;
+  }
+  __syncthreads();
+  thr = s_min[0][0];
+  hyp = s_min[1][0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) {
+    thr = min_ref(thr, s_min[0][w]);
+    hyp = min_ref(hyp, s_min[1][w]);
+  }
+  const bool bad = exact_only(a.maxabs) || s_bad != 0;
+  bool acc;
+  if (tie) {
+    acc = false;
+  } else if constexpr (!kExact) {
+    acc = hyp > thr;
+  } else if (!bad && hyp > thr + R(kGuardCycle)) {
+    acc = true;
+  } else if (!bad && hyp < thr - R(kGuardCycle)) {
+    acc = false;
+  } else {
+    // Near-tie: the reference's literal α of every triangle (alpha_at), CTA-wide minima.
+    __syncthreads();  // s_min is reused
+    R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+    for (int j = tid; j < deg; j += kHubBlock) {
+      const uint32_t f = __ldg(fan + j);
+      const R2 qa = get(fan_i1(f)), qb = get(fan_i2(f));
+      const int k = fan_k(f);
+      const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+      const R sabx = O::mul(dabx, dabx), saby = O::mul(daby, daby);
+      thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby));
+      hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, sabx, saby));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      thr_e = min_ref(thr_e, __shfl_xor_sync(0xffffffffu, thr_e, o));
+      hyp_e = min_ref(hyp_e, __shfl_xor_sync(0xffffffffu, hyp_e, o));
+    }
+    if (lane == 0) {
+      s_min[0][warp] = thr_e;
+      s_min[1][warp] = hyp_e;
+    }
+    __syncthreads();
+    thr_e = s_min[0][0];
+    hyp_e = s_min[1][0];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) {
+      thr_e = min_ref(thr_e, s_min[0][w]);
+      hyp_e = min_ref(hyp_e, s_min[1][w]);
+    }
+    acc = hyp_e > thr_e;
+  }
+  if (tid == 0) {
+    N.store(s, acc ? cand : pv);
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+    if (acc) {
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      const unsigned slot = pass * kStatSlots + (blockIdx.x & (kStatSlots - 1));
+      atomicAdd(a.slot_acc + slot, 1);
+      if (d > 0.0) atomicMax(a.slot_md + slot, static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
+  }
+}
+
 // CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)
 // by `cap` view pairs; entries beyond cap are read from global memory.
 template <typename R, bool kSoA, bool kFormB, bool kTwoPhase>
