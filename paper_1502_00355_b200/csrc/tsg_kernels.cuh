@@ -16,6 +16,8 @@
 //                sets the WHILE-graph condition.
 #pragma once
 
+#include <type_traits>
+
 #include "tsg_device.cuh"
 
 namespace tsg {
@@ -587,21 +589,34 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   if (bulk) mbar_wait(&bar, 0);
 
   const TileView<R, kSoA, kStaged> tv{pts, words, P, t.ext + e0, t.rec + r0, t.ext_cap, t.rec_cap};
+  const bool xonly = exact_only(a.maxabs);
+  int8_t* const decision = a.decision;
   int accepted = 0;
   double disp = 0.0;
-#pragma unroll 1
-  for (int i = tid; i < n_in; i += kThreads) {
-    const uint32_t meta = meta_s[i];
-    const int deg = static_cast<int>((meta >> kMetaDegShift) & 15u);
-    if (deg == 0) continue;  // pinned, or a medium / warp tier row
+
+  // One vertex; D > 0: the valence is the compile-time constant D (fully unrolled sum and cycle
+  // sweep, no loop-carried copies), D == 0: run-time valence.
+  auto vertex = [&](auto d_const, int i, uint32_t meta) {
+    constexpr int D = decltype(d_const)::value;
+    const int deg = D > 0 ? D : static_cast<int>((meta >> kMetaDegShift) & 15u);
     const uint32_t w0 = meta & kMetaBaseMask, stride = meta >> kMetaStrideShift;
+    auto wd = [&](int j) { return tv.word(w0 + j * stride); };
     const R2 pv = pts[i];
     R sx = R(0), sy = R(0);
+    if constexpr (D > 0) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const R2 c = tv.get(wd(j) & kLocalMask);
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
+    } else {
 #pragma unroll 2
-    for (int j = 0; j < deg; ++j) {
-      const R2 c = tv.get(tv.word(w0 + j * stride) & kLocalMask);
-      sx = O::add(sx, c.x);
-      sy = O::add(sy, c.y);
+      for (int j = 0; j < deg; ++j) {
+        const R2 c = tv.get(wd(j) & kLocalMask);
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
     }
     const R inv = inv_deg<R>(deg);
     const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
@@ -610,11 +625,10 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     // Exact tie (candidate == position; Form A reads only pass-start values): every
     // hypothetical α equals its threshold α bit for bit, the strict test fails.
     if (!(cand.x == pv.x && cand.y == pv.y)) {
-      const uint32_t l0 = (tv.word(w0) >> kWordCycleShift) & kLocalMask;
+      const uint32_t l0 = (wd(0) >> kWordCycleShift) & kLocalMask;
       R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
       const bool cyc = l0 != kNoLocal;
       if (cyc) {
-        RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
         auto tri = [&](const RingEdge<R>& x, const RingEdge<R>& y) {
           R tp, tc;
           ring_pair<R>(x, y, tp, tc);
@@ -626,16 +640,29 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
           thr = min_ref(thr, tp);
           hyp = min_ref(hyp, tc);
         };
+        auto edge = [&](int j) { return ring_edge<R>(tv.get((wd(j) >> kWordCycleShift) & kLocalMask), pv, cand); };
+        if constexpr (D > 0) {
+          const RingEdge<R> e0 = ring_edge<R>(tv.get(l0), pv, cand);
+          RingEdge<R> ea = e0;
+#pragma unroll
+          for (int j = 1; j < D; ++j) {
+            const RingEdge<R> eb = edge(j);
+            tri(ea, eb);
+            ea = eb;
+          }
+          tri(ea, e0);
+        } else {
+          RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
 #pragma unroll 2
-        for (int j = 1; j < deg; ++j) {
-          const RingEdge<R> eb =
-              ring_edge<R>(tv.get((tv.word(w0 + j * stride) >> kWordCycleShift) & kLocalMask), pv, cand);
-          tri(ea, eb);
-          ea = eb;
+          for (int j = 1; j < deg; ++j) {
+            const RingEdge<R> eb = edge(j);
+            tri(ea, eb);
+            ea = eb;
+          }
+          tri(ea, ring_edge<R>(tv.get(l0), pv, cand));  // closing triangle (recomputed: registers)
         }
-        tri(ea, ring_edge<R>(tv.get(l0), pv, cand));  // closing triangle (recomputed: registers)
       }
-      const bool bad = exact_only(a.maxabs) || !(fabs(nan_acc) < R(1e30));
+      const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
       if (cyc && !kExact) {
         acc = hyp > thr;  // fp32: decisions are compared in lockstep with a margin
       } else if (cyc && !bad && hyp > thr + R(kGuardCycle)) {
@@ -652,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
           b = b < 0 ? 0 : b > 15 ? 15 : b;
           atomicAdd(a.rare + b, 1ull);
         }
-        continue;
+        return;
       } else {
         const uint32_t self = static_cast<uint32_t>(deg <= t.small_max ? t.small_max : t.medium_max);
         acc = tile_decide_rare<R, kSoA, kStaged>(tv, a.fan16 + __ldg(a.off + s), self, w0, stride, deg, pv, cand, thr,
@@ -666,7 +693,16 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
       const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
       disp = d > disp ? d : disp;
     }
-    if (a.decision) a.decision[s] = acc ? 1 : 0;
+    if (decision) decision[s] = acc ? 1 : 0;
+  };
+
+  // (Fully unrolled per-valence variants of `vertex` were measured slower: their code size
+  // thrashes the instruction cache — stall_no_inst became the top stall.)
+#pragma unroll 1
+  for (int i = tid; i < n_in; i += kThreads) {
+    const uint32_t meta = meta_s[i];
+    if (((meta >> kMetaDegShift) & 15u) == 0) continue;  // pinned, or a medium / warp tier row
+    vertex(std::integral_constant<int, 0>{}, i, meta);
   }
   // Exact decisions of the tile's near-ties, from the staged tile, one warp per vertex (lane j
   // evaluates triangle j): the reference's arithmetic throughout — ordered neighbour sum,
