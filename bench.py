@@ -19,8 +19,9 @@ JSON keys (one line, rank 0):
   clocks       nvidia-smi samples taken during the timed region
 
 --impl reference runs the reference's CPU implementation instead (rank 0 only).
-Multi-GPU (torchrun): every rank smooths its own replica of the mesh (weak scaling); the
-partitioned halo-exchange path is DESIGN.md §6 "next".
+Multi-GPU (torchrun, N > 1): the mesh is partitioned over the ranks (Hilbert ranges with
+one-ring halos) and every pass exchanges the halo coordinates (NCCL); strong
+scaling of the same mesh.
 """
 from __future__ import annotations
 
@@ -490,7 +491,7 @@ def main():
             "ms_per_pass": pass_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "node_update (thread per vertex) + hub_update",
+                         "kernel": "tile_update (tile-staged, thread per vertex) + warp_update + hub_fast_update",
                          "bytes_per_launch": b_pass, "launch_ms": node_ms_per_launch,
                          "bytes_model": "SURVEY 8(d) B_pass: 2c*nv + 8(nv+1) + 4*sum_deg + 24*nt + nv"},
             "e2e": e2e,
