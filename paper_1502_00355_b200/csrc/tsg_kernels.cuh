@@ -594,26 +594,18 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   int accepted = 0;
   double disp = 0.0;
 
-  // One vertex; D > 0: the valence is the compile-time constant D (fully unrolled sum and cycle
-  // sweep, no loop-carried copies), D == 0: run-time valence.
-  auto vertex = [&](auto d_const, int i, uint32_t meta) {
-    constexpr int D = decltype(d_const)::value;
-    const int deg = D > 0 ? D : static_cast<int>((meta >> kMetaDegShift) & 15u);
+  // One vertex of the tile (local index i).
+  auto vertex = [&](int i, uint32_t meta) {
+    const int deg = static_cast<int>((meta >> kMetaDegShift) & 15u);
     const uint32_t w0 = meta & kMetaBaseMask, stride = meta >> kMetaStrideShift;
-    auto wd = [&](int j) { return tv.word(w0 + j * stride); };
     const R2 pv = pts[i];
+    // neighbor_mean (smoothing.hpp:72-80): ordered chain over row[] (ascending original id).
     R sx = R(0), sy = R(0);
-    if constexpr (D > 0) {
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const R2 c = tv.get(wd(j) & kLocalMask);
-        sx = O::add(sx, c.x);
-        sy = O::add(sy, c.y);
-      }
-    } else {
+    {
+      uint32_t w = w0;
 #pragma unroll 2
-      for (int j = 0; j < deg; ++j) {
-        const R2 c = tv.get(wd(j) & kLocalMask);
+      for (int j = 0; j < deg; ++j, w += stride) {
+        const R2 c = tv.get(tv.word(w) & kLocalMask);
         sx = O::add(sx, c.x);
         sy = O::add(sy, c.y);
       }
@@ -625,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     // Exact tie (candidate == position; Form A reads only pass-start values): every
     // hypothetical α equals its threshold α bit for bit, the strict test fails.
     if (!(cand.x == pv.x && cand.y == pv.y)) {
-      const uint32_t l0 = (wd(0) >> kWordCycleShift) & kLocalMask;
+      const uint32_t l0 = (tv.word(w0) >> kWordCycleShift) & kLocalMask;
       R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
       const bool cyc = l0 != kNoLocal;
       if (cyc) {
@@ -640,26 +632,28 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
           thr = min_ref(thr, tp);
           hyp = min_ref(hyp, tc);
         };
-        auto edge = [&](int j) { return ring_edge<R>(tv.get((wd(j) >> kWordCycleShift) & kLocalMask), pv, cand); };
-        if constexpr (D > 0) {
-          const RingEdge<R> e0 = ring_edge<R>(tv.get(l0), pv, cand);
-          RingEdge<R> ea = e0;
-#pragma unroll
-          for (int j = 1; j < D; ++j) {
-            const RingEdge<R> eb = edge(j);
-            tri(ea, eb);
-            ea = eb;
-          }
-          tri(ea, e0);
+        auto edge_at = [&](uint32_t w) {
+          return ring_edge<R>(tv.get((tv.word(w) >> kWordCycleShift) & kLocalMask), pv, cand);
+        };
+        // Around the cycle two triangles per iteration with the two edge variables swapping
+        // roles (no loop-carried register copies); the closing triangle recomputes the first
+        // edge instead of keeping it live.
+        RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
+        uint32_t w = w0 + stride;
+        int j = 1;
+#pragma unroll 1
+        for (; j + 2 <= deg; j += 2, w += 2 * stride) {
+          const RingEdge<R> eb = edge_at(w);
+          tri(ea, eb);
+          ea = edge_at(w + stride);
+          tri(eb, ea);
+        }
+        if (j < deg) {
+          const RingEdge<R> eb = edge_at(w);
+          tri(ea, eb);
+          tri(eb, ring_edge<R>(tv.get(l0), pv, cand));
         } else {
-          RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
-#pragma unroll 2
-          for (int j = 1; j < deg; ++j) {
-            const RingEdge<R> eb = edge(j);
-            tri(ea, eb);
-            ea = eb;
-          }
-          tri(ea, ring_edge<R>(tv.get(l0), pv, cand));  // closing triangle (recomputed: registers)
+          tri(ea, ring_edge<R>(tv.get(l0), pv, cand));
         }
       }
       const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
@@ -702,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   for (int i = tid; i < n_in; i += kThreads) {
     const uint32_t meta = meta_s[i];
     if (((meta >> kMetaDegShift) & 15u) == 0) continue;  // pinned, or a medium / warp tier row
-    vertex(std::integral_constant<int, 0>{}, i, meta);
+    vertex(i, meta);
   }
   // Exact decisions of the tile's near-ties, from the staged tile, one warp per vertex (lane j
   // evaluates triangle j): the reference's arithmetic throughout — ordered neighbour sum,
