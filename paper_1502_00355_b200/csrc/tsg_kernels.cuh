@@ -349,8 +349,8 @@ __device__ __forceinline__ void ring_pair(const RingEdge<R>& x, const RingEdge<R
   const R lab = fma(ex, ex, ey * ey);
   const R cp = fma(x.px, y.py, -(x.py * y.px));
   const R cc = fma(x.cx, y.cy, -(x.cy * y.cx));
-  tp = cp * rcp_refined<2>(x.lp + y.lp + lab);
-  tc = cc * rcp_refined<2>(x.lc + y.lc + lab);
+  tp = cp * rcp_cubic(x.lp + y.lp + lab);
+  tc = cc * rcp_cubic(x.lc + y.lc + lab);
 }
 
 template <typename R>
@@ -826,8 +826,8 @@ __global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) 
       const R cax = qa.x - cand.x, cay = qa.y - cand.y, cbx = qb.x - cand.x, cby = qb.y - cand.y;
       const R ep = fma(pax, pax, pay * pay) + fma(pbx, pbx, pby * pby) + lab;
       const R ec = fma(cax, cax, cay * cay) + fma(cbx, cbx, cby * cby) + lab;
-      R tp = fma(pax, pby, -(pay * pbx)) * rcp_refined<2>(ep);
-      R tc = fma(cax, cby, -(cay * cbx)) * rcp_refined<2>(ec);
+      R tp = fma(pax, pby, -(pay * pbx)) * rcp_cubic(ep);
+      R tc = fma(cax, cby, -(cay * cbx)) * rcp_cubic(ec);
       if constexpr (!kExact) {
         tp = isfinite(tp) ? tp : R(0);
         tc = isfinite(tc) ? tc : R(0);
@@ -893,7 +893,7 @@ __device__ __forceinline__ R rot_fast(typename Arith<R>::R2 qa, typename Arith<R
   const R ex = bx - ax, ey = by - ay;
   const R lab = fma(ex, ex, ey * ey);
   const R la = fma(ax, ax, ay * ay), lb = fma(bx, bx, by * by);
-  return fma(ax, by, -(ay * bx)) * rcp_refined<2>(la + lb + lab);
+  return fma(ax, by, -(ay * bx)) * rcp_cubic(la + lb + lab);
 }
 
 // CTA per hub (Form A fused, valence above the warp tier's staging cap): the paper's CDP child
