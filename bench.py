@@ -238,7 +238,8 @@ def run_reference_arm(args, cfg):
 def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     """N GPUs, one process each: the mesh is partitioned (Hilbert ranges + one-ring halos) and
     every pass exchanges halos (NCCL all-to-all on device buffers) and all-reduces the stop
-    statistics — strong scaling of one mesh (paper_1502_00355_b200/distributed.py)."""
+    statistics, all enqueued on the engine stream (DeviceLoop: no host round trip per pass) —
+    strong scaling of one mesh (paper_1502_00355_b200/distributed.py)."""
     import paper_1502_00355_b200 as ts
     from paper_1502_00355_b200 import capi, distributed as D
 
@@ -253,7 +254,8 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     ctx = capi.Context(dev_index)
     eng = D.DeviceEngine(ctx, part, layout=cfg["layout"], precision=cfg["precision"])
     device_buffers = args.transport == "nccl"
-    ex = D.Exchanger(part, device=device_buffers, torch_device=torch.device("cuda", dev_index))
+    loop = D.DeviceLoop(eng, part, device=device_buffers, torch_device=torch.device("cuda", dev_index),
+                        stream_ptr=ctx.stream)
     prep_s = time.time() - t0
     diag = ts.bbox_diagonal(xy)
     passes = cfg["passes"]
@@ -261,12 +263,13 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
                          move_tol=cfg["move_tol"], bbox_diag=diag)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev_index))
 
-    def step():
+    def step():  # device-resident pass loop: pass, halo all-to-all, stats all-reduce, stop rule
         eng.mesh.restore_coords()
-        return D.smooth_partitioned(eng, ex, scfg, passes, cfg["move_tol"], diag)
+        return loop.smooth(scfg)
 
     for _ in range(args.warmup):
         it, _, _, _ = step()
+    launches_per_step = eng.mesh.dist_launches  # this rank's kernels in one step (tsg_dist_end)
     sampler = ClockSampler(dev_index)
     sampler.start()
     dist.barrier()
@@ -288,6 +291,30 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     value = updates / (elapsed_ms / 1000.0)  # whole-mesh node updates (every rank's share)
     halo = torch.tensor([len(part.send_ids)], dtype=torch.int64, device="cuda" if device_buffers else "cpu")
     dist.all_reduce(halo, op=dist.ReduceOp.MAX)
+
+    # End to end through the public API with host buffers: each rank uploads its partition's
+    # coordinates (H2D), runs the pass loop and reads back its owned coordinates (D2H).
+    part_xy = np.ascontiguousarray(part.xy)
+    dist.barrier()
+    t_e = time.perf_counter()
+    e2e_updates = 0
+    for _ in range(args.steps):
+        eng.mesh.set_coords(part_xy)
+        it_e, _, _, _ = loop.smooth(scfg)
+        _ = eng.owned_coords()
+        e2e_updates += nv * it_e
+    dist.barrier()
+    e2e_s = torch.tensor([time.perf_counter() - t_e], dtype=torch.float64,
+                         device="cuda" if device_buffers else "cpu")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    io = torch.tensor([16 * len(part_xy), 16 * int(part.owned.sum())], dtype=torch.int64,
+                      device="cuda" if device_buffers else "cpu")
+    dist.all_reduce(io, op=dist.ReduceOp.SUM)
+    sum_deg = int(topo["nbr_off"][-1])
+    b_pass = algorithmic_bytes_per_pass(nv, nt, sum_deg, cfg["precision"])
+    pass_ms = elapsed_ms / max(1, args.steps * passes)
+    peak, peak_src = measured_peak()
+    achieved = b_pass / world / (pass_ms / 1000.0) / 1e9  # per GPU, pass time incl. the exchange
     if rank == 0:
         out = {
             "metric": "node-updates/sec (Smart Laplacian)", "value": value, "unit": "node-updates/s",
@@ -299,9 +326,18 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
                        "parallelism": f"partitioned x{world} (Hilbert ranges, one-ring halo, "
                                       f"{args.transport} all-to-all per pass)",
                        "max_halo_vertices_per_rank": int(halo.item()), "generator_args": list(gargs)},
-            "ms_per_pass": elapsed_ms / max(1, args.steps * passes),
-            "roofline": None, "e2e": None, "cpu_baseline": None, "clocks": clocks,
-            "gpu_launches": None, "prep_s": prep_s,
+            "ms_per_pass": pass_ms,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "per-GPU share of B_pass over the whole pass (node kernels + halo "
+                                   "exchange + stats all-reduce)",
+                         "bytes_per_launch": b_pass / world},
+            "e2e": {"value": e2e_updates / float(e2e_s.item()), "unit": "node-updates/s",
+                    "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item()),
+                    "path": "per rank: set_coords (host) -> device pass loop -> owned coords (host)"},
+            "cpu_baseline": None, "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps, "launches_per_step_rank0": launches_per_step,
+            "prep_s": prep_s,
         }
         print(json.dumps(out))
     eng.mesh.free()

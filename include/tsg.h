@@ -168,6 +168,31 @@ tsg_status tsg_halo_plan(tsg_mesh* mesh, const int64_t* send_ids, int64_t n_send
 tsg_status tsg_halo_pack(tsg_mesh* mesh, double* out, int32_t out_is_host);
 tsg_status tsg_halo_unpack(tsg_mesh* mesh, const double* in, int32_t in_is_host);
 
+/* Device-resident partitioned pass loop (Form A): every call below only ENQUEUES work on the
+ * context stream (no host synchronisation), so a driver can chain, per pass,
+ *   tsg_dist_pass -> tsg_dist_halo_pack -> all-to-all -> tsg_dist_halo_unpack
+ *                 -> all-gather of the stats pairs -> tsg_dist_finalize
+ * with NCCL collectives ordered on the same stream, and poll tsg_dist_status every few passes.
+ * Kernels of passes enqueued after the global stop fired exit immediately.
+ *   begin:    resets the device pass state for a run of cfg->max_iters passes
+ *   pass:     one pass's node kernels; writes this partition's {accepted count, max
+ *             displacement} of the pass as two doubles to the DEVICE buffer stats_dev
+ *   halo_*:   halo copies through DEVICE buffers, current buffer chosen on the device
+ *   finalize: the reference's stop rule (smoothing.cpp:132-141) on the n_parts all-gathered
+ *             DEVICE pairs (sum of accepted, max of displacement)
+ *   status:   synchronises; passes executed, done flag, TSG_STOP_*
+ *   end:      synchronises; per-pass totals (as tsg_smooth), the final state and the number of
+ *             kernels the dist calls enqueued since begin */
+tsg_status tsg_dist_begin(tsg_mesh* mesh, const tsg_smooth_cfg* cfg);
+tsg_status tsg_dist_pass(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, double* stats_dev);
+tsg_status tsg_dist_halo_pack(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, double* out_dev);
+tsg_status tsg_dist_halo_unpack(tsg_mesh* mesh, const double* in_dev);
+tsg_status tsg_dist_finalize(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, const double* gathered_dev, int32_t n_parts);
+tsg_status tsg_dist_status(tsg_mesh* mesh, int32_t* iterations, int32_t* done, int32_t* stop);
+tsg_status tsg_dist_end(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, int32_t* accepted_per_pass,
+                        double* max_disp_per_pass, int32_t capacity, int32_t* iterations_out, int32_t* stop_out,
+                        int64_t* launches_out);
+
 /* ---- diagnostics ---- */
 /* Evaluates n seeded random triangles (unit scale, tiny, huge, near-degenerate) with the
  * kernels' fast alpha (refined reciprocal) and with the reference's IEEE division; returns the

@@ -32,7 +32,8 @@ EXPORTS = (
     "tsg_tri_alpha",
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
     "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
-    "tsg_halo_pack", "tsg_halo_unpack",
+    "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
+    "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end",
 )
 
 
@@ -90,6 +91,13 @@ def lib() -> C.CDLL:
             "tsg_halo_plan": (i32, [P, P, i64, P, i64]),
             "tsg_halo_pack": (i32, [P, C.c_void_p, i32]),
             "tsg_halo_unpack": (i32, [P, C.c_void_p, i32]),
+            "tsg_dist_begin": (i32, [P, C.POINTER(SmoothCfg)]),
+            "tsg_dist_pass": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p]),
+            "tsg_dist_halo_pack": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p]),
+            "tsg_dist_halo_unpack": (i32, [P, C.c_void_p]),
+            "tsg_dist_finalize": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p, i32]),
+            "tsg_dist_status": (i32, [P, P, P, P]),
+            "tsg_dist_end": (i32, [P, C.POINTER(SmoothCfg), P, P, i32, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -266,3 +274,36 @@ class DeviceMesh:
 
     def halo_unpack(self, in_ptr: int, on_host: bool):
         check(lib().tsg_halo_unpack(self.h, C.c_void_p(in_ptr), 1 if on_host else 0), "tsg_halo_unpack")
+
+    # Device-resident partitioned loop (include/tsg.h, tsg_dist_*): enqueue-only calls taking
+    # device pointers (e.g. torch CUDA tensors' data_ptr()).
+    def dist_begin(self, cfg: SmoothCfg):
+        check(lib().tsg_dist_begin(self.h, C.byref(cfg)), "tsg_dist_begin")
+
+    def dist_pass(self, cfg: SmoothCfg, stats_ptr: int):
+        check(lib().tsg_dist_pass(self.h, C.byref(cfg), C.c_void_p(stats_ptr)), "tsg_dist_pass")
+
+    def dist_halo_pack(self, cfg: SmoothCfg, out_ptr: int):
+        check(lib().tsg_dist_halo_pack(self.h, C.byref(cfg), C.c_void_p(out_ptr)), "tsg_dist_halo_pack")
+
+    def dist_halo_unpack(self, in_ptr: int):
+        check(lib().tsg_dist_halo_unpack(self.h, C.c_void_p(in_ptr)), "tsg_dist_halo_unpack")
+
+    def dist_finalize(self, cfg: SmoothCfg, gathered_ptr: int, n_parts: int):
+        check(lib().tsg_dist_finalize(self.h, C.byref(cfg), C.c_void_p(gathered_ptr), n_parts), "tsg_dist_finalize")
+
+    def dist_status(self):
+        it, done, stop = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib().tsg_dist_status(self.h, C.byref(it), C.byref(done), C.byref(stop)), "tsg_dist_status")
+        return it.value, bool(done.value), STOP[stop.value]
+
+    def dist_end(self, cfg: SmoothCfg):
+        cap = max(1, cfg.max_iters)
+        acc = np.zeros(cap, dtype=np.int32)
+        md = np.zeros(cap, dtype=np.float64)
+        it, stop, launches = C.c_int32(), C.c_int32(), C.c_int64()
+        check(lib().tsg_dist_end(self.h, C.byref(cfg), _ptr(acc), _ptr(md), cap, C.byref(it), C.byref(stop),
+                                 C.byref(launches)), "tsg_dist_end")
+        n = it.value
+        self.dist_launches = launches.value
+        return n, STOP[stop.value], acc[:n].copy(), md[:n].copy()

@@ -233,6 +233,90 @@ __global__ void selftest_alpha_cycle(int64_t n, uint64_t seed, unsigned long lon
   }
 }
 
+// Partitioned driver (tsg_dist_*): this partition's totals of the current pass, {accepted,
+// max displacement} as two doubles (exact: counts < 2^53), for the cross-partition all-gather
+// (0 / 0 once the global stop fired: the pass did not run).
+__global__ void dist_fold(const tsg::PassState* st, const int32_t* slot_acc, const unsigned long long* slot_md,
+                          double* out) {
+  const int lane = threadIdx.x;
+  const int q = st->pass;
+  const bool done = st->done != 0;
+  int32_t acc = done ? 0 : slot_acc[q * tsg::kStatSlots + lane];
+  unsigned long long mdb = done ? 0ull : slot_md[q * tsg::kStatSlots + lane];
+  acc = __reduce_add_sync(0xffffffffu, acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, mdb, o);
+    mdb = other > mdb ? other : mdb;
+  }
+  if (lane == 0) {
+    out[0] = static_cast<double>(acc);
+    out[1] = __longlong_as_double(static_cast<long long>(mdb));
+  }
+}
+
+// The reference's stop rule (smoothing.cpp:132-141) on the totals of all partitions (the
+// all-gathered {accepted, max displacement} pairs: sum and max); advances the device pass
+// counter exactly like finalize_pass.
+__global__ void dist_finalize(tsg::PassState* st, const double* gathered, int32_t n_parts, int32_t* pass_acc,
+                              unsigned long long* pass_md, double tol_abs, int32_t max_iters) {
+  if (st->done) return;
+  const int q = st->pass;
+  long long acc = 0;
+  double md = 0.0;
+  for (int r = 0; r < n_parts; ++r) {
+    acc += static_cast<long long>(gathered[2 * r]);
+    md = gathered[2 * r + 1] > md ? gathered[2 * r + 1] : md;
+  }
+  pass_acc[q] = static_cast<int32_t>(acc);
+  pass_md[q] = static_cast<unsigned long long>(__double_as_longlong(md));
+  st->pass = q + 1;
+  if (acc == 0) {
+    st->done = 1;
+    st->stop = tsg::kStopNoMoves;
+  } else if (md < tol_abs) {
+    st->done = 1;
+    st->stop = tsg::kStopDisplacement;
+  } else if (q + 1 >= max_iters) {
+    st->done = 1;
+    st->stop = tsg::kStopMaxIters;
+  }
+}
+
+// Halo copies of the partitioned driver: the current buffer is chosen on the device (the pass
+// just executed wrote N = buffer ((pass & 1) ? buf0 : buf1) in ping-pong mode, buf0 in copy
+// mode); nothing is copied once the global stop fired.
+template <typename R, bool kSoA>
+__global__ void dist_halo_pack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1, int32_t swap,
+                               const tsg::PassState* st, const int32_t* __restrict__ slots, int64_t n,
+                               double* __restrict__ out) {
+  if (st->done) return;
+  const tsg::Coords<R, kSoA> cur = (swap == tsg::kSwapCopy || (st->pass & 1)) ? b0 : b1;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const auto p = cur.load_mut(slots[i]);
+    out[2 * i] = static_cast<double>(p.x);
+    out[2 * i + 1] = static_cast<double>(p.y);
+  }
+}
+
+template <typename R, bool kSoA>
+__global__ void dist_halo_unpack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1, const tsg::PassState* st,
+                                 const int32_t* __restrict__ slots, int64_t n, const double* __restrict__ in,
+                                 unsigned long long* maxabs) {
+  if (st->done) return;
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = in[2 * i], y = in[2 * i + 1];
+    const auto p = tsg::Arith<R>::make(static_cast<R>(x), static_cast<R>(y));
+    b0.store(slots[i], p);
+    b1.store(slots[i], p);
+    m = fmax(m, abs_max2(x, y));
+  }
+  commit_maxabs(m, maxabs);
+}
+
 struct GraphCache {
   bool valid = false;
   int32_t form = -1, strategy = -1, chunks = -1, swap = -1, max_iters = -1;
@@ -294,6 +378,7 @@ struct tsg_mesh {
   int cur = 0;
   int32_t hub_max_deg = 0;
   int64_t n_hub_fast = 0;  // leading entries of hm.large with deg > kWarpTierCap
+  int64_t dist_launches = 0;  // kernels enqueued by tsg_dist_* since tsg_dist_begin
   // Form B schedule cache
   int32_t fb_chunks = 0;
   uint32_t* d_nbr_fresh = nullptr;
@@ -515,7 +600,7 @@ struct Engine {
   static tsg_status enqueue_pass_t(tsg_mesh* m, const tsg_smooth_cfg& c, cudaStream_t s,
                                    double tol_abs, cudaGraphConditionalHandle h, int use_handle,
                                    int8_t* decision, cudaEvent_t ev_begin, cudaEvent_t ev_end,
-                                   int64_t* kernels) {
+                                   int64_t* kernels, bool with_finalize = true) {
     const int64_t nv = m->hm.nv;
     m->ctx->fork_next = 0;  // fork/join events are reusable once their waits are enqueued
     if (c.swap == TSG_SWAP_COPY)
@@ -550,6 +635,7 @@ struct Engine {
       }
     }
     if (ev_end) TSG_CUDA(cudaEventRecord(ev_end, s));
+    if (!with_finalize) return TSG_OK;  // partitioned driver: the stop rule runs on global totals
     tsg::finalize_pass<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, m->d_acc, m->d_md, tol_abs,
                                         c.max_iters, h, use_handle);
     TSG_CUDA(cudaGetLastError());
@@ -603,12 +689,12 @@ struct Engine {
 
   static tsg_status enqueue_pass(tsg_mesh* m, const tsg_smooth_cfg& c, cudaStream_t s, double tol_abs,
                                  cudaGraphConditionalHandle h, int use_handle, int8_t* decision,
-                                 cudaEvent_t e0, cudaEvent_t e1, int64_t* kernels) {
+                                 cudaEvent_t e0, cudaEvent_t e1, int64_t* kernels, bool fin = true) {
     const bool fb = c.form == TSG_FORM_B, tp = c.strategy == TSG_STRATEGY_TWOPHASE;
-    if (fb && tp) return enqueue_pass_t<true, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
-    if (fb) return enqueue_pass_t<true, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
-    if (tp) return enqueue_pass_t<false, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
-    return enqueue_pass_t<false, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels);
+    if (fb && tp) return enqueue_pass_t<true, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
+    if (fb) return enqueue_pass_t<true, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
+    if (tp) return enqueue_pass_t<false, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
+    return enqueue_pass_t<false, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
   }
 
   static tsg_status set_coords(tsg_mesh* m, const double* xy_host) {
@@ -1247,6 +1333,130 @@ tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, c
   TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
   m->n_send = n_send;
   m->n_recv = n_recv;
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_begin(tsg_mesh* m, const tsg_smooth_cfg* c) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  tsg_status st = validate_cfg(c);
+  if (st) return st;
+  if (c->form != TSG_FORM_A) return fail(TSG_ERR_INVALID, "the partitioned driver supports Form A");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  if ((st = ensure_stats_capacity(m, c->max_iters + 1))) return st;
+  st = dispatch(m, [&](auto E) { return decltype(E)::normalize(m); });  // current coordinates in buf0
+  if (st) return st;
+  m->dist_launches = 0;
+  TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * (c->max_iters + 1), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * (c->max_iters + 1), s));
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_pass(tsg_mesh* m, const tsg_smooth_cfg* c, double* stats_dev) {
+  if (!m || !stats_dev) return fail(TSG_ERR_INVALID, "null argument");
+  tsg_status st = validate_cfg(c);
+  if (st) return st;
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  cudaStream_t s = m->ctx->stream;
+  int64_t k = 0;
+  st = dispatch(m, [&](auto E) {
+    return decltype(E)::enqueue_pass(m, *c, s, -1.0, cudaGraphConditionalHandle{}, 0, nullptr, nullptr, nullptr, &k,
+                                     false);
+  });
+  if (st) return st;
+  dist_fold<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, stats_dev);
+  TSG_CUDA(cudaGetLastError());
+  m->dist_launches += k + 1;
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_halo_pack(tsg_mesh* m, const tsg_smooth_cfg* c, double* out_dev) {
+  if (!m || !c || (m->n_send && !out_dev)) return fail(TSG_ERR_INVALID, "bad halo pack arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  if (m->n_send == 0) return TSG_OK;
+  cudaStream_t s = m->ctx->stream;
+  const unsigned g = grid_for(m->n_send, 256);
+  if (m->prec == TSG_F64) {
+    if (m->layout == TSG_LAYOUT_SOA)
+      dist_halo_pack<double, true><<<g, 256, 0, s>>>(coords_of<double, true>(m, 0), coords_of<double, true>(m, 1), c->swap, m->d_state, m->d_send_slots, m->n_send, out_dev);
+    else
+      dist_halo_pack<double, false><<<g, 256, 0, s>>>(coords_of<double, false>(m, 0), coords_of<double, false>(m, 1), c->swap, m->d_state, m->d_send_slots, m->n_send, out_dev);
+  } else {
+    if (m->layout == TSG_LAYOUT_SOA)
+      dist_halo_pack<float, true><<<g, 256, 0, s>>>(coords_of<float, true>(m, 0), coords_of<float, true>(m, 1), c->swap, m->d_state, m->d_send_slots, m->n_send, out_dev);
+    else
+      dist_halo_pack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), c->swap, m->d_state, m->d_send_slots, m->n_send, out_dev);
+  }
+  TSG_CUDA(cudaGetLastError());
+  ++m->dist_launches;
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_halo_unpack(tsg_mesh* m, const double* in_dev) {
+  if (!m || (m->n_recv && !in_dev)) return fail(TSG_ERR_INVALID, "bad halo unpack arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  if (m->n_recv == 0) return TSG_OK;
+  cudaStream_t s = m->ctx->stream;
+  const unsigned g = grid_for(m->n_recv, 256);
+  if (m->prec == TSG_F64) {
+    if (m->layout == TSG_LAYOUT_SOA)
+      dist_halo_unpack<double, true><<<g, 256, 0, s>>>(coords_of<double, true>(m, 0), coords_of<double, true>(m, 1), m->d_state, m->d_recv_slots, m->n_recv, in_dev, m->d_maxabs);
+    else
+      dist_halo_unpack<double, false><<<g, 256, 0, s>>>(coords_of<double, false>(m, 0), coords_of<double, false>(m, 1), m->d_state, m->d_recv_slots, m->n_recv, in_dev, m->d_maxabs);
+  } else {
+    if (m->layout == TSG_LAYOUT_SOA)
+      dist_halo_unpack<float, true><<<g, 256, 0, s>>>(coords_of<float, true>(m, 0), coords_of<float, true>(m, 1), m->d_state, m->d_recv_slots, m->n_recv, in_dev, m->d_maxabs);
+    else
+      dist_halo_unpack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), m->d_state, m->d_recv_slots, m->n_recv, in_dev, m->d_maxabs);
+  }
+  TSG_CUDA(cudaGetLastError());
+  ++m->dist_launches;
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_finalize(tsg_mesh* m, const tsg_smooth_cfg* c, const double* gathered_dev, int32_t n_parts) {
+  if (!m || !c || !gathered_dev || n_parts < 1) return fail(TSG_ERR_INVALID, "bad finalize arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
+  dist_finalize<<<1, 1, 0, m->ctx->stream>>>(m->d_state, gathered_dev, n_parts, m->d_acc, m->d_md, tol_abs,
+                                            c->max_iters);
+  TSG_CUDA(cudaGetLastError());
+  ++m->dist_launches;
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_status(tsg_mesh* m, int32_t* iterations, int32_t* done, int32_t* stop) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  tsg::PassState hs;
+  TSG_CUDA(cudaMemcpyAsync(&hs, m->d_state, sizeof hs, cudaMemcpyDeviceToHost, m->ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  if (iterations) *iterations = hs.pass;
+  if (done) *done = hs.done;
+  if (stop) *stop = hs.stop;
+  return TSG_OK;
+}
+
+tsg_status tsg_dist_end(tsg_mesh* m, const tsg_smooth_cfg* c, int32_t* accepted_per_pass, double* max_disp_per_pass,
+                        int32_t capacity, int32_t* iterations_out, int32_t* stop_out, int64_t* launches_out) {
+  if (!m || !c) return fail(TSG_ERR_INVALID, "null argument");
+  int32_t it = 0, done = 0, stop = 0;
+  tsg_status st = tsg_dist_status(m, &it, &done, &stop);
+  if (st) return st;
+  if (c->swap == TSG_SWAP_PINGPONG) m->cur = it & 1;
+  else m->cur = 0;
+  const int32_t n = std::min(capacity, it);
+  if (accepted_per_pass && n > 0)
+    TSG_CUDA(cudaMemcpy(accepted_per_pass, m->d_acc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  if (max_disp_per_pass && n > 0) {
+    std::vector<unsigned long long> bits(n);
+    TSG_CUDA(cudaMemcpy(bits.data(), m->d_md, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+    std::memcpy(max_disp_per_pass, bits.data(), sizeof(double) * n);
+  }
+  if (iterations_out) *iterations_out = it;
+  if (stop_out) *stop_out = stop;
+  if (launches_out) *launches_out = m->dist_launches;
   return TSG_OK;
 }
 

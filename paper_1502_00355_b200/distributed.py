@@ -6,6 +6,11 @@ device mesh holds the owned vertices plus a one-ring **halo** (every vertex of a
 touches an owned vertex), numbered locally in ascending global id so that neighbour sums keep
 the reference's ascending-id order.  Halo vertices are pinned locally.
 
+Two drivers: `smooth_partitioned` (host-synchronous per pass: simple, used by the CPU-side
+tests) and `DeviceLoop` (device-resident: the pass, the halo exchange, the stats all-gather and the
+stop rule are all enqueued on the engine's stream, NCCL ordered on it, the host polls every 8
+passes — the multi-GPU bench path).
+
 One pass (Form A, Jacobi — every read is pass-start) =
   1. `tsg_pass` on every rank (owned movable vertices updated on the device);
   2. halo exchange: each rank packs the new coordinates of its vertices that lie in other
@@ -214,6 +219,67 @@ def smooth_partitioned(engine, exchanger: Exchanger, cfg, max_iters: int, move_t
             stop = "displacement"
             break
     return len(accepted), stop, accepted, max_disp
+
+
+class DeviceLoop:
+    """The device-resident pass loop (include/tsg.h, tsg_dist_*): per pass the node kernels, the
+    halo exchange and the all-gather of {accepted, max displacement} are all ENQUEUED on the
+    engine's stream — NCCL collectives are ordered on it through torch's current stream — and the
+    stop rule runs on the device; the host polls the stop flag every `check_every` passes.  With
+    host (gloo) buffers the exchange and the all-gather go through host copies (testing)."""
+
+    def __init__(self, engine, part: Partition, device: bool, torch_device, stream_ptr: int):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.engine, self.part, self.device = torch, dist, engine, part, device
+        self.dev = torch_device
+        self.stream = torch.cuda.ExternalStream(stream_ptr, device=torch_device)
+        n_s, n_r = len(part.send_ids), len(part.recv_ids)
+        self.n_s, self.n_r = n_s, n_r
+        self.send = torch.empty(2 * max(1, n_s), dtype=torch.float64, device=torch_device)
+        self.recv = torch.empty(2 * max(1, n_r), dtype=torch.float64, device=torch_device)
+        self.stats = torch.zeros(2, dtype=torch.float64, device=torch_device)  # {accepted, max disp}
+        self.gathered = torch.zeros(2 * part.world, dtype=torch.float64, device=torch_device)
+        self.in_splits = [2 * c for c in part.send_counts]
+        self.out_splits = [2 * c for c in part.recv_counts]
+
+    def _exchange(self, cfg):
+        mesh, dist = self.engine.mesh, self.dist
+        if self.n_s:
+            mesh.dist_halo_pack(cfg, self.send.data_ptr())
+        if self.device:
+            dist.all_to_all_single(self.recv[: 2 * self.n_r], self.send[: 2 * self.n_s], self.out_splits,
+                                   self.in_splits)
+        else:
+            recv = self.recv[: 2 * self.n_r].cpu()
+            dist.all_to_all_single(recv, self.send[: 2 * self.n_s].cpu(), self.out_splits, self.in_splits)
+            self.recv[: 2 * self.n_r].copy_(recv)
+        if self.n_r:
+            mesh.dist_halo_unpack(self.recv.data_ptr())
+
+    def _gather(self):
+        if self.device:
+            self.dist.all_gather_into_tensor(self.gathered, self.stats)
+        else:
+            out = [self.torch.empty(2, dtype=self.torch.float64) for _ in range(self.part.world)]
+            self.dist.all_gather(out, self.stats.cpu())
+            self.gathered.copy_(self.torch.cat(out))
+
+    def smooth(self, cfg, check_every: int = 8):
+        """Runs cfg.max_iters passes at most (stop rule on the global totals).  Returns
+        (iterations, stop, accepted_per_pass, max_disp_per_pass)."""
+        mesh = self.engine.mesh
+        mesh.dist_begin(cfg)
+        with self.torch.cuda.stream(self.stream):
+            for q in range(cfg.max_iters):
+                mesh.dist_pass(cfg, self.stats.data_ptr())
+                self._exchange(cfg)
+                self._gather()
+                mesh.dist_finalize(cfg, self.gathered.data_ptr(), self.part.world)
+                if (q + 1) % check_every == 0 and mesh.dist_status()[1]:
+                    break
+        return mesh.dist_end(cfg)
 
 
 def gather_coords(part: Partition, owned_xy: np.ndarray, nv: int):

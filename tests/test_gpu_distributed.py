@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port_num, args, layout, precision, max_iters, move_tol, out_path):
+def _worker(rank, world, port_num, args, layout, precision, max_iters, move_tol, out_path, driver="host"):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
 
@@ -34,9 +34,17 @@ def _worker(rank, world, port_num, args, layout, precision, max_iters, move_tol,
     part = D.build_partition(rank, world, owner, xy, tri, topo)
     ctx = capi.Context(0)
     eng = D.DeviceEngine(ctx, part, layout=layout, precision=precision)
-    ex = D.Exchanger(part, device=False)
-    cfg = capi.make_cfg(form="a", strategy="fused", max_iters=max_iters)
-    it, stop, acc, md = D.smooth_partitioned(eng, ex, cfg, max_iters, move_tol, ts.bbox_diagonal(xy))
+    if driver == "host":
+        ex = D.Exchanger(part, device=False)
+        cfg = capi.make_cfg(form="a", strategy="fused", max_iters=max_iters)
+        it, stop, acc, md = D.smooth_partitioned(eng, ex, cfg, max_iters, move_tol, ts.bbox_diagonal(xy))
+    else:  # device-resident loop (tsg_dist_*), gloo through host copies
+        import torch
+
+        cfg = capi.make_cfg(form="a", strategy="fused", max_iters=max_iters, move_tol=move_tol,
+                            bbox_diag=ts.bbox_diagonal(xy))
+        loop = D.DeviceLoop(eng, part, device=False, torch_device=torch.device("cuda", 0), stream_ptr=ctx.stream)
+        it, stop, acc, md = loop.smooth(cfg, check_every=3)
     full = D.gather_coords(part, eng.owned_coords(), len(xy))
     if rank == 0:
         np.savez(out_path, xy=full, acc=np.array(acc), md=np.array(md), it=it, stop=stop)
@@ -45,12 +53,15 @@ def _worker(rank, world, port_num, args, layout, precision, max_iters, move_tol,
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,args,layout,tol", [(2, (20000, 3), "aos", 0.0), (3, (9000, 8), "soa", 1e-6)])
-def test_partitioned_device_equals_single(tmp_path, port, world, args, layout, tol):
+@pytest.mark.parametrize("world,args,layout,tol,driver", [(2, (20000, 3), "aos", 0.0, "host"),
+                                                          (3, (9000, 8), "soa", 1e-6, "host"),
+                                                          (2, (20000, 3), "aos", 0.0, "device"),
+                                                          (3, (9000, 8), "aos", 1e-6, "device")])
+def test_partitioned_device_equals_single(tmp_path, port, world, args, layout, tol, driver):
     import paper_1502_00355_b200 as ts
 
     out = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(world, _free_port(), args, layout, "f64", 30, tol, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), args, layout, "f64", 30, tol, out, driver), nprocs=world, join=True)
     r = np.load(out)
     xy, tri = ts.delaunay_arrays(*args)
     want = port.smooth(xy, tri, form="a", chunks=1, max_iters=30, move_tol=tol)
