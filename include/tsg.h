@@ -193,6 +193,12 @@ tsg_status tsg_dist_end(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, int32_t* acce
                         double* max_disp_per_pass, int32_t capacity, int32_t* iterations_out, int32_t* stop_out,
                         int64_t* launches_out);
 
+/* Form B schedule: AUTO (default) walks the dependency levels inside one CTA per chunk when the
+ * levels are narrow (mean width < 4096 vertices: serial Form B on small meshes), else launches
+ * one set of tier kernels per level; LEVELS / CHUNKS force one of the two (identical results). */
+enum { TSG_FORMB_AUTO = 0, TSG_FORMB_LEVELS = 1, TSG_FORMB_CHUNKS = 2 };
+tsg_status tsg_mesh_formb_schedule(tsg_mesh* mesh, int32_t mode);
+
 /* ---- diagnostics ---- */
 /* Evaluates n seeded random triangles (unit scale, tiny, huge, near-degenerate) with the
  * kernels' fast alpha (refined reciprocal) and with the reference's IEEE division; returns the

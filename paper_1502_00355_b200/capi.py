@@ -33,7 +33,7 @@ EXPORTS = (
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
     "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
     "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
-    "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end",
+    "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
 )
 
 
@@ -92,6 +92,7 @@ def lib() -> C.CDLL:
             "tsg_halo_pack": (i32, [P, C.c_void_p, i32]),
             "tsg_halo_unpack": (i32, [P, C.c_void_p, i32]),
             "tsg_dist_begin": (i32, [P, C.POINTER(SmoothCfg)]),
+            "tsg_mesh_formb_schedule": (i32, [P, i32]),
             "tsg_dist_pass": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p]),
             "tsg_dist_halo_pack": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p]),
             "tsg_dist_halo_unpack": (i32, [P, C.c_void_p]),
@@ -274,6 +275,12 @@ class DeviceMesh:
 
     def halo_unpack(self, in_ptr: int, on_host: bool):
         check(lib().tsg_halo_unpack(self.h, C.c_void_p(in_ptr), 1 if on_host else 0), "tsg_halo_unpack")
+
+    def formb_schedule(self, mode: str):
+        """Form B schedule: "auto", "levels" (a launch per dependency level) or "chunks" (one CTA
+        per chunk walking its levels).  Results are identical."""
+        check(lib().tsg_mesh_formb_schedule(self.h, {"auto": 0, "levels": 1, "chunks": 2}[mode]),
+              "tsg_mesh_formb_schedule")
 
     # Device-resident partitioned loop (include/tsg.h, tsg_dist_*): enqueue-only calls taking
     # device pointers (e.g. torch CUDA tensors' data_ptr()).

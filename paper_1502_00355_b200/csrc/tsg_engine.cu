@@ -46,6 +46,7 @@ constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
 constexpr int kTileRecCap = 12288;  // ... row words staged in shared memory (multiple of 4)
+constexpr int64_t kFormBChunkWidth = 4096;  // Form B: chunk kernel below this mean level width
 constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
@@ -382,8 +383,12 @@ struct tsg_mesh {
   // Form B schedule cache
   int32_t fb_chunks = 0;
   uint32_t* d_nbr_fresh = nullptr;
-  int32_t *d_fb_nodes = nullptr, *d_fb_hubs = nullptr, *d_fb_medium = nullptr;
+  int32_t *d_fb_nodes = nullptr, *d_fb_hubs = nullptr, *d_fb_medium = nullptr;  // level-set schedule
   std::vector<tsg::Phase> fb_levels;
+  int32_t *d_cb_order = nullptr, *d_cb_lvl = nullptr, *d_cb_chunk = nullptr;  // chunk schedule
+  int64_t fb_nchunks = 0;
+  bool fb_use_chunks = false;  // narrow levels: one CTA per chunk instead of a launch per level
+  int32_t fb_mode = TSG_FORMB_AUTO;
   int64_t fb_bytes = 0;
   GraphCache gc;
   // Halo exchange plan (multi-GPU partitions): slots sent to / received from peers.
@@ -400,13 +405,17 @@ void free_form_b(tsg_mesh* m) {
   cudaFree(m->d_fb_nodes);
   cudaFree(m->d_fb_hubs);
   cudaFree(m->d_fb_medium);
-  m->d_fb_medium = nullptr;
+  m->d_fb_nodes = m->d_fb_hubs = m->d_fb_medium = nullptr;
+  m->fb_levels.clear();
+  cudaFree(m->d_cb_order);
+  cudaFree(m->d_cb_lvl);
+  cudaFree(m->d_cb_chunk);
+  m->d_cb_order = m->d_cb_lvl = m->d_cb_chunk = nullptr;
   m->d_nbr_fresh = nullptr;
-  m->d_fb_nodes = m->d_fb_hubs = nullptr;
   m->bytes -= m->fb_bytes;
   m->fb_bytes = 0;
   m->fb_chunks = 0;
-  m->fb_levels.clear();
+  m->fb_nchunks = 0;
 }
 
 tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
@@ -423,7 +432,19 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   if ((st = upload(&m->d_fb_nodes, sch.nodes, &b, s))) return st;
   if ((st = upload(&m->d_fb_hubs, sch.hubs, &b, s))) return st;
   if ((st = upload(&m->d_fb_medium, sch.medium, &b, s))) return st;
+  if ((st = upload(&m->d_cb_order, sch.cb_order, &b, s))) return st;
+  if ((st = upload(&m->d_cb_lvl, sch.lvl_off, &b, s))) return st;
+  if ((st = upload(&m->d_cb_chunk, sch.chunk_lvl, &b, s))) return st;
   TSG_CUDA(cudaStreamSynchronize(s));
+  m->fb_nchunks = static_cast<int64_t>(sch.chunk_lvl.size()) - 1;
+  {
+    // A launch per level costs a few microseconds; below ~4K vertices per level the chunk
+    // kernel (levels walked inside one CTA per chunk) is faster (cfg1: 195 levels of ~51).
+    const int64_t movable = static_cast<int64_t>(sch.cb_order.size());
+    const int64_t nlev = static_cast<int64_t>(sch.levels.size());
+    m->fb_use_chunks = m->fb_mode == TSG_FORMB_AUTO ? (nlev > 0 && movable < kFormBChunkWidth * nlev)
+                                                    : m->fb_mode == TSG_FORMB_CHUNKS;
+  }
   m->fb_levels = std::move(sch.levels);
   m->fb_bytes = b;
   m->bytes += b;
@@ -612,7 +633,7 @@ struct Engine {
     m->ctx->fork_next = 0;  // fork/join events are reusable once their waits are enqueued
     if (c.swap == TSG_SWAP_COPY)
       TSG_CUDA(cudaMemcpyAsync(m->buf[1], m->buf[0], 2 * nv * sizeof(R), cudaMemcpyDeviceToDevice, s));
-    if (kTwoPhase) {
+    if (kTwoPhase && !(kFormB && m->fb_use_chunks)) {
       tsg::tri_alpha<R, kSoA><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
           coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1), c.swap, m->d_state, m->d_tri,
           m->hm.nt, static_cast<R*>(m->d_alpha));
@@ -632,6 +653,12 @@ struct Engine {
                                                      static_cast<int64_t>(m->hm.hubs.size()),
                                                      hub_cap, s, kernels);
       if (st) return st;
+    } else if (m->fb_use_chunks) {
+      // Form B, both strategies (equal thresholds): one CTA per chunk.
+      tsg::formb_chunk_update<R, kSoA><<<static_cast<unsigned>(m->fb_nchunks), 256, 0, s>>>(
+          base, m->d_cb_order, m->d_cb_lvl, m->d_cb_chunk);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
     } else {
       for (const tsg::Phase& L : m->fb_levels) {
         tsg_status st = launch_phase<true, kTwoPhase>(m, base, m->d_fb_nodes + L.small_begin,
@@ -1340,6 +1367,17 @@ tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, c
   TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
   m->n_send = n_send;
   m->n_recv = n_recv;
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_formb_schedule(tsg_mesh* m, int32_t mode) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  if (mode < TSG_FORMB_AUTO || mode > TSG_FORMB_CHUNKS) return fail(TSG_ERR_INVALID, "unknown Form B schedule");
+  if (m->fb_mode != mode) {
+    m->fb_mode = mode;
+    m->fb_chunks = 0;  // rebuilt (and the graph re-captured) by the next Form B call
+    m->gc.reset();
+  }
   return TSG_OK;
 }
 

@@ -896,6 +896,110 @@ __device__ __forceinline__ R rot_fast(typename Arith<R>::R2 qa, typename Arith<R
   return fma(ax, by, -(ay * bx)) * rcp_cubic(la + lb + lab);
 }
 
+// Form B (ChunkView, quality.hpp:40-50; worker_chunk, parallel.hpp:19-24) with one CTA per
+// chunk: the CTA walks its chunk's dependency levels in order with a barrier between levels, so a
+// whole pass is ONE launch (the level-set schedule needs a launch per level: 195 per pass on the
+// 100x100 grid in serial Form B).  Thread per vertex, any valence: neighbour reads through the
+// view (in-chunk lower-id neighbours — kFreshBit — from N, written by earlier levels of this
+// CTA, the rest from the pass-start buffer P); the threshold at pass-start positions and the
+// hypothetical with the rotation filter (rot_fast, kGuardCycle), near-ties / degenerate
+// triangles with the reference's literal arithmetic (alpha_at).  Fused and TwoPhase give the same
+// thresholds, so both strategies use this kernel.
+template <typename R, bool kSoA>
+__global__ void __launch_bounds__(256) formb_chunk_update(PassArgs<R, kSoA> a, const int32_t* __restrict__ order,
+                                                          const int32_t* __restrict__ lvl_off,
+                                                          const int32_t* __restrict__ chunk_lvl) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  constexpr bool kExact = sizeof(R) == 8;
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+  const bool xonly = exact_only(a.maxabs);
+  int accepted = 0;
+  double disp = 0.0;
+  const int l0 = chunk_lvl[blockIdx.x], l1 = chunk_lvl[blockIdx.x + 1];
+#pragma unroll 1
+  for (int L = l0; L < l1; ++L) {
+    const int b = lvl_off[L], e = lvl_off[L + 1];
+#pragma unroll 1
+    for (int idx = b + threadIdx.x; idx < e; idx += blockDim.x) {
+      const int64_t s = order[idx];
+      const uint32_t o0 = __ldg(a.off + s);
+      const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
+      const uint32_t* nb = a.nbr + o0;
+      const uint32_t* fan = a.fan + o0;
+      auto view = [&](uint32_t u) -> R2 { return (u & kFreshBit) ? N.load_mut(u & ~kFreshBit) : P.load(u); };
+      const R2 pv = P.load(s);
+      R sx = R(0), sy = R(0);
+      for (int j = 0; j < deg; ++j) {  // neighbor_mean through the view (smoothing.hpp:72-80)
+        const R2 c = view(__ldg(nb + j));
+        sx = O::add(sx, c.x);
+        sy = O::add(sy, c.y);
+      }
+      const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
+      const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+      R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = __ldg(fan + j);
+        const uint32_t ua = __ldg(nb + fan_i1(f)), ub = __ldg(nb + fan_i2(f));
+        const R2 pa = P.load(ua & ~kFreshBit), pb = P.load(ub & ~kFreshBit);
+        const R2 va = (ua & kFreshBit) ? N.load_mut(ua & ~kFreshBit) : pa;
+        const R2 vb = (ub & kFreshBit) ? N.load_mut(ub & ~kFreshBit) : pb;
+        R tp = rot_fast<R>(pa, pb, pv), tc = rot_fast<R>(va, vb, cand);
+        if constexpr (!kExact) {
+          tp = isfinite(tp) ? tp : R(0);
+          tc = isfinite(tc) ? tc : R(0);
+        }
+        nan_acc = fma(tp, tc, nan_acc);
+        thr = min_ref(thr, tp);
+        hyp = min_ref(hyp, tc);
+      }
+      const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
+      bool acc;
+      if constexpr (!kExact) {
+        acc = hyp > thr;
+      } else if (!bad && hyp > thr + R(kGuardCycle)) {
+        acc = true;
+      } else if (!bad && hyp < thr - R(kGuardCycle)) {
+        acc = false;
+      } else {
+        R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+        for (int j = 0; j < deg; ++j) {
+          const uint32_t f = __ldg(fan + j);
+          const uint32_t ua = __ldg(nb + fan_i1(f)), ub = __ldg(nb + fan_i2(f));
+          const int k = fan_k(f);
+          {
+            const R2 qa = P.load(ua & ~kFreshBit), qb = P.load(ub & ~kFreshBit);
+            const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+            thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
+                                               O::mul(daby, daby)));
+          }
+          {
+            const R2 qa = view(ua), qb = view(ub);
+            const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+            hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby,
+                                               O::mul(dabx, dabx), O::mul(daby, daby)));
+          }
+        }
+        acc = hyp_e > thr_e;
+      }
+      N.store(s, acc ? cand : pv);
+      if (acc) {
+        ++accepted;
+        const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+        const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+        disp = d > disp ? d : disp;
+      }
+      if (a.decision) a.decision[s] = acc ? 1 : 0;
+    }
+    __syncthreads();  // this level's N writes are read by the next levels of the chunk
+  }
+  commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+}
+
 // CTA per hub (Form A fused, valence above the warp tier's staging cap): the paper's CDP child
 // launch becomes one CTA.  The row is staged in dynamic shared memory (up to
 // `cap` entries, the rest re-read from global memory); warp 0 forms the ordered neighbour sum

@@ -453,6 +453,33 @@ std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers,
     const int t = tiers.tier(hm.off[s + 1] - hm.off[s]);
     (*lists[t])[fill[t][L]++] = static_cast<int32_t>(s);
   }
+  {
+    // Chunk schedule: counting sort of the movable vertices by (chunk, level); slot order
+    // inside a level.
+    const int64_t nchunks = (nv + k - 1) / k;
+    std::vector<int32_t> chunk_levels(nchunks, 0);
+    for (int64_t v = 0; v < nv; ++v)
+      if (level[v] >= 0) chunk_levels[v / k] = std::max(chunk_levels[v / k], level[v] + 1);
+    out.chunk_lvl.assign(nchunks + 1, 0);
+    for (int64_t c = 0; c < nchunks; ++c) out.chunk_lvl[c + 1] = out.chunk_lvl[c] + chunk_levels[c];
+    const int64_t total_lv = out.chunk_lvl[nchunks];
+    std::vector<int64_t> cnt(total_lv + 1, 0);
+    for (int64_t s = 0; s < nv; ++s) {
+      const int64_t v = hm.order[s];
+      if (level[v] >= 0) ++cnt[out.chunk_lvl[v / k] + level[v] + 1];
+    }
+    for (int64_t i = 0; i < total_lv; ++i) cnt[i + 1] += cnt[i];
+    out.lvl_off.assign(cnt.begin(), cnt.end());
+    out.cb_order.assign(cnt[total_lv], 0);
+    std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
+    for (int64_t s = 0; s < nv; ++s) {
+      const int64_t v = hm.order[s];
+      if (level[v] >= 0) out.cb_order[fillp[out.chunk_lvl[v / k] + level[v]]++] = static_cast<int32_t>(s);
+    }
+    out.max_chunk_work = 0;
+    for (int64_t c = 0; c < nchunks; ++c)
+      out.max_chunk_work = std::max<int64_t>(out.max_chunk_work, cnt[out.chunk_lvl[c + 1]] - cnt[out.chunk_lvl[c]]);
+  }
   out.levels.resize(nlev);
   for (int32_t L = 0; L < nlev; ++L) {
     Phase& ph = out.levels[L];

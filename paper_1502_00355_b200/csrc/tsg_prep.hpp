@@ -80,6 +80,13 @@ struct FormBSchedule {
   std::vector<int32_t> medium;      // medium-tier slots grouped by level
   std::vector<int32_t> hubs;        // hub slots grouped by level
   std::vector<Phase> levels;
+  // Chunk schedule (one CTA per chunk, levels in order inside the CTA): the movable slots
+  // sorted by (chunk, level, slot); chunk c owns levels chunk_lvl[c] .. chunk_lvl[c+1]-1 of
+  // lvl_off, level entries lvl_off[i] .. lvl_off[i+1]-1 of cb_order.
+  std::vector<int32_t> cb_order;
+  std::vector<int32_t> lvl_off;
+  std::vector<int32_t> chunk_lvl;
+  int64_t max_chunk_work = 0;  // most movable vertices in one chunk
 };
 
 // Returns "" on success, else an error message.

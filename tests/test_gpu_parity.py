@@ -142,6 +142,25 @@ def test_single_fan_hub_beyond_shared_memory(capi, gpu_ctx, ts, port, n):
         dm.free()
 
 
+@pytest.mark.parametrize("mode", ["levels", "chunks"])
+@pytest.mark.parametrize("case", [("grid", (30, 40, 0.3, 2), 1), ("delaunay", (12000, 9), 7),
+                                  ("delaunay", (12000, 9), 300)])
+def test_form_b_schedules_vs_oracle(capi, gpu_ctx, ts, port, mode, case):
+    """Both Form B schedules (a launch per dependency level / one CTA per chunk walking its
+    levels) reproduce the reference bit for bit, both strategies."""
+    kind, args, chunks = case
+    xy, tri = ts.grid_arrays(*args) if kind == "grid" else ts.delaunay_arrays(*args)
+    want = port.smooth(xy, tri, form="b", chunks=chunks, max_iters=25, move_tol=0.0)
+    for strategy, layout in (("fused", "aos"), ("twophase", "soa")):
+        topo = ts.topology(len(xy), tri)
+        dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, layout=layout)
+        dm.formb_schedule(mode)
+        got = dm.smooth(capi.make_cfg(form="b", strategy=strategy, chunks=chunks, max_iters=25, move_tol=0.0))
+        assert np.array_equal(got["accepted"], want.accepted)
+        assert np.array_equal(dm.get_coords().view(np.uint64), want.xy.view(np.uint64))
+        dm.free()
+
+
 @pytest.mark.parametrize("seed", [0, 1])
 def test_mixed_orientation_and_bowtie_links_vs_oracle(capi, gpu_ctx, ts, port, seed):
     """Vertices whose link is not one directed cycle (flipped triangles, a bow-tie vertex shared by
