@@ -46,7 +46,9 @@ constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
 constexpr int kTileRecCap = 12288;  // ... row words staged in shared memory (multiple of 4)
-constexpr int64_t kFormBChunkWidth = 4096;  // Form B: chunk kernel below this mean level width
+constexpr int64_t kFormBChunkWidth = 4096;
+// formb_chunk_update: record double buffer + per-thread pass-start / view rings (f64 pairs)
+constexpr int kChunkRecSmem = 2 * 256 * tsg::kChunkRecWords * 4 + 2 * tsg::kChunkRecMaxDeg * 256 * 16;  // Form B: chunk kernel below this mean level width
 constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
@@ -386,6 +388,7 @@ struct tsg_mesh {
   int32_t *d_fb_nodes = nullptr, *d_fb_hubs = nullptr, *d_fb_medium = nullptr;  // level-set schedule
   std::vector<tsg::Phase> fb_levels;
   int32_t *d_cb_order = nullptr, *d_cb_lvl = nullptr, *d_cb_chunk = nullptr;  // chunk schedule
+  uint32_t* d_cb_rec = nullptr;
   int64_t fb_nchunks = 0;
   bool fb_use_chunks = false;  // narrow levels: one CTA per chunk instead of a launch per level
   int32_t fb_mode = TSG_FORMB_AUTO;
@@ -410,7 +413,9 @@ void free_form_b(tsg_mesh* m) {
   cudaFree(m->d_cb_order);
   cudaFree(m->d_cb_lvl);
   cudaFree(m->d_cb_chunk);
+  cudaFree(m->d_cb_rec);
   m->d_cb_order = m->d_cb_lvl = m->d_cb_chunk = nullptr;
+  m->d_cb_rec = nullptr;
   m->d_nbr_fresh = nullptr;
   m->bytes -= m->fb_bytes;
   m->fb_bytes = 0;
@@ -435,6 +440,7 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   if ((st = upload(&m->d_cb_order, sch.cb_order, &b, s))) return st;
   if ((st = upload(&m->d_cb_lvl, sch.lvl_off, &b, s))) return st;
   if ((st = upload(&m->d_cb_chunk, sch.chunk_lvl, &b, s))) return st;
+  if ((st = upload(&m->d_cb_rec, sch.cb_rec, &b, s))) return st;
   TSG_CUDA(cudaStreamSynchronize(s));
   m->fb_nchunks = static_cast<int64_t>(sch.chunk_lvl.size()) - 1;
   {
@@ -655,8 +661,8 @@ struct Engine {
       if (st) return st;
     } else if (m->fb_use_chunks) {
       // Form B, both strategies (equal thresholds): one CTA per chunk.
-      tsg::formb_chunk_update<R, kSoA><<<static_cast<unsigned>(m->fb_nchunks), 256, 0, s>>>(
-          base, m->d_cb_order, m->d_cb_lvl, m->d_cb_chunk);
+      tsg::formb_chunk_update<R, kSoA><<<static_cast<unsigned>(m->fb_nchunks), 256, kChunkRecSmem, s>>>(
+          base, m->d_cb_order, m->d_cb_lvl, m->d_cb_chunk, m->d_cb_rec);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     } else {
@@ -702,6 +708,8 @@ struct Engine {
 
   // Opt-in shared memory for the hub kernels (done outside any stream capture).
   static tsg_status prepare(tsg_mesh* m) {
+    TSG_CUDA(cudaFuncSetAttribute(tsg::formb_chunk_update<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kChunkRecSmem));
     TSG_CUDA(cudaFuncSetAttribute(tsg::hub_fast_update<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(hub_fast_cap(m) * sizeof(R2))));
     {

@@ -908,10 +908,14 @@ __device__ __forceinline__ R rot_fast(typename Arith<R>::R2 qa, typename Arith<R
 template <typename R, bool kSoA>
 __global__ void __launch_bounds__(256) formb_chunk_update(PassArgs<R, kSoA> a, const int32_t* __restrict__ order,
                                                           const int32_t* __restrict__ lvl_off,
-                                                          const int32_t* __restrict__ chunk_lvl) {
+                                                          const int32_t* __restrict__ chunk_lvl,
+                                                          const uint32_t* __restrict__ rec) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr bool kExact = sizeof(R) == 8;
+  constexpr int kRecMaxDeg = 15, kRecWords = 32;
+  extern __shared__ __align__(16) uint32_t rbuf[];  // [2][blockDim.x][kRecWords], then the rings
+  R2* ring = reinterpret_cast<R2*>(rbuf + 2 * blockDim.x * kRecWords);  // [2 * kRecMaxDeg][blockDim.x]
   const int2 state = *reinterpret_cast<const int2*>(a.st);
   if (state.y) return;
   Coords<R, kSoA> P, N;
@@ -920,81 +924,203 @@ __global__ void __launch_bounds__(256) formb_chunk_update(PassArgs<R, kSoA> a, c
   const bool xonly = exact_only(a.maxabs);
   int accepted = 0;
   double disp = 0.0;
+  const int tid = threadIdx.x;
+
+  // One vertex: row / fan entries through the accessors (staged record or global rows).
+  auto update = [&](int64_t s, int deg, auto nbr_at, auto fan_at) {
+    auto view = [&](uint32_t u) -> R2 { return (u & kFreshBit) ? N.load_mut(u & ~kFreshBit) : P.load(u); };
+    const R2 pv = P.load(s);
+    R sx = R(0), sy = R(0);
+    for (int j = 0; j < deg; ++j) {  // neighbor_mean through the view (smoothing.hpp:72-80)
+      const R2 c = view(nbr_at(j));
+      sx = O::add(sx, c.x);
+      sy = O::add(sy, c.y);
+    }
+    const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
+    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+    for (int j = 0; j < deg; ++j) {
+      const uint32_t f = fan_at(j);
+      const uint32_t ua = nbr_at(fan_i1(f)), ub = nbr_at(fan_i2(f));
+      const R2 pa = P.load(ua & ~kFreshBit), pb = P.load(ub & ~kFreshBit);
+      const R2 va = (ua & kFreshBit) ? N.load_mut(ua & ~kFreshBit) : pa;
+      const R2 vb = (ub & kFreshBit) ? N.load_mut(ub & ~kFreshBit) : pb;
+      R tp = rot_fast<R>(pa, pb, pv), tc = rot_fast<R>(va, vb, cand);
+      if constexpr (!kExact) {
+        tp = isfinite(tp) ? tp : R(0);
+        tc = isfinite(tc) ? tc : R(0);
+      }
+      nan_acc = fma(tp, tc, nan_acc);
+      thr = min_ref(thr, tp);
+      hyp = min_ref(hyp, tc);
+    }
+    const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
+    bool acc;
+    if constexpr (!kExact) {
+      acc = hyp > thr;
+    } else if (!bad && hyp > thr + R(kGuardCycle)) {
+      acc = true;
+    } else if (!bad && hyp < thr - R(kGuardCycle)) {
+      acc = false;
+    } else {
+      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = fan_at(j);
+        const uint32_t ua = nbr_at(fan_i1(f)), ub = nbr_at(fan_i2(f));
+        const int k = fan_k(f);
+        {
+          const R2 qa = P.load(ua & ~kFreshBit), qb = P.load(ub & ~kFreshBit);
+          const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+          thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
+                                             O::mul(daby, daby)));
+        }
+        {
+          const R2 qa = view(ua), qb = view(ub);
+          const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+          hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby,
+                                             O::mul(dabx, dabx), O::mul(daby, daby)));
+        }
+      }
+      acc = hyp_e > thr_e;
+    }
+    N.store(s, acc ? cand : pv);
+    if (acc) {
+      ++accepted;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      disp = d > disp ? d : disp;
+    }
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+  };
+  // The same decision from staged coordinates: sp / sv = pass-start / view value of row entry j
+  // at [j * blockDim.x], fan records from the record.
+  auto update_staged = [&](int64_t s, int deg, const R2* sp, const R2* sv, const uint32_t* fan) {
+    const int bs = static_cast<int>(blockDim.x);
+    const R2 pv = P.load(s);
+    R sx = R(0), sy = R(0);
+    for (int j = 0; j < deg; ++j) {
+      const R2 c = sv[j * bs];
+      sx = O::add(sx, c.x);
+      sy = O::add(sy, c.y);
+    }
+    const R inv = inv_deg<R>(deg);
+    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+    for (int j = 0; j < deg; ++j) {
+      const uint32_t f = fan[j];
+      const int ia = static_cast<int>(fan_i1(f)) * bs, ib = static_cast<int>(fan_i2(f)) * bs;
+      R tp = rot_fast<R>(sp[ia], sp[ib], pv), tc = rot_fast<R>(sv[ia], sv[ib], cand);
+      if constexpr (!kExact) {
+        tp = isfinite(tp) ? tp : R(0);
+        tc = isfinite(tc) ? tc : R(0);
+      }
+      nan_acc = fma(tp, tc, nan_acc);
+      thr = min_ref(thr, tp);
+      hyp = min_ref(hyp, tc);
+    }
+    const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
+    bool acc;
+    if constexpr (!kExact) {
+      acc = hyp > thr;
+    } else if (!bad && hyp > thr + R(kGuardCycle)) {
+      acc = true;
+    } else if (!bad && hyp < thr - R(kGuardCycle)) {
+      acc = false;
+    } else {
+      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+      for (int j = 0; j < deg; ++j) {
+        const uint32_t f = fan[j];
+        const int ia = static_cast<int>(fan_i1(f)) * bs, ib = static_cast<int>(fan_i2(f)) * bs;
+        const int k = fan_k(f);
+        {
+          const R2 qa = sp[ia], qb = sp[ib];
+          const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+          thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
+                                             O::mul(daby, daby)));
+        }
+        {
+          const R2 qa = sv[ia], qb = sv[ib];
+          const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+          hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby,
+                                             O::mul(dabx, dabx), O::mul(daby, daby)));
+        }
+      }
+      acc = hyp_e > thr_e;
+    }
+    N.store(s, acc ? cand : pv);
+    if (acc) {
+      ++accepted;
+      const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
+      const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
+      disp = d > disp ? d : disp;
+    }
+    if (a.decision) a.decision[s] = acc ? 1 : 0;
+  };
+  auto update_global = [&](int64_t s) {
+    const uint32_t o0 = __ldg(a.off + s);
+    const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
+    const uint32_t* nb = a.nbr + o0;
+    const uint32_t* fan = a.fan + o0;
+    update(s, deg, [&](int j) { return __ldg(nb + j); }, [&](int j) { return __ldg(fan + j); });
+  };
+
+  // The record of the first vertex of each level this thread handles is prefetched one level
+  // ahead (asynchronous copies into a double buffer), so only the coordinate reads of a level
+  // sit on the level's critical path (narrow levels: serial Form B on small meshes).
   const int l0 = chunk_lvl[blockIdx.x], l1 = chunk_lvl[blockIdx.x + 1];
+  auto prefetch = [&](int L) {
+    if (L < l1) {
+      const int idx = lvl_off[L] + tid;
+      if (idx < lvl_off[L + 1]) {
+        uint32_t* dst = rbuf + ((L & 1) * blockDim.x + tid) * kRecWords;
+        const uint32_t* src = rec + static_cast<int64_t>(idx) * kRecWords;
+#pragma unroll
+        for (int q = 0; q < kRecWords / 4; ++q) cp_async<16>(dst + 4 * q, src + 4 * q);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch(l0);
 #pragma unroll 1
   for (int L = l0; L < l1; ++L) {
+    prefetch(L + 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this level's record has landed
     const int b = lvl_off[L], e = lvl_off[L + 1];
-#pragma unroll 1
-    for (int idx = b + threadIdx.x; idx < e; idx += blockDim.x) {
-      const int64_t s = order[idx];
-      const uint32_t o0 = __ldg(a.off + s);
-      const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
-      const uint32_t* nb = a.nbr + o0;
-      const uint32_t* fan = a.fan + o0;
-      auto view = [&](uint32_t u) -> R2 { return (u & kFreshBit) ? N.load_mut(u & ~kFreshBit) : P.load(u); };
-      const R2 pv = P.load(s);
-      R sx = R(0), sy = R(0);
-      for (int j = 0; j < deg; ++j) {  // neighbor_mean through the view (smoothing.hpp:72-80)
-        const R2 c = view(__ldg(nb + j));
-        sx = O::add(sx, c.x);
-        sy = O::add(sy, c.y);
-      }
-      const R inv = deg <= kMaxInvDeg ? inv_deg<R>(deg) : O::div(R(1), static_cast<R>(deg));
-      const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-      R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
-      for (int j = 0; j < deg; ++j) {
-        const uint32_t f = __ldg(fan + j);
-        const uint32_t ua = __ldg(nb + fan_i1(f)), ub = __ldg(nb + fan_i2(f));
-        const R2 pa = P.load(ua & ~kFreshBit), pb = P.load(ub & ~kFreshBit);
-        const R2 va = (ua & kFreshBit) ? N.load_mut(ua & ~kFreshBit) : pa;
-        const R2 vb = (ub & kFreshBit) ? N.load_mut(ub & ~kFreshBit) : pb;
-        R tp = rot_fast<R>(pa, pb, pv), tc = rot_fast<R>(va, vb, cand);
-        if constexpr (!kExact) {
-          tp = isfinite(tp) ? tp : R(0);
-          tc = isfinite(tc) ? tc : R(0);
+    if (b + tid < e) {
+      const uint32_t* r = rbuf + ((L & 1) * blockDim.x + tid) * kRecWords;
+      const int deg = static_cast<int>(r[1]);
+      if (deg <= kRecMaxDeg) {
+        // All neighbour coordinates of the vertex in one batch of independent loads (pass-start
+        // and view values) into this thread's slices, then the arithmetic from shared memory.
+        R2* sp = ring + tid;                    // entry j at sp[j * blockDim.x]
+        R2* sv = ring + kRecMaxDeg * blockDim.x + tid;
+#pragma unroll
+        for (int base = 0; base < kRecMaxDeg; base += 8) {
+          if (base < deg) {
+            R2 cp[8], cv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (base + j < deg) {
+                const uint32_t u = r[2 + base + j];
+                cp[j] = P.load(u & ~kFreshBit);
+                cv[j] = (u & kFreshBit) ? N.load_mut(u & ~kFreshBit) : cp[j];
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (base + j < deg) {
+                sp[(base + j) * blockDim.x] = cp[j];
+                sv[(base + j) * blockDim.x] = cv[j];
+              }
+          }
         }
-        nan_acc = fma(tp, tc, nan_acc);
-        thr = min_ref(thr, tp);
-        hyp = min_ref(hyp, tc);
-      }
-      const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
-      bool acc;
-      if constexpr (!kExact) {
-        acc = hyp > thr;
-      } else if (!bad && hyp > thr + R(kGuardCycle)) {
-        acc = true;
-      } else if (!bad && hyp < thr - R(kGuardCycle)) {
-        acc = false;
+        update_staged(static_cast<int64_t>(r[0]), deg, sp, sv, r + 2 + kRecMaxDeg);
       } else {
-        R thr_e = R(INFINITY), hyp_e = R(INFINITY);
-        for (int j = 0; j < deg; ++j) {
-          const uint32_t f = __ldg(fan + j);
-          const uint32_t ua = __ldg(nb + fan_i1(f)), ub = __ldg(nb + fan_i2(f));
-          const int k = fan_k(f);
-          {
-            const R2 qa = P.load(ua & ~kFreshBit), qb = P.load(ub & ~kFreshBit);
-            const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
-            thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
-                                               O::mul(daby, daby)));
-          }
-          {
-            const R2 qa = view(ua), qb = view(ub);
-            const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
-            hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby,
-                                               O::mul(dabx, dabx), O::mul(daby, daby)));
-          }
-        }
-        acc = hyp_e > thr_e;
+        update_global(static_cast<int64_t>(r[0]));
       }
-      N.store(s, acc ? cand : pv);
-      if (acc) {
-        ++accepted;
-        const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
-        const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-        disp = d > disp ? d : disp;
-      }
-      if (a.decision) a.decision[s] = acc ? 1 : 0;
     }
+#pragma unroll 1
+    for (int idx = b + tid + static_cast<int>(blockDim.x); idx < e; idx += blockDim.x) update_global(order[idx]);
     __syncthreads();  // this level's N writes are read by the next levels of the chunk
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);

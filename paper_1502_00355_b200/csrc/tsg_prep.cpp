@@ -476,6 +476,19 @@ std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers,
       const int64_t v = hm.order[s];
       if (level[v] >= 0) out.cb_order[fillp[out.chunk_lvl[v / k] + level[v]]++] = static_cast<int32_t>(s);
     }
+    out.cb_rec.assign(out.cb_order.size() * kChunkRecWords, 0);
+    for (size_t p = 0; p < out.cb_order.size(); ++p) {
+      const int64_t s = out.cb_order[p];
+      const uint32_t o0 = hm.off[s], n = hm.off[s + 1] - o0;
+      uint32_t* r = out.cb_rec.data() + p * kChunkRecWords;
+      r[0] = static_cast<uint32_t>(s);
+      r[1] = n;
+      if (n <= static_cast<uint32_t>(kChunkRecMaxDeg))
+        for (uint32_t j = 0; j < n; ++j) {
+          r[2 + j] = out.nbr_fresh[o0 + j];
+          r[2 + kChunkRecMaxDeg + j] = hm.fan[o0 + j];
+        }
+    }
     out.max_chunk_work = 0;
     for (int64_t c = 0; c < nchunks; ++c)
       out.max_chunk_work = std::max<int64_t>(out.max_chunk_work, cnt[out.chunk_lvl[c + 1]] - cnt[out.chunk_lvl[c]]);

@@ -87,7 +87,12 @@ struct FormBSchedule {
   std::vector<int32_t> lvl_off;
   std::vector<int32_t> chunk_lvl;
   int64_t max_chunk_work = 0;  // most movable vertices in one chunk
+  // Per entry of cb_order a kChunkRecWords-word record: slot, valence, then (valence <=
+  // kChunkRecMaxDeg) the row's neighbour slots (with kFreshBit) and its fan records.
+  std::vector<uint32_t> cb_rec;
 };
+constexpr int kChunkRecWords = 32;
+constexpr int kChunkRecMaxDeg = 15;
 
 // Returns "" on success, else an error message.
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
