@@ -142,6 +142,14 @@ tsg_status tsg_smooth(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, tsg_smooth_stat
 tsg_status tsg_smooth_host(tsg_mesh* mesh, const double* xy_in, const tsg_smooth_cfg* cfg,
                            double* xy_out, tsg_smooth_stats* stats, int32_t* accepted_per_pass,
                            double* max_disp_per_pass, int32_t capacity);
+/* Smooths n coordinate sets of the same mesh end to end: xy_in[k] (host, original order; pinned
+ * memory for asynchronous copies) -> cfg passes -> xy_out[k], with the host->device copy of item
+ * k+1 and the device->host copy of item k-1 overlapping the passes of item k (copy engines on
+ * their own streams, two device staging slots).  Graph driver only; per-item passes executed and
+ * TSG_STOP_* in iterations_out / stop_out (may be NULL).  Leaves the device coordinates of the
+ * last item current (the restore point of tsg_mesh_restore_coords is unchanged). */
+tsg_status tsg_smooth_host_batch(tsg_mesh* mesh, int32_t n, const double* const* xy_in, const tsg_smooth_cfg* cfg,
+                                 double* const* xy_out, int32_t* iterations_out, int32_t* stop_out);
 
 /*
  * One pass in lockstep from the current device state, without the stop rule; writes the

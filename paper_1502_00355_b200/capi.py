@@ -31,7 +31,7 @@ EXPORTS = (
     "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_mesh_restore_coords",
     "tsg_tri_alpha",
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
-    "tsg_pass_lockstep", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
+    "tsg_pass_lockstep", "tsg_smooth_host_batch", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
     "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
 )
@@ -84,6 +84,7 @@ def lib() -> C.CDLL:
             "tsg_smooth": (i32, [P, C.POINTER(SmoothCfg), C.POINTER(SmoothStats), P, P, i32]),
             "tsg_smooth_host": (i32, [P, P, C.POINTER(SmoothCfg), P, C.POINTER(SmoothStats), P, P, i32]),
             "tsg_pass_lockstep": (i32, [P, i32, i32, P, P, P]),
+            "tsg_smooth_host_batch": (i32, [P, i32, P, C.POINTER(SmoothCfg), P, P, P]),
             "tsg_hilbert_order": (i32, [i64, P, P]),
             "tsg_selftest_alpha": (i32, [P, i64, C.c_uint64, i32, P, P]),
             "tsg_selftest_alpha_cycle": (i32, [P, i64, C.c_uint64, P, P]),
@@ -248,6 +249,22 @@ class DeviceMesh:
         it = st.iterations
         return xy_out, dict(iterations=it, stop=STOP[st.stop], accepted=acc[:it], max_disp=md[:it],
                             device_ms=st.device_ms, launches=st.launches)
+
+    def smooth_host_batch(self, xy_ins, cfg: SmoothCfg, xy_outs):
+        """tsg_smooth_host_batch: smooths every coordinate set of `xy_ins` (host arrays, ideally
+        pinned) into the matching array of `xy_outs`, copies overlapped with the passes.
+        Returns (iterations, stop names) per item."""
+        n = len(xy_ins)
+        assert len(xy_outs) == n
+        for a in list(xy_ins) + list(xy_outs):
+            assert a.dtype == np.float64 and a.flags.c_contiguous and a.shape == (self.nv, 2)
+        ins = (C.c_void_p * max(1, n))(*[a.ctypes.data for a in xy_ins])
+        outs = (C.c_void_p * max(1, n))(*[a.ctypes.data for a in xy_outs])
+        it = np.zeros(max(1, n), dtype=np.int32)
+        stop = np.zeros(max(1, n), dtype=np.int32)
+        check(lib().tsg_smooth_host_batch(self.h, n, ins, C.byref(cfg), outs, _ptr(it), _ptr(stop)),
+              "tsg_smooth_host_batch")
+        return it[:n].copy(), [STOP[x] for x in stop[:n]]
 
     def pass_lockstep(self, form="a", chunks=1):
         dec = np.empty(self.nv, dtype=np.int8)

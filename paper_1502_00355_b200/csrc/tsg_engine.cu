@@ -117,6 +117,22 @@ __global__ void coords_to_orig(tsg::Coords<R, kSoA> b, const int64_t* __restrict
   }
 }
 
+// Current coordinates -> original-order f64 pairs, the current buffer chosen on the device
+// from the pass counter (ping-pong: the last pass wrote buffer (pass & 1) ? buf1 : buf0).
+template <typename R, bool kSoA>
+__global__ void coords_to_orig_parity(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1, int32_t swap,
+                                      const tsg::PassState* st, const int64_t* __restrict__ order, int64_t nv,
+                                      double* __restrict__ xy) {
+  const tsg::Coords<R, kSoA> b = (swap == tsg::kSwapPingPong && (st->pass & 1)) ? b1 : b0;
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = order ? order[s] : s;
+    const auto p = b.load_mut(s);
+    xy[2 * v] = static_cast<double>(p.x);
+    xy[2 * v + 1] = static_cast<double>(p.y);
+  }
+}
+
 template <typename R>
 __global__ void to_double_scatter(const R* __restrict__ in, const int64_t* __restrict__ order,
                                   int64_t n, double* __restrict__ out) {
@@ -346,6 +362,8 @@ struct tsg_context {
   // Side stream for the medium / hub tiers, forked from and joined back into `stream` so
   // the tiers of one pass (or one Form B level) run concurrently (also inside graphs).
   cudaStream_t side = nullptr;
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;  // tsg_smooth_host_batch
+  cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
   std::vector<cudaEvent_t> fork_events;
   size_t fork_next = 0;
 };
@@ -368,6 +386,10 @@ struct tsg_mesh {
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   void* d_alpha = nullptr;
   double* d_xy_stage = nullptr;  // 2*nv original-order doubles
+  double* d_batch_in[2] = {nullptr, nullptr};   // tsg_smooth_host_batch staging (lazy)
+  double* d_batch_out[2] = {nullptr, nullptr};
+  tsg::PassState* h_batch_state = nullptr;      // pinned, per batch item
+  int32_t h_batch_cap = 0;
   double* d_vmin = nullptr;
   int8_t *d_decision = nullptr, *d_decision_orig = nullptr;
   tsg::PassState* d_state = nullptr;
@@ -765,6 +787,26 @@ struct Engine {
   }
 
   // Current coordinates into buf0 (both buffers equal afterwards for pinned vertices anyway).
+  // Batch: staged original-order input -> both buffers (on the context stream).
+  static tsg_status batch_load(tsg_mesh* m, const double* stage) {
+    cudaStream_t s = m->ctx->stream;
+    const int64_t nv = m->hm.nv;
+    TSG_CUDA(cudaMemsetAsync(m->d_maxabs, 0, sizeof(unsigned long long), s));
+    coords_from_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(stage, m->d_order, nv, coords_of<R, kSoA>(m, 0),
+                                                                coords_of<R, kSoA>(m, 1), m->d_maxabs);
+    TSG_CUDA(cudaGetLastError());
+    m->cur = 0;
+    return TSG_OK;
+  }
+  static tsg_status batch_store(tsg_mesh* m, int32_t swap, double* stage) {
+    cudaStream_t s = m->ctx->stream;
+    const int64_t nv = m->hm.nv;
+    coords_to_orig_parity<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1),
+                                                                     swap, m->d_state, m->d_order, nv, stage);
+    TSG_CUDA(cudaGetLastError());
+    return TSG_OK;
+  }
+
   static tsg_status normalize(tsg_mesh* m) {
     if (m->cur != 0) {
       TSG_CUDA(cudaMemcpyAsync(m->buf[0], m->buf[1], 2 * m->hm.nv * sizeof(R), cudaMemcpyDeviceToDevice,
@@ -861,6 +903,11 @@ tsg_status tsg_context_create(int32_t device, tsg_context** out) {
   TSG_CUDA(cudaEventCreate(&ctx->ev0));
   TSG_CUDA(cudaEventCreate(&ctx->ev1));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  TSG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+  TSG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t* e : {&ctx->ev_in_ready[b], &ctx->ev_in_free[b], &ctx->ev_out_ready[b], &ctx->ev_out_free[b]})
+      TSG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   *out = ctx.release();
   return TSG_OK;
 }
@@ -873,6 +920,11 @@ tsg_status tsg_context_destroy(tsg_context* ctx) {
   cudaEventDestroy(ctx->ev1);
   for (cudaEvent_t e : ctx->fork_events) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->side);
+  cudaStreamDestroy(ctx->copy_in);
+  cudaStreamDestroy(ctx->copy_out);
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t e : {ctx->ev_in_ready[b], ctx->ev_in_free[b], ctx->ev_out_ready[b], ctx->ev_out_free[b]})
+      cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TSG_OK;
@@ -999,6 +1051,11 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
   for (void* p : ptrs) cudaFree(p);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(m->d_batch_in[b]);
+    cudaFree(m->d_batch_out[b]);
+  }
+  cudaFreeHost(m->h_batch_state);
   delete m;
   return TSG_OK;
 }
@@ -1112,6 +1169,65 @@ tsg_status tsg_alpha_extrema(tsg_mesh* m, double* min_out, double* max_out, int6
   return TSG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Resets the pass state and enqueues a whole smooth() as one launch of the cached
+// conditional-WHILE graph on the context stream (no synchronisation).
+tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* kernels_per_pass) {
+  tsg_context* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  tsg_status st;
+  if (c->form == TSG_FORM_B && (st = ensure_form_b(m, c->chunks))) return st;
+  if ((st = ensure_stats_capacity(m, c->max_iters))) return st;
+  const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
+  TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
+  TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * c->max_iters, s));
+  TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
+  GraphCache& g = m->gc;
+  if (!(g.valid && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
+        g.swap == c->swap && g.max_iters == c->max_iters && g.tol_abs == tol_abs)) {
+    g.reset();
+    TSG_CUDA(cudaGraphCreate(&g.graph, 0));
+    cudaGraphConditionalHandle h;
+    TSG_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    TSG_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    TSG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    int64_t k = 0;
+    st = dispatch(m, [&](auto E) {
+      return decltype(E)::enqueue_pass(m, *c, s, tol_abs, h, 1, nullptr, nullptr, nullptr, &k);
+    });
+    cudaGraph_t captured = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &captured);
+    if (st) return st;
+    if (e != cudaSuccess) return fail(TSG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+    TSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+    g.valid = true;
+    g.form = c->form;
+    g.strategy = c->strategy;
+    g.chunks = c->chunks;
+    g.swap = c->swap;
+    g.max_iters = c->max_iters;
+    g.tol_abs = tol_abs;
+    g.kernels_per_pass = k;
+  }
+  *kernels_per_pass = g.kernels_per_pass;
+  TSG_CUDA(cudaGraphLaunch(g.exec, s));
+  return TSG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* stats,
                       int32_t* accepted_per_pass, double* max_disp_per_pass, int32_t capacity) {
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
@@ -1134,43 +1250,8 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   double node_ms = -1.0;
   int64_t launches = 0;
   if (c->driver == TSG_DRIVER_GRAPH) {
-    GraphCache& g = m->gc;
-    if (!(g.valid && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
-          g.swap == c->swap && g.max_iters == c->max_iters && g.tol_abs == tol_abs)) {
-      g.reset();
-      TSG_CUDA(cudaGraphCreate(&g.graph, 0));
-      cudaGraphConditionalHandle h;
-      TSG_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, 1, cudaGraphCondAssignDefault));
-      cudaGraphNodeParams cp = {};
-      cp.type = cudaGraphNodeTypeConditional;
-      cp.conditional.handle = h;
-      cp.conditional.type = cudaGraphCondTypeWhile;
-      cp.conditional.size = 1;
-      cudaGraphNode_t node;
-      TSG_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
-      cudaGraph_t body = cp.conditional.phGraph_out[0];
-      TSG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-      int64_t k = 0;
-      st = dispatch(m, [&](auto E) {
-        return decltype(E)::enqueue_pass(m, *c, s, tol_abs, h, 1, nullptr, nullptr, nullptr, &k);
-      });
-      cudaGraph_t captured = nullptr;
-      cudaError_t e = cudaStreamEndCapture(s, &captured);
-      if (st) return st;
-      if (e != cudaSuccess) return fail(TSG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
-      TSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
-      g.valid = true;
-      g.form = c->form;
-      g.strategy = c->strategy;
-      g.chunks = c->chunks;
-      g.swap = c->swap;
-      g.max_iters = c->max_iters;
-      g.tol_abs = tol_abs;
-      g.kernels_per_pass = k;
-    }
-    kernels_per_pass = g.kernels_per_pass;
     TSG_CUDA(cudaEventRecord(ctx->ev0, s));
-    TSG_CUDA(cudaGraphLaunch(g.exec, s));
+    if ((st = smooth_enqueue_graph(m, c, &kernels_per_pass))) return st;
     TSG_CUDA(cudaEventRecord(ctx->ev1, s));
   } else {
     // Plain launches; kernels early-exit once done is set.  Per-pass events bracket the
@@ -1251,6 +1332,61 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
     stats->node_kernel_ms = node_ms;
     stats->launches = c->driver == TSG_DRIVER_GRAPH ? kernels_per_pass * it : launches;
   }
+  return TSG_OK;
+}
+
+tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy_in, const tsg_smooth_cfg* c,
+                                 double* const* xy_out, int32_t* iterations_out, int32_t* stop_out) {
+  if (!m || n < 0 || (n > 0 && (!xy_in || !xy_out))) return fail(TSG_ERR_INVALID, "bad batch arguments");
+  tsg_status st = validate_cfg(c);
+  if (st) return st;
+  if (c->driver != TSG_DRIVER_GRAPH) return fail(TSG_ERR_INVALID, "the batch API runs the graph driver");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  tsg_context* ctx = m->ctx;
+  const int64_t nv = m->hm.nv;
+  const size_t bytes = 2 * static_cast<size_t>(nv) * sizeof(double);
+  for (int b = 0; b < 2; ++b) {
+    if (!m->d_batch_in[b]) TSG_CUDA(cudaMalloc(&m->d_batch_in[b], bytes));
+    if (!m->d_batch_out[b]) TSG_CUDA(cudaMalloc(&m->d_batch_out[b], bytes));
+  }
+  if (m->h_batch_cap < n) {
+    cudaFreeHost(m->h_batch_state);
+    m->h_batch_state = nullptr;
+    TSG_CUDA(cudaHostAlloc(&m->h_batch_state, sizeof(tsg::PassState) * n, cudaHostAllocDefault));
+    m->h_batch_cap = n;
+  }
+  cudaStream_t s = ctx->stream;
+  // Item k uses staging slot k & 1.  copy_in: H2D (after the slot's previous input was
+  // consumed); compute: reorder in, smooth graph, reorder out (after the slot's previous output
+  // was copied out), pass state -> pinned host; copy_out: D2H.  Copies of items k-1 / k+1 overlap
+  // the passes of item k.
+  for (int32_t k = 0; k < n; ++k) {
+    const int b = k & 1;
+    if (k >= 2) TSG_CUDA(cudaStreamWaitEvent(ctx->copy_in, ctx->ev_in_free[b], 0));
+    TSG_CUDA(cudaMemcpyAsync(m->d_batch_in[b], xy_in[k], bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+    TSG_CUDA(cudaEventRecord(ctx->ev_in_ready[b], ctx->copy_in));
+    TSG_CUDA(cudaStreamWaitEvent(s, ctx->ev_in_ready[b], 0));
+    st = dispatch(m, [&](auto E) { return decltype(E)::batch_load(m, m->d_batch_in[b]); });
+    if (st) return st;
+    TSG_CUDA(cudaEventRecord(ctx->ev_in_free[b], s));
+    int64_t kpp = 0;
+    if ((st = smooth_enqueue_graph(m, c, &kpp))) return st;
+    if (k >= 2) TSG_CUDA(cudaStreamWaitEvent(s, ctx->ev_out_free[b], 0));
+    st = dispatch(m, [&](auto E) { return decltype(E)::batch_store(m, c->swap, m->d_batch_out[b]); });
+    if (st) return st;
+    TSG_CUDA(cudaMemcpyAsync(m->h_batch_state + k, m->d_state, sizeof(tsg::PassState), cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaEventRecord(ctx->ev_out_ready[b], s));
+    TSG_CUDA(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_ready[b], 0));
+    TSG_CUDA(cudaMemcpyAsync(xy_out[k], m->d_batch_out[b], bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+    TSG_CUDA(cudaEventRecord(ctx->ev_out_free[b], ctx->copy_out));
+  }
+  TSG_CUDA(cudaStreamSynchronize(ctx->copy_out));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  for (int32_t k = 0; k < n; ++k) {
+    if (iterations_out) iterations_out[k] = m->h_batch_state[k].pass;
+    if (stop_out) stop_out[k] = m->h_batch_state[k].stop;
+  }
+  if (n > 0) m->cur = c->swap == TSG_SWAP_PINGPONG ? (m->h_batch_state[n - 1].pass & 1) : 0;
   return TSG_OK;
 }
 

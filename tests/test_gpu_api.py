@@ -84,3 +84,26 @@ def test_device_mesh_class_round_trip():
     assert np.array_equal(dm.get_coords(), xy)
     r = dm.run(ts.bbox_diagonal(xy), form="a", max_iters=10)
     assert r["iterations"] == 10 and len(r["max_disp_per_pass"]) == 10
+
+
+def test_smooth_host_batch_equals_single_calls(capi, gpu_ctx, ts, port):
+    """tsg_smooth_host_batch (copies overlapped with the passes, two staging slots) gives, item by
+    item, exactly what tsg_smooth_host gives; odd and even item counts, different inputs."""
+    xy, tri = ts.delaunay_arrays(7000, 21)
+    topo = ts.topology(len(xy), tri)
+    dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, order=capi.hilbert_order(xy))
+    cfg = capi.make_cfg(form="a", max_iters=30, move_tol=1e-6, bbox_diag=ts.bbox_diagonal(xy))
+    rng = np.random.default_rng(3)
+    ins = [np.ascontiguousarray(xy + rng.normal(0, 1e-4, xy.shape) * (k % 2)) for k in range(5)]
+    for n in (1, 2, 5):
+        outs = [np.empty_like(xy) for _ in range(n)]
+        its, stops = dm.smooth_host_batch(ins[:n], cfg, outs)
+        for k in range(n):
+            want, r = dm.smooth_host(ins[k], cfg)
+            assert its[k] == r["iterations"] and stops[k] == r["stop"]
+            assert np.array_equal(outs[k].view(np.uint64), want.view(np.uint64))
+    want = port.smooth(ins[0], tri, form="a", max_iters=30, move_tol=1e-6)
+    outs = [np.empty_like(xy)]
+    dm.smooth_host_batch(ins[:1], cfg, outs)
+    assert np.array_equal(outs[0].view(np.uint64), want.xy.view(np.uint64))
+    dm.free()
