@@ -154,17 +154,21 @@ __device__ __forceinline__ float rcp_cubic(float x) { return __frcp_rn(x); }
 
 // Decisions whose fast-path margin is within kGuard (absolute; |α| <= 1) are settled exactly.
 constexpr double kGuard = 0x1p-45;
-// Guard of the rotation (cycle) fast path, in α/K units.  With u = 2^-53, per triangle the fast
-// value t = ((a-v) x (b-v)) * rcp(|a-v|^2 + |b-v|^2 + |b-a|^2) (FMA, rcp_cubic reciprocal with
-// relative error <= 3u) is within 6.7u of the real τ = X/S (numerator error <= 2.01u·S,
-// denominator <= 12u·S, |τ| <= 1/K), and the reference's α/K is within 5u of τ (numerator
-// 2.01u·S, edge-square sum 8u·S, two final roundings); the minima over the fan are 1-Lipschitz,
-// so hyp - thr is known to within 2 x 11.7u = 23.4u < 2^-48.5.  kGuardCycle = 64u leaves a
-// factor 2.7; tsg_selftest_alpha_cycle measures the per-triangle error on the device (max
-// 1.95u over 2^24 random and near-degenerate triangles at 2^-30..2^30 scales).
-// Valid while every coordinate magnitude is below 2^500 (no overflow / flushed reciprocal);
-// beyond that the engine sets PassArgs::exact_only.
-constexpr double kGuardCycle = 0x1p-47;
+// Guard of the rotation (cycle) fast path, in α/K units (u = 2^-53).  With A = a - v, B = b - v,
+// C = b - a (real), X = A x B, S = |A|^2 + |B|^2 + |C|^2, τ = X / S (|τ| <= 1/K = 0.2887):
+//  * fast value t = RN(cp * rcp(es)): the numerator cp = fma(pAx, pBy, -RN(pAy pBx)) of the rounded
+//    offsets is within 3u|A||B| + u|X| <= 2uS of X; the denominator es = (lp_a + lp_b) + lab is
+//    within 7uS of S (4u per squared offset length, u(6|C|^2 + |A|^2 + |B|^2) for |b-a|^2 formed
+//    from the offsets, two additions); rcp_cubic is within 1.01u; one final product:
+//    |t - τ| <= 2u + |τ| (7u + 1.01u + u) <= 4.6u;
+//  * the reference's α/K = RN(RN(K ta) / es_r) / K (quality.hpp:15-23): ta within 2uS, es_r within
+//    8uS (six squares of rounded differences, five additions), two roundings:
+//    |α_ref/K - τ| <= 2u + 10u |τ| <= 4.9u;
+//  * minima are 1-Lipschitz, so each of thr and hyp is known to 9.5u and hyp - thr to 19u (plus
+//    0.3u for forming thr ± guard).  kGuardCycle = 2^-48 = 32u leaves a factor 1.66;
+//    tsg_selftest_alpha_cycle measures the per-triangle |t - α_ref/K| on the device (max 1.95u
+//    over 2^24 random and near-degenerate triangles at 2^-30..2^30 scales, bound 9.5u).
+constexpr double kGuardCycle = 0x1p-48;
 constexpr double kExactOnlyAbove = 0x1p500;
 
 // triangle_alpha with the division replaced by the refined reciprocal; everything before the
