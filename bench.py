@@ -49,7 +49,7 @@ CONFIGS = {
                  layout="aos", precision="f64", passes=100, move_tol=0.0, reorder=True,
                  label="graded / irregular-valence Delaunay 16M nodes (0.1% hubs, valence 32..1024), Form A"),
     "cfg4": dict(gen="grid", args=(8000, 8000, 0.3, 1), form="a", strategy="fused", chunks=1, layout="aos",
-                 precision="f64", passes=100, move_tol=0.0, reorder=False,
+                 precision="f64", passes=100, move_tol=0.0, reorder=True,
                  label="perturbed grid 8000x8000 (64M nodes), Form A, fp64"),
     "cfg5": dict(gen="delaunay", args=(256_000_000, 42), form="a", strategy="fused", chunks=1, layout="aos",
                  precision="f32", passes=100, move_tol=0.0, reorder=True,
