@@ -133,6 +133,19 @@ __global__ void coords_to_orig_parity(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kS
   }
 }
 
+__global__ void save_state(const tsg::PassState* st, tsg::PassState* out) { *out = *st; }
+
+__global__ void reset_pass_state(tsg::PassState* st, int32_t* slot_acc, unsigned long long* slot_md, int64_t n) {
+  const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i0 == 0) *st = tsg::PassState{0, 0, 0, 0};
+  for (int64_t i = i0; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    slot_acc[i] = 0;
+    slot_md[i] = 0ull;
+  }
+}
+
+__global__ void zero_u64(unsigned long long* p) { *p = 0ull; }
+
 template <typename R>
 __global__ void to_double_scatter(const R* __restrict__ in, const int64_t* __restrict__ order,
                                   int64_t n, double* __restrict__ out) {
@@ -389,6 +402,7 @@ struct tsg_mesh {
   double* d_batch_in[2] = {nullptr, nullptr};   // tsg_smooth_host_batch staging (lazy)
   double* d_batch_out[2] = {nullptr, nullptr};
   tsg::PassState* h_batch_state = nullptr;      // pinned, per batch item
+  tsg::PassState* d_batch_state = nullptr;
   int32_t h_batch_cap = 0;
   double* d_vmin = nullptr;
   int8_t *d_decision = nullptr, *d_decision_orig = nullptr;
@@ -791,7 +805,7 @@ struct Engine {
   static tsg_status batch_load(tsg_mesh* m, const double* stage) {
     cudaStream_t s = m->ctx->stream;
     const int64_t nv = m->hm.nv;
-    TSG_CUDA(cudaMemsetAsync(m->d_maxabs, 0, sizeof(unsigned long long), s));
+    zero_u64<<<1, 1, 0, s>>>(m->d_maxabs);  // (a kernel: see smooth_enqueue_graph)
     coords_from_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(stage, m->d_order, nv, coords_of<R, kSoA>(m, 0),
                                                                 coords_of<R, kSoA>(m, 1), m->d_maxabs);
     TSG_CUDA(cudaGetLastError());
@@ -1056,6 +1070,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
     cudaFree(m->d_batch_out[b]);
   }
   cudaFreeHost(m->h_batch_state);
+  cudaFree(m->d_batch_state);
   delete m;
   return TSG_OK;
 }
@@ -1182,9 +1197,11 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
   if (c->form == TSG_FORM_B && (st = ensure_form_b(m, c->chunks))) return st;
   if ((st = ensure_stats_capacity(m, c->max_iters))) return st;
   const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
-  TSG_CUDA(cudaMemsetAsync(m->d_state, 0, sizeof(tsg::PassState), s));
-  TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * c->max_iters, s));
-  TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
+  // (zeroed by a kernel: memsets may be served by a copy engine, where they would queue behind
+  // the host<->device copies tsg_smooth_host_batch overlaps with this stream)
+  reset_pass_state<<<grid_for(int64_t{tsg::kStatSlots} * c->max_iters, 256), 256, 0, s>>>(
+      m->d_state, m->d_sacc, m->d_smd, int64_t{tsg::kStatSlots} * c->max_iters);
+  TSG_CUDA(cudaGetLastError());
   GraphCache& g = m->gc;
   if (!(g.valid && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
         g.swap == c->swap && g.max_iters == c->max_iters && g.tol_abs == tol_abs)) {
@@ -1351,20 +1368,31 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
   }
   if (m->h_batch_cap < n) {
     cudaFreeHost(m->h_batch_state);
+    cudaFree(m->d_batch_state);
     m->h_batch_state = nullptr;
+    m->d_batch_state = nullptr;
     TSG_CUDA(cudaHostAlloc(&m->h_batch_state, sizeof(tsg::PassState) * n, cudaHostAllocDefault));
+    TSG_CUDA(cudaMalloc(&m->d_batch_state, sizeof(tsg::PassState) * n));
     m->h_batch_cap = n;
   }
   cudaStream_t s = ctx->stream;
-  // Item k uses staging slot k & 1.  copy_in: H2D (after the slot's previous input was
-  // consumed); compute: reorder in, smooth graph, reorder out (after the slot's previous output
-  // was copied out), pass state -> pinned host; copy_out: D2H.  Copies of items k-1 / k+1 overlap
-  // the passes of item k.
-  for (int32_t k = 0; k < n; ++k) {
+  // Item k uses staging slot k & 1.  The copy engines serve host<->device copies in issue
+  // order, so the loop issues the input copy of item k+1 BEFORE the result copy of item k:
+  //   copy_in : H2D(k+1)            (after item k-1 released the slot)
+  //   compute : reorder in (k), smooth graph (k), reorder out (k) (after item k-2's result left)
+  //   copy_out: D2H(k)
+  // H2D(k+1) then runs during the passes of item k, D2H(k) during those of item k+1.
+  auto h2d = [&](int32_t k) -> tsg_status {
     const int b = k & 1;
     if (k >= 2) TSG_CUDA(cudaStreamWaitEvent(ctx->copy_in, ctx->ev_in_free[b], 0));
     TSG_CUDA(cudaMemcpyAsync(m->d_batch_in[b], xy_in[k], bytes, cudaMemcpyHostToDevice, ctx->copy_in));
     TSG_CUDA(cudaEventRecord(ctx->ev_in_ready[b], ctx->copy_in));
+    return TSG_OK;
+  };
+  if (n > 0 && (st = h2d(0))) return st;
+  for (int32_t k = 0; k < n; ++k) {
+    const int b = k & 1;
+    if (k + 1 < n && (st = h2d(k + 1))) return st;
     TSG_CUDA(cudaStreamWaitEvent(s, ctx->ev_in_ready[b], 0));
     st = dispatch(m, [&](auto E) { return decltype(E)::batch_load(m, m->d_batch_in[b]); });
     if (st) return st;
@@ -1374,12 +1402,14 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
     if (k >= 2) TSG_CUDA(cudaStreamWaitEvent(s, ctx->ev_out_free[b], 0));
     st = dispatch(m, [&](auto E) { return decltype(E)::batch_store(m, c->swap, m->d_batch_out[b]); });
     if (st) return st;
-    TSG_CUDA(cudaMemcpyAsync(m->h_batch_state + k, m->d_state, sizeof(tsg::PassState), cudaMemcpyDeviceToHost, s));
+    save_state<<<1, 1, 0, s>>>(m->d_state, m->d_batch_state + k);
+    TSG_CUDA(cudaGetLastError());
     TSG_CUDA(cudaEventRecord(ctx->ev_out_ready[b], s));
     TSG_CUDA(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_ready[b], 0));
     TSG_CUDA(cudaMemcpyAsync(xy_out[k], m->d_batch_out[b], bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
     TSG_CUDA(cudaEventRecord(ctx->ev_out_free[b], ctx->copy_out));
   }
+  TSG_CUDA(cudaMemcpyAsync(m->h_batch_state, m->d_batch_state, sizeof(tsg::PassState) * n, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(ctx->copy_out));
   TSG_CUDA(cudaStreamSynchronize(s));
   for (int32_t k = 0; k < n; ++k) {

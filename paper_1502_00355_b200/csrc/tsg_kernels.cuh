@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
 
   // One vertex of the tile (local index i).
   auto vertex = [&](int i, uint32_t meta) {
-    const int deg = static_cast<int>((meta >> kMetaDegShift) & 15u);
+    const int deg = static_cast<int>((meta >> kMetaDegShift) & kMetaDegMask);
     const uint32_t w0 = meta & kMetaBaseMask, stride = meta >> kMetaStrideShift;
     const R2 pv = pts[i];
     // neighbor_mean (smoothing.hpp:72-80): ordered chain over row[] (ascending original id).
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
 #pragma unroll 1
   for (int i = tid; i < n_in; i += kThreads) {
     const uint32_t meta = meta_s[i];
-    if (((meta >> kMetaDegShift) & 15u) == 0) continue;  // pinned, or a medium / warp tier row
+    if (((meta >> kMetaDegShift) & kMetaDegMask) == 0) continue;  // pinned, or a row of another tier
     vertex(i, meta);
   }
   // Exact decisions of the tile's near-ties, from the staged tile, one warp per vertex (lane j
@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   for (int e = tid >> 5; e < qn; e += kThreads / 32) {
     const int i = q_s[e];
     const uint32_t meta = meta_s[i];
-    const int deg = static_cast<int>((meta >> kMetaDegShift) & 15u);
+    const int deg = static_cast<int>((meta >> kMetaDegShift) & kMetaDegMask);
     const uint32_t w0 = meta & kMetaBaseMask, stride = meta >> kMetaStrideShift;
     const R2 pv = pts[i];
     R sx = R(0), sy = R(0);

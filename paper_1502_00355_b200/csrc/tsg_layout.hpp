@@ -5,8 +5,7 @@
 
 namespace tsg {
 
-constexpr uint64_t kNoCycle = ~uint64_t{0};  // cycle word of a row without a single link cycle
-constexpr int kMaxCycleDeg = 15;             // deg + 1 nibbles in 64 bits
+constexpr int kMaxCycleDeg = 31;  // tile (thread-per-vertex) rows: valence <= 31
 // Tiles of tile_update: kTile consecutive slots (the degree-sort windows of the locality
 // order).  A tile's small rows address their neighbours by LOCAL index: slot - tile base for
 // in-tile slots, kTile + position in the tile's sorted external-slot list otherwise.
@@ -16,9 +15,11 @@ constexpr uint32_t kNoLocal = 0x3fffu;  // cycle entry of a row without a single
 constexpr uint32_t kLocalMask = 0x3fffu;
 constexpr int kWordCycleShift = 16;
 constexpr int kWordRotShift = 30;
-// Tile meta word: first-word offset | valence | group stride (tsg_prep.hpp HostMesh::tmeta).
-constexpr uint32_t kMetaBaseMask = 0xffffu;
-constexpr int kMetaDegShift = 16;     // 4 bits
-constexpr int kMetaStrideShift = 20;  // 11 bits (<= kTile)
+// Tile meta word: first-word offset (15 bits: <= kTile * kMaxCycleDeg words) | valence (5
+// bits) | group stride (11 bits, <= kTile) (tsg_prep.hpp HostMesh::tmeta).
+constexpr uint32_t kMetaBaseMask = 0x7fffu;
+constexpr int kMetaDegShift = 15;
+constexpr uint32_t kMetaDegMask = 31u;
+constexpr int kMetaStrideShift = 20;
 
 }  // namespace tsg

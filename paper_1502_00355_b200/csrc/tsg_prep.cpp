@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <thread>
 
 namespace tsg {
@@ -159,11 +160,11 @@ std::string build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t 
         uint32_t* r = hm.trec.data() + hm.tile_rec[t] + (meta & kMetaBaseMask);
         const uint32_t stride = meta >> kMetaStrideShift;
         const uint32_t o0 = hm.off[s], n = deg[s];
-        const uint64_t cyc = hm.cyc[s];
+        const bool cyc = hm.has_cycle[s] != 0;
         for (uint32_t j = 0; j < n; ++j) {
           const uint32_t row = local(hm.nbr[o0 + j]);
-          const uint32_t cy = cyc == kNoCycle ? kNoLocal : local(hm.nbr[o0 + ((cyc >> (4 * j)) & 15u)]);
-          const uint32_t k = cyc == kNoCycle ? 0u : (hm.cyck[s] >> (2 * j)) & 3u;
+          const uint32_t cy = cyc ? local(hm.nbr[o0 + hm.cycpos[o0 + j]]) : kNoLocal;
+          const uint32_t k = cyc ? hm.cycrot[o0 + j] : 0u;
           r[j * stride] = row | (cy << kWordCycleShift) | (k << kWordRotShift);
         }
       }
@@ -214,7 +215,10 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     }
     // Degree sort inside windows of kSigma consecutive slots of the locality order (SELL-C-σ
     // style): warps then see near-uniform valences (no divergent loop tails) while every
-    // window stays spatially compact.  Results do not depend on the slot order.
+    // window stays spatially compact.  Descending: a tile's longest rows are in its first
+    // rounds, overlapping the other warps' work instead of forming a tail (measured: ascending
+    // with dynamic rounds 31.7 G, descending with static rounds 33.3 G node-upd/s on cfg3).
+    // Results do not depend on the slot order.
     constexpr int64_t kSigma = kTile;  // windows coincide with the tiles of tile_update
     auto degree_key = [&](int64_t v) -> int64_t {
       return d.boundary[v] ? 0 : d.nbr_off[v + 1] - d.nbr_off[v];
@@ -223,7 +227,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
       for (int64_t w = b; w < e; ++w) {
         auto first = hm.order.begin() + w * kSigma;
         auto last = hm.order.begin() + std::min(nv, (w + 1) * kSigma);
-        std::stable_sort(first, last, [&](int64_t x, int64_t y) { return degree_key(x) < degree_key(y); });
+        std::stable_sort(first, last, [&](int64_t x, int64_t y) { return degree_key(x) > degree_key(y); });
       }
     });
     for (int64_t s = 0; s < nv; ++s) hm.rank[hm.order[s]] = s;
@@ -266,8 +270,9 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   hm.nbr.assign(total, 0);
   hm.fan.assign(total, 0);
   hm.fan16.assign(total, 0);
-  hm.cyc.assign(nv, kNoCycle);
-  hm.cyck.assign(nv, 0);
+  hm.cycpos.assign(total, 0);
+  hm.cycrot.assign(total, 0);
+  hm.has_cycle.assign(nv, 0);
 
   // Device triangle order: identity, or by the smallest slot among the corners (stable) so
   // that the triangle kernels stream coordinates in the same locality order as the vertices.
@@ -347,19 +352,16 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
       }
       if (cycle_ok) {
         // Single directed cycle through all n positions, starting at position 0.
-        uint64_t w = 0;
-        uint32_t kw = 0;
+        uint8_t* cp = hm.cycpos.data() + hm.off[s];
+        uint8_t* cr = hm.cycrot.data() + hm.off[s];
         int32_t p = 0, steps = 0;
         do {
-          w |= static_cast<uint64_t>(p) << (4 * steps);
-          kw |= static_cast<uint32_t>(rot[p]) << (2 * steps);
+          cp[steps] = static_cast<uint8_t>(p);
+          cr[steps] = static_cast<uint8_t>(rot[p]);
           p = succ[p];
           ++steps;
         } while (p > 0 && steps < n);
-        if (p == 0 && steps == n) {  // nibble n (= n_0 = 0) is already 0
-          hm.cyc[s] = w;
-          hm.cyck[s] = kw;
-        }
+        if (p == 0 && steps == n) hm.has_cycle[s] = 1;
       }
     }
   });
@@ -400,6 +402,8 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   {
     const std::string terr = build_tiles(hm, deg, kMaxCycleDeg);
     if (!terr.empty()) return terr;
+    std::vector<uint8_t>().swap(hm.cycpos);  // only build_tiles reads the cycles
+    std::vector<uint8_t>().swap(hm.cycrot);
   }
   // Longest rows first: the warp tier's tail is its largest hubs.
   std::stable_sort(hm.large.begin(), hm.large.end(), [&](int32_t x, int32_t y) { return deg[x] > deg[y]; });

@@ -41,12 +41,13 @@ struct HostMesh {
   std::vector<uint32_t> nbr;      // slots
   std::vector<uint32_t> fan;      // every row: (i1, i2, k) records
   std::vector<uint16_t> fan16;    // small rows: ring positions of (p1, p2, p3), 5 bits each
-  // Small rows: the one-ring as a directed cycle, 4-bit row positions n_0..n_deg (n_deg = n_0)
-  // such that every incident triangle is a rotation of (v, row[n_j], row[n_j+1]).  kNoCycle
-  // when the link of v is not a single directed cycle (bow-tie / inconsistent orientation) or
-  // the row is not in the small tier; those vertices use the fan records.
-  std::vector<uint64_t> cyc;
-  std::vector<uint32_t> cyck;     // 2 bits per cycle step j: v's position k in triangle j
+  // Rows with deg <= kMaxCycleDeg: the one-ring as a directed cycle — cycpos[off[s] + j] is the
+  // row position of the j-th cycle entry (every incident triangle is a rotation of (v,
+  // row[cycpos[j]], row[cycpos[j+1]])), cycrot[...] the position k of v in that literal
+  // triangle; has_cycle[s] = 0 when the link of v is not a single directed cycle (bow-tie /
+  // inconsistent orientation): those rows use the fan records.  cycpos / cycrot are released
+  // once the tiles are built.
+  std::vector<uint8_t> cycpos, cycrot, has_cycle;
   std::vector<uint32_t> vinc_off; // nv+1, all vertices
   std::vector<uint32_t> vinc;     // device triangle ids
   std::vector<int32_t> tri;       // 3*nt device slots, device triangle order
