@@ -493,6 +493,7 @@ def main():
         its, _ = dm.smooth_host_batch([xin_np] * args.steps, scfg, [xout_np] * args.steps)
         e2e_updates = nv * int(its.sum())
         e2e_s = time.perf_counter() - t0
+
         if dist:
             t = torch.tensor([e2e_s], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
