@@ -485,7 +485,8 @@ def main():
         xin = torch.from_numpy(np.ascontiguousarray(xy)).pin_memory()
         xout = torch.empty_like(xin).pin_memory()
         xin_np, xout_np = xin.numpy(), xout.numpy()
-        dm.smooth_host_batch([xin_np], scfg, [xout_np])
+        # untimed warm-up: the same call shape (batch staging buffers, captured graph)
+        dm.smooth_host_batch([xin_np] * args.steps, scfg, [xout_np] * args.steps)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         # one public call for the K steps: every step copies its input host->device and its

@@ -374,7 +374,7 @@ struct tsg_context {
   std::vector<cudaEvent_t> pass_events;  // stream-timed driver
   // Side stream for the medium / hub tiers, forked from and joined back into `stream` so
   // the tiers of one pass (or one Form B level) run concurrently (also inside graphs).
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // tsg_smooth_host_batch
   cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
   std::vector<cudaEvent_t> fork_events;
@@ -604,39 +604,26 @@ struct Engine {
   static tsg_status launch_form_a_fused(tsg_mesh* m, const Args& base, cudaStream_t s, int64_t* kernels) {
     tsg_context* ctx = m->ctx;
     const int64_t nv = m->hm.nv, nlarge = static_cast<int64_t>(m->hm.large.size());
+    const int64_t nhub = m->n_hub_fast, nwarp = nlarge - nhub;
     static const bool serial = std::getenv("TSG_SERIAL_TIERS") != nullptr;  // experiment knob
-    const bool fork = !serial && nlarge > 0;
-    cudaStream_t t = s;
-    if (fork) {
+    static const bool two_side = std::getenv("TSG_TWO_SIDE_STREAMS") != nullptr;  // experiment knob
+    // Stream of each side tier: the side tiers run on a stream forked inside the captured graph,
+    // concurrently with the tile kernel (hub and warp tiers on two streams: -1 %, measured).
+    cudaStream_t th = s, tw = s;
+    if (!serial && nlarge > 0) th = tw = ctx->side;
+    if (two_side && nhub > 0 && nwarp > 0) th = ctx->side2;
+    cudaStream_t forked[2];
+    int nf = 0;
+    for (cudaStream_t t : {th, tw})
+      if (t != s && (nf == 0 || forked[0] != t)) forked[nf++] = t;
+    for (int i = 0; i < nf; ++i) {
+      cudaStream_t t = forked[i];
       cudaEvent_t e;
       tsg_status st = next_event(ctx, &e);
       if (st) return st;
       TSG_CUDA(cudaEventRecord(e, s));
-      TSG_CUDA(cudaStreamWaitEvent(ctx->side, e, 0));
-      t = ctx->side;
+      TSG_CUDA(cudaStreamWaitEvent(t, e, 0));
     }
-    auto side_tiers = [&]() -> tsg_status {
-      const int64_t nhub = m->n_hub_fast, nwarp = nlarge - nhub;
-      if (nhub > 0) {  // the longest rows (a prefix of the degree-descending list): CTA per hub
-        Args a = base;
-        a.list = m->d_large;
-        a.count = nhub;
-        const int32_t cap = hub_fast_cap(m);
-        tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(nhub), tsg::kHubBlock, cap * sizeof(R2), t>>>(a, cap);
-        TSG_CUDA(cudaGetLastError());
-        ++*kernels;
-      }
-      if (nwarp > 0) {
-        Args a = base;
-        a.list = m->d_large + nhub;
-        a.count = nwarp;
-        tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>
-            <<<static_cast<unsigned>((nwarp + kWarpTierWarps - 1) / kWarpTierWarps), kWarpTierWarps * 32, 0, t>>>(a);
-        TSG_CUDA(cudaGetLastError());
-        ++*kernels;
-      }
-      return TSG_OK;
-    };
     {
       Args a = base;
       a.list = nullptr;
@@ -650,17 +637,32 @@ struct Engine {
         tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
-
     }
-    {  // side tiers launched after the tile kernel (its CTAs are dispatched first: +1 %, measured)
-      tsg_status st = side_tiers();
-      if (st) return st;
+    // Side tiers launched after the tile kernel (its CTAs are dispatched first: +1 %, measured).
+    if (nhub > 0) {  // the longest rows (a prefix of the degree-descending list): CTA per hub
+      Args a = base;
+      a.list = m->d_large;
+      a.count = nhub;
+      const int32_t cap = hub_fast_cap(m);
+      tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(nhub), tsg::kHubBlock, cap * sizeof(R2), th>>>(a, cap);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
     }
-    if (fork) {
+    if (nwarp > 0) {
+      Args a = base;
+      a.list = m->d_large + nhub;
+      a.count = nwarp;
+      tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>
+          <<<static_cast<unsigned>((nwarp + kWarpTierWarps - 1) / kWarpTierWarps), kWarpTierWarps * 32, 0, tw>>>(a);
+      TSG_CUDA(cudaGetLastError());
+      ++*kernels;
+    }
+    for (int i = 0; i < nf; ++i) {  // join
+      cudaStream_t t = forked[i];
       cudaEvent_t e;
       tsg_status st = next_event(ctx, &e);
       if (st) return st;
-      TSG_CUDA(cudaEventRecord(e, ctx->side));
+      TSG_CUDA(cudaEventRecord(e, t));
       TSG_CUDA(cudaStreamWaitEvent(s, e, 0));
     }
     return TSG_OK;
@@ -917,6 +919,7 @@ tsg_status tsg_context_create(int32_t device, tsg_context** out) {
   TSG_CUDA(cudaEventCreate(&ctx->ev0));
   TSG_CUDA(cudaEventCreate(&ctx->ev1));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  TSG_CUDA(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b)
@@ -934,6 +937,7 @@ tsg_status tsg_context_destroy(tsg_context* ctx) {
   cudaEventDestroy(ctx->ev1);
   for (cudaEvent_t e : ctx->fork_events) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->side);
+  cudaStreamDestroy(ctx->side2);
   cudaStreamDestroy(ctx->copy_in);
   cudaStreamDestroy(ctx->copy_out);
   for (int b = 0; b < 2; ++b)

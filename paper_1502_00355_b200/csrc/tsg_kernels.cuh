@@ -543,16 +543,18 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   uint32_t* meta_s = words + t.rec_cap;
 
   const int tid = threadIdx.x;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
-  const int n_in = static_cast<int>(t.nv - base < kTile ? t.nv - base : kTile);
   const int2 state = *reinterpret_cast<const int2*>(a.st);
   if (state.y) return;
   Coords<R, kSoA> P, N;
   select_buffers(a, state.x, P, N);
   const int pass = state.x;
 
-  const uint32_t e0 = __ldg(t.ext_off + blockIdx.x), ne = __ldg(t.ext_off + blockIdx.x + 1) - e0;
-  const uint32_t r0 = __ldg(t.tile_rec + blockIdx.x), nr = __ldg(t.tile_rec + blockIdx.x + 1) - r0;
+  const int tile = static_cast<int>(blockIdx.x);
+  const int64_t base = static_cast<int64_t>(tile) * kTile;
+  const int n_in = static_cast<int>(t.nv - base < kTile ? t.nv - base : kTile);
+
+  const uint32_t e0 = __ldg(t.ext_off + tile), ne = __ldg(t.ext_off + tile + 1) - e0;
+  const uint32_t r0 = __ldg(t.tile_rec + tile), nr = __ldg(t.tile_rec + tile + 1) - r0;
   const int n_ext = static_cast<int>(kStaged || ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
   const int n_rec = static_cast<int>(kStaged || nr < static_cast<uint32_t>(t.rec_cap) ? nr : t.rec_cap);
   // Bulk copies: full AoS tiles (coordinates and meta are then 16-byte multiples); the rest
@@ -762,26 +764,18 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
 // neighbour sum from the slice (broadcast reads, uniform control flow), lanes sweep the fan
 // records with the fast α/K filter for both positions of v, and a shuffle reduction gives the
 // warp-uniform decision.  Near-ties are settled with the reference's exact α (alpha_at).
-template <typename R, bool kSoA, int kWarps, int kCap>
-__global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) {
+template <typename R, bool kSoA, int kCap>
+__device__ __forceinline__ void warp_row(const PassArgs<R, kSoA>& a, const Coords<R, kSoA>& P,
+                                         const Coords<R, kSoA>& N, int pass, int64_t s,
+                                         typename Arith<R>::R2* ring) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr bool kExact = sizeof(R) == 8;
-  __shared__ R2 ring_s[kWarps * kCap];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * kWarps + w;
-  if (idx >= a.count) return;  // warp-uniform
-  const int2 state = *reinterpret_cast<const int2*>(a.st);
-  if (state.y) return;
-  Coords<R, kSoA> P, N;
-  select_buffers(a, state.x, P, N);
-  const int pass = state.x;
-  const int64_t s = a.list[idx];
+  const int lane = threadIdx.x & 31;
   const uint32_t o0 = __ldg(a.off + s);
   const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
   const uint32_t* nb = a.nbr + o0;
   const uint32_t* fan = a.fan + o0;
-  R2* ring = ring_s + w * kCap;
   const R2 pv = P.load(s);
 
   // neighbor_mean (smoothing.hpp:72-80): one ordered chain, computed redundantly by all lanes
@@ -883,6 +877,20 @@ __global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) 
     }
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+}
+
+template <typename R, bool kSoA, int kWarps, int kCap>
+__global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) {
+  using R2 = typename Arith<R>::R2;
+  __shared__ R2 ring_s[kWarps * kCap];
+  const int w = threadIdx.x >> 5;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * kWarps + w;
+  if (idx >= a.count) return;  // warp-uniform
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  warp_row<R, kSoA, kCap>(a, P, N, state.x, a.list[idx], ring_s + w * kCap);
 }
 
 // Fast α/K of the triangle (v, a, b) for one position of v: the rotation formula of the cycle
@@ -1132,25 +1140,25 @@ __global__ void __launch_bounds__(256) formb_chunk_update(PassArgs<R, kSoA> a, c
 // (smoothing.hpp:72-80) while warps 1.. sweep the fan at the pass-start position; then every
 // warp sweeps the fan at the candidate; block min-reductions give the decision, near-ties are
 // re-evaluated exactly (alpha_at) by the whole CTA.
+template <typename R>
+struct HubShared {
+  typename Arith<R>::R2 cand;
+  R min[2][kHubBlock / 32];
+  int bad;
+};
+
 template <typename R, bool kSoA>
-__global__ void __launch_bounds__(kHubBlock) hub_fast_update(PassArgs<R, kSoA> a, int cap) {
+__device__ __forceinline__ void hub_row(const PassArgs<R, kSoA>& a, const Coords<R, kSoA>& P,
+                                        const Coords<R, kSoA>& N, int pass, int64_t s, int cap,
+                                        unsigned slot_key, typename Arith<R>::R2* ring, HubShared<R>& hs) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr bool kExact = sizeof(R) == 8;
   constexpr int kWarps = kHubBlock / 32;
-  extern __shared__ __align__(16) unsigned char hub_smem[];
-  R2* ring = reinterpret_cast<R2*>(hub_smem);
-  __shared__ R2 s_cand;
-  __shared__ R s_min[2][kWarps];
-  __shared__ int s_bad;
-
-  const int2 state = *reinterpret_cast<const int2*>(a.st);
-  if (state.y) return;
-  Coords<R, kSoA> P, N;
-  select_buffers(a, state.x, P, N);
-  const int pass = state.x;
+  R2& s_cand = hs.cand;
+  R(&s_min)[2][kWarps] = hs.min;
+  int& s_bad = hs.bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t s = a.list[blockIdx.x];
   const uint32_t o0 = __ldg(a.off + s);
   const int deg = static_cast<int>(__ldg(a.off + s + 1) - o0);
   const uint32_t* nb = a.nbr + o0;
@@ -1268,11 +1276,23 @@ __global__ void __launch_bounds__(kHubBlock) hub_fast_update(PassArgs<R, kSoA> a
     if (acc) {
       const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
       const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-      const unsigned slot = pass * kStatSlots + (blockIdx.x & (kStatSlots - 1));
+      const unsigned slot = pass * kStatSlots + (slot_key & (kStatSlots - 1));
       atomicAdd(a.slot_acc + slot, 1);
       if (d > 0.0) atomicMax(a.slot_md + slot, static_cast<unsigned long long>(__double_as_longlong(d)));
     }
   }
+}
+
+template <typename R, bool kSoA>
+__global__ void __launch_bounds__(kHubBlock) hub_fast_update(PassArgs<R, kSoA> a, int cap) {
+  using R2 = typename Arith<R>::R2;
+  extern __shared__ __align__(16) unsigned char hub_smem[];
+  __shared__ HubShared<R> hs;
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  hub_row<R, kSoA>(a, P, N, state.x, a.list[blockIdx.x], cap, blockIdx.x, reinterpret_cast<R2*>(hub_smem), hs);
 }
 
 // CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)
