@@ -12,7 +12,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 # -fmad=false: no FMA contraction anywhere in device code (the kernels also use explicit
 # _rn intrinsics); IEEE div/sqrt are nvcc's defaults and are kept.
 NVFLAGS  := -O3 -std=c++20 $(ARCH) -lineinfo -fmad=false -Xptxas -v -Xcompiler -fPIC,-O3 \
-            -Iinclude -I$(CSRC) --expt-relaxed-constexpr
+            -Iinclude -I$(CSRC) --expt-relaxed-constexpr $(EXTRA_NVFLAGS)
 CXXFLAGS := -O3 -std=c++20 -fPIC -Iinclude -I$(CSRC) -Wall -Wextra -Wno-unused-parameter
 PYEXT    := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))")
 PYINC    := $(shell $(PYTHON) -m pybind11 --includes)

@@ -217,9 +217,14 @@ tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_
                               double* max_abs_err_out, int64_t* nonfinite_out);
 /* The same for the rotation (cycle) fast path of the Form A fused kernels: the maximum
  * |t - alpha_ref / K| in alpha/K units, K = 2*sqrt(3) as the reference rounds it.  Its guard
- * band is 2^-47 in those units (derivation in tsg_device.cuh, kGuardCycle). */
+ * band is 2^-48 in those units (derivation in tsg_device.cuh, kGuardCycle). */
 tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, double* max_abs_err_out,
                                     int64_t* nonfinite_out);
+
+/* Timeline instrumentation readout: copies the per-CTA / per-warp (start ns, duration ns << 8 |
+ * SM id) records of one pass into out.  Only builds made with -DTSG_TRACE record them
+ * (tools/trace_cfg3.py); other builds return TSG_ERR_INVALID. */
+tsg_status tsg_debug_trace(void* out, int64_t bytes);
 
 /* ---- locality ordering (host prep helper) ---- */
 /* order_out[s] = original id for slot s: vertices sorted along a Hilbert curve over the

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsg.so")
+LIB_PATH = os.environ.get("TSG_LIB") or os.path.join(HERE, "libtsg.so")  # TSG_LIB: experiment builds
 
 TSG_OK, TSG_ERR_INVALID, TSG_ERR_CUDA, TSG_ERR_NOMEM, TSG_ERR_NODEVICE = 0, 1, 2, 3, 4
 LAYOUT = {"aos": 0, "soa": 1}

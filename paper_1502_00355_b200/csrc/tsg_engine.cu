@@ -753,10 +753,26 @@ struct Engine {
     {
       const tsg::TileArgs ta = tile_args(m);
       const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap));
+      if (std::getenv("TSG_DIAG"))
+        std::fprintf(stderr, "[tsg] tile smem %d B (ext_cap %d, rec_cap %d words), large rows %zu (hub CTAs %lld)\n",
+                     smem, ta.ext_cap, ta.rec_cap, m->hm.large.size(), static_cast<long long>(m->n_hub_fast));
       TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    // Kernels that run concurrently on one SM must agree on its L1 / shared-memory split: the
+    // tile and side-tier kernels all ask for the maximum shared-memory carveout, so that a
+    // side-tier CTA does not pin an SM to a smaller split that excludes the tile kernel's CTAs.
+    {
+      const int kMax = cudaSharedmemCarveoutMaxShared;
+      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
+      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
+      TSG_CUDA(cudaFuncSetAttribute(tsg::hub_fast_update<R, kSoA>, cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
+      TSG_CUDA(cudaFuncSetAttribute(tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
     }
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
     const int smem1 = static_cast<int>(hub_cap * sizeof(R2)), smem2 = 2 * smem1;
@@ -1735,3 +1751,16 @@ tsg_status tsg_halo_unpack(tsg_mesh* m, const double* in, int32_t in_is_host) {
 }
 
 }  // extern "C"
+
+// Timeline instrumentation readout (TSG_TRACE builds only; see tsg_kernels.cuh).
+extern "C" tsg_status tsg_debug_trace(void* out, int64_t bytes) {
+#ifdef TSG_TRACE
+  if (!out || bytes < 0 || static_cast<size_t>(bytes) > sizeof(tsg::g_trace)) return fail(TSG_ERR_INVALID, "bad trace buffer");
+  TSG_CUDA(cudaMemcpyFromSymbol(out, tsg::g_trace, static_cast<size_t>(bytes)));
+  return TSG_OK;
+#else
+  (void)out;
+  (void)bytes;
+  return fail(TSG_ERR_INVALID, "built without TSG_TRACE");
+#endif
+}

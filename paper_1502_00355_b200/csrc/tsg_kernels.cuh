@@ -22,6 +22,37 @@
 
 namespace tsg {
 
+// Timeline instrumentation (build with EXTRA_NVFLAGS=-DTSG_TRACE; tools/trace_cfg3.py): per
+// CTA / warp start time, duration and SM of the tile and side kernels in pass kTracePass.
+#ifdef TSG_TRACE
+constexpr int kTracePass = 20;
+constexpr int kTraceMax = 65536;
+__device__ unsigned long long g_trace[3][kTraceMax][2];
+__device__ __forceinline__ unsigned long long trace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned trace_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#define TSG_TRACE_BEGIN(pass, id) \
+  const unsigned long long trace_t0 = trace_now(); \
+  const bool trace_on = (pass) == kTracePass && (id) < kTraceMax;
+#define TSG_TRACE_END(k, id, leader)                                                   \
+  if (trace_on && (leader)) {                                                          \
+    g_trace[k][id][0] = trace_t0;                                                      \
+    g_trace[k][id][1] = ((trace_now() - trace_t0) << 8) | trace_smid();                \
+  }
+#define TSG_TRACE_SYNC() __syncthreads()
+#else
+#define TSG_TRACE_BEGIN(pass, id)
+#define TSG_TRACE_END(k, id, leader)
+#define TSG_TRACE_SYNC()
+#endif
+
 constexpr int kNodeBlock = 128;
 constexpr int kHubBlock = 256;
 
@@ -543,16 +574,12 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   uint32_t* meta_s = words + t.rec_cap;
 
   const int tid = threadIdx.x;
-  const int2 state = *reinterpret_cast<const int2*>(a.st);
-  if (state.y) return;
-  Coords<R, kSoA> P, N;
-  select_buffers(a, state.x, P, N);
-  const int pass = state.x;
-
   const int tile = static_cast<int>(blockIdx.x);
   const int64_t base = static_cast<int64_t>(tile) * kTile;
   const int n_in = static_cast<int>(t.nv - base < kTile ? t.nv - base : kTile);
-
+  // The pass state (which coordinate buffer is current) is read in parallel with the tile's
+  // parity-independent records; only the coordinate copies wait for it.
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
   const uint32_t e0 = __ldg(t.ext_off + tile), ne = __ldg(t.ext_off + tile + 1) - e0;
   const uint32_t r0 = __ldg(t.tile_rec + tile), nr = __ldg(t.tile_rec + tile + 1) - r0;
   const int n_ext = static_cast<int>(kStaged || ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
@@ -564,13 +591,24 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     qn_s = 0;
     mbar_init(&bar, 1);
     if (bulk) {
-      const uint32_t bytes = kTile * sizeof(R2) + kTile * 4u + 4u * n_rec;
-      mbar_expect_tx(&bar, bytes);
-      bulk_g2s(pts, P.base + 2 * base, kTile * sizeof(R2), &bar);
+      mbar_expect_tx(&bar, kTile * sizeof(R2) + kTile * 4u + 4u * n_rec);
       bulk_g2s(meta_s, t.meta + base, kTile * 4u, &bar);
       if (n_rec > 0) bulk_g2s(words, t.rec + r0, 4u * n_rec, &bar);
     }
   }
+  // External slot indices (up to kExtRegs per thread; larger rings take a second loop).
+  constexpr int kExtRegs = 2;
+  uint32_t eidx[kExtRegs];
+#pragma unroll
+  for (int j = 0; j < kExtRegs; ++j) {
+    const int k = tid + j * kThreads;
+    eidx[j] = k < n_ext ? __ldg(t.ext + e0 + k) : 0u;
+  }
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int pass = state.x;
+  TSG_TRACE_BEGIN(pass, blockIdx.x)
+  if (bulk && tid == 0) bulk_g2s(pts, P.base + 2 * base, kTile * sizeof(R2), &bar);
   if (!bulk) {
     for (int i = tid; i < n_in; i += kThreads) {
       pts[i] = P.load(base + i);
@@ -580,15 +618,26 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     uint4* dst = reinterpret_cast<uint4*>(words);
     for (int k = tid; k < n_rec / 4; k += kThreads) dst[k] = __ldg(src + k);
   }
-  if constexpr (kSoA) {
-    for (int k = tid; k < n_ext; k += kThreads) pts[kTile + k] = P.load(__ldg(t.ext + e0 + k));
-  } else {
-    for (int k = tid; k < n_ext; k += kThreads)
-      cp_async<sizeof(R2)>(pts + kTile + k, reinterpret_cast<const R2*>(P.base) + __ldg(t.ext + e0 + k));
-    cp_async_wait_all();
+#pragma unroll
+  for (int j = 0; j < kExtRegs; ++j) {
+    const int k = tid + j * kThreads;
+    if (k < n_ext) {
+      if constexpr (kSoA)
+        pts[kTile + k] = P.load(eidx[j]);
+      else
+        cp_async<sizeof(R2)>(pts + kTile + k, reinterpret_cast<const R2*>(P.base) + eidx[j]);
+    }
   }
+  for (int k = tid + kExtRegs * kThreads; k < n_ext; k += kThreads) {
+    if constexpr (kSoA)
+      pts[kTile + k] = P.load(__ldg(t.ext + e0 + k));
+    else
+      cp_async<sizeof(R2)>(pts + kTile + k, reinterpret_cast<const R2*>(P.base) + __ldg(t.ext + e0 + k));
+  }
+  if constexpr (!kSoA) cp_async_wait_all();
   __syncthreads();  // also publishes the mbarrier initialisation
   if (bulk) mbar_wait(&bar, 0);
+  if (state.y) return;  // (after the copies into this CTA's shared memory have landed)
 
   const TileView<R, kSoA, kStaged> tv{pts, words, P, t.ext + e0, t.rec + r0, t.ext_cap, t.rec_cap};
   const bool xonly = exact_only(a.maxabs);
@@ -755,6 +804,8 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     }
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+  TSG_TRACE_SYNC();
+  TSG_TRACE_END(0, blockIdx.x, tid == 0)
 }
 
 // Warp per vertex, Form A fused, for rows above the cycle tiers (valence 16 .. any): the
@@ -890,7 +941,9 @@ __global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) 
   if (state.y) return;
   Coords<R, kSoA> P, N;
   select_buffers(a, state.x, P, N);
+  TSG_TRACE_BEGIN(state.x, idx)
   warp_row<R, kSoA, kCap>(a, P, N, state.x, a.list[idx], ring_s + w * kCap);
+  TSG_TRACE_END(2, idx, (threadIdx.x & 31) == 0)
 }
 
 // Fast α/K of the triangle (v, a, b) for one position of v: the rotation formula of the cycle
@@ -1292,7 +1345,10 @@ __global__ void __launch_bounds__(kHubBlock) hub_fast_update(PassArgs<R, kSoA> a
   if (state.y) return;
   Coords<R, kSoA> P, N;
   select_buffers(a, state.x, P, N);
+  TSG_TRACE_BEGIN(state.x, blockIdx.x)
   hub_row<R, kSoA>(a, P, N, state.x, a.list[blockIdx.x], cap, blockIdx.x, reinterpret_cast<R2*>(hub_smem), hs);
+  TSG_TRACE_SYNC();
+  TSG_TRACE_END(1, blockIdx.x, threadIdx.x == 0)
 }
 
 // CTA per high-valence vertex.  Dynamic shared memory: `cap` pass-start pairs followed (Form B)
