@@ -34,6 +34,7 @@ EXPORTS = (
     "tsg_pass_lockstep", "tsg_smooth_host_batch", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
     "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
+    "tsg_debug_trace",
 )
 
 
@@ -88,6 +89,7 @@ def lib() -> C.CDLL:
             "tsg_hilbert_order": (i32, [i64, P, P]),
             "tsg_selftest_alpha": (i32, [P, i64, C.c_uint64, i32, P, P]),
             "tsg_selftest_alpha_cycle": (i32, [P, i64, C.c_uint64, P, P]),
+            "tsg_debug_trace": (i32, [P, i64]),
             "tsg_pass": (i32, [P, C.POINTER(SmoothCfg), P, P]),
             "tsg_halo_plan": (i32, [P, P, i64, P, i64]),
             "tsg_halo_pack": (i32, [P, C.c_void_p, i32]),
