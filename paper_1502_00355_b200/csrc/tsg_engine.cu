@@ -49,7 +49,10 @@ constexpr int kTileRecCap = 12288;  // ... row words staged in shared memory (mu
 constexpr int64_t kFormBChunkWidth = 4096;
 // formb_chunk_update: record double buffer + per-thread pass-start / view rings (f64 pairs)
 constexpr int kChunkRecSmem = 2 * 256 * tsg::kChunkRecWords * 4 + 2 * tsg::kChunkRecMaxDeg * 256 * 16;  // Form B: chunk kernel below this mean level width
-constexpr int kWarpTierWarps = 8;  // warp-per-vertex tier: warps per CTA
+#ifndef TSG_WARP_TIER_WARPS
+#define TSG_WARP_TIER_WARPS 1
+#endif
+constexpr int kWarpTierWarps = TSG_WARP_TIER_WARPS;  // warp-per-row tier: warps per CTA (1: finest dispatch in the tail; -0.6 % vs 8, measured)
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
 
 template <class T>
@@ -644,7 +647,7 @@ struct Engine {
       a.list = m->d_large;
       a.count = nhub;
       const int32_t cap = hub_fast_cap(m);
-      tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(nhub), tsg::kHubBlock, cap * sizeof(R2), th>>>(a, cap);
+      tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(nhub), tsg::kHubFastBlock, cap * sizeof(R2), th>>>(a, cap);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
