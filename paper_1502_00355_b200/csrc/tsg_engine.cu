@@ -54,6 +54,10 @@ constexpr int kChunkRecSmem = 2 * 256 * tsg::kChunkRecWords * 4 + 2 * tsg::kChun
 #endif
 constexpr int kWarpTierWarps = TSG_WARP_TIER_WARPS;  // warp-per-row tier: warps per CTA (1: finest dispatch in the tail; -0.6 % vs 8, measured)
 constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory per warp
+#ifndef TSG_HUB_FAST_MIN
+#define TSG_HUB_FAST_MIN 256
+#endif
+constexpr int kHubFastMin = TSG_HUB_FAST_MIN;  // rows above this valence get a CTA each
 
 template <class T>
 tsg_status dalloc(T** p, size_t count, int64_t* bytes) {
@@ -1066,7 +1070,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = dalloc(&m->d_ext, 3, b))) return st;
   for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
   while (m->n_hub_fast < static_cast<int64_t>(hm.large.size()) &&
-         hm.off[hm.large[m->n_hub_fast] + 1] - hm.off[hm.large[m->n_hub_fast]] > static_cast<uint32_t>(kWarpTierCap))
+         hm.off[hm.large[m->n_hub_fast] + 1] - hm.off[hm.large[m->n_hub_fast]] > static_cast<uint32_t>(kHubFastMin))
     ++m->n_hub_fast;
   if ((st = ensure_stats_capacity(m.get(), 128))) return st;
   st = dispatch(m.get(), [&](auto E) { return decltype(E)::set_coords(m.get(), d->xy); });
