@@ -207,6 +207,14 @@ tsg_status tsg_dist_end(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, int32_t* acce
 enum { TSG_FORMB_AUTO = 0, TSG_FORMB_LEVELS = 1, TSG_FORMB_CHUNKS = 2 };
 tsg_status tsg_mesh_formb_schedule(tsg_mesh* mesh, int32_t mode);
 
+/* Form A fused, rows of valence >= 32 (the paper's high-valence nodes): AUTO (default) runs them
+ * in a small persistent kernel beside the tile grid (one 4-warp CTA per SM, warps taking rows
+ * longest-first) when their estimated time fits inside the tile grid's, else as per-tier grids
+ * (CTA per hub, warp per row) after it; KERNELS / PERSIST force one of the two (identical
+ * results). */
+enum { TSG_SIDE_AUTO = 0, TSG_SIDE_KERNELS = 1, TSG_SIDE_PERSIST = 2 };
+tsg_status tsg_mesh_side_schedule(tsg_mesh* mesh, int32_t mode);
+
 /* ---- diagnostics ---- */
 /* Evaluates n seeded random triangles (unit scale, tiny, huge, near-degenerate) with the
  * kernels' fast alpha (refined reciprocal) and with the reference's IEEE division; returns the

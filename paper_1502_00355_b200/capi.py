@@ -34,7 +34,7 @@ EXPORTS = (
     "tsg_pass_lockstep", "tsg_smooth_host_batch", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
     "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
-    "tsg_debug_trace",
+    "tsg_debug_trace", "tsg_mesh_side_schedule",
 )
 
 
@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
             "tsg_halo_unpack": (i32, [P, C.c_void_p, i32]),
             "tsg_dist_begin": (i32, [P, C.POINTER(SmoothCfg)]),
             "tsg_mesh_formb_schedule": (i32, [P, i32]),
+            "tsg_mesh_side_schedule": (i32, [P, i32]),
             "tsg_dist_pass": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p]),
             "tsg_dist_halo_pack": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p]),
             "tsg_dist_halo_unpack": (i32, [P, C.c_void_p]),
@@ -300,6 +301,12 @@ class DeviceMesh:
         per chunk walking its levels).  Results are identical."""
         check(lib().tsg_mesh_formb_schedule(self.h, {"auto": 0, "levels": 1, "chunks": 2}[mode]),
               "tsg_mesh_formb_schedule")
+
+    def side_schedule(self, mode: str):
+        """Form A fused rows of valence >= 32: "auto", "kernels" (per-tier grids after the tile
+        grid) or "persist" (a persistent kernel beside it).  Results are identical."""
+        check(lib().tsg_mesh_side_schedule(self.h, {"auto": 0, "kernels": 1, "persist": 2}[mode]),
+              "tsg_mesh_side_schedule")
 
     # Device-resident partitioned loop (include/tsg.h, tsg_dist_*): enqueue-only calls taking
     # device pointers (e.g. torch CUDA tensors' data_ptr()).

@@ -58,6 +58,8 @@ constexpr int kWarpTierCap = 256;  // ... row entries staged in shared memory pe
 #define TSG_HUB_FAST_MIN 256
 #endif
 constexpr int kHubFastMin = TSG_HUB_FAST_MIN;  // rows above this valence get a CTA each
+constexpr int kSideWarps = 4;   // side_rows: warps per CTA (one per SM sub-partition), one CTA per SM
+constexpr int kSideRegs = 32;   // ... registers per thread (fits beside 3 tile CTAs of 80 registers)
 
 template <class T>
 tsg_status dalloc(T** p, size_t count, int64_t* bytes) {
@@ -402,6 +404,13 @@ struct tsg_mesh {
   uint32_t *d_off = nullptr, *d_nbr = nullptr, *d_fan = nullptr, *d_vinc_off = nullptr,
            *d_vinc = nullptr;
   int32_t *d_tri = nullptr, *d_hubs = nullptr, *d_medium = nullptr, *d_large = nullptr;
+  uint32_t* d_side_ctr = nullptr;  // side_rows ticket pair (zero between launches)
+  int32_t num_sms = 0;
+  // Rows above the cycle tiers: persistent side_rows kernel beside the tile grid, or per-tier
+  // grids after it (tsg_mesh_side_schedule; AUTO decides from the estimated work at upload).
+  int32_t side_mode = TSG_SIDE_AUTO;
+  bool side_persist_auto = false;
+  int64_t n_side_cta = 0;  // persistent mode: leading rows too long for one warp (hub CTAs)
   unsigned long long* d_maxabs = nullptr;  // bits of max |coordinate|
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   void* d_alpha = nullptr;
@@ -645,17 +654,30 @@ struct Engine {
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
+    const bool persist = nlarge > 0 && side_persistent(m);
+    if (persist) {
+      Args a = base;
+      a.list = m->d_large + m->n_side_cta;
+      a.count = nlarge - m->n_side_cta;
+      if (a.count > 0) {
+        tsg::side_rows<R, kSoA, kSideWarps, kWarpTierCap, kSideRegs>
+            <<<static_cast<unsigned>(m->num_sms), kSideWarps * 32, 0, tw>>>(a, m->d_side_ctr);
+        TSG_CUDA(cudaGetLastError());
+        ++*kernels;
+      }
+    }
+    const int64_t n_cta = persist ? m->n_side_cta : nhub;  // rows with a CTA each
     // Side tiers launched after the tile kernel (its CTAs are dispatched first: +1 %, measured).
-    if (nhub > 0) {  // the longest rows (a prefix of the degree-descending list): CTA per hub
+    if (n_cta > 0) {  // the longest rows (a prefix of the degree-descending list): CTA per hub
       Args a = base;
       a.list = m->d_large;
-      a.count = nhub;
+      a.count = n_cta;
       const int32_t cap = hub_fast_cap(m);
-      tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(nhub), tsg::kHubFastBlock, cap * sizeof(R2), th>>>(a, cap);
+      tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(n_cta), tsg::kHubFastBlock, cap * sizeof(R2), th>>>(a, cap);
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
-    if (nwarp > 0) {
+    if (!persist && nwarp > 0) {
       Args a = base;
       a.list = m->d_large + nhub;
       a.count = nwarp;
@@ -728,6 +750,10 @@ struct Engine {
     return TSG_OK;
   }
 
+  static bool side_persistent(const tsg_mesh* m) {
+    return m->side_mode == TSG_SIDE_PERSIST || (m->side_mode == TSG_SIDE_AUTO && m->side_persist_auto);
+  }
+
   static int32_t hub_fast_cap(const tsg_mesh* m) {
     return std::max(1, std::min(m->hm.max_deg, kHubCap));
   }
@@ -779,6 +805,8 @@ struct Engine {
                                     cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
       TSG_CUDA(cudaFuncSetAttribute(tsg::hub_fast_update<R, kSoA>, cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
       TSG_CUDA(cudaFuncSetAttribute(tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
+      TSG_CUDA(cudaFuncSetAttribute(tsg::side_rows<R, kSoA, kSideWarps, kWarpTierCap, kSideRegs>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
     }
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
@@ -1068,10 +1096,34 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = dalloc(&m->d_state, 1, b))) return st;
   if ((st = dalloc(&m->d_maxabs, 1, b))) return st;
   if ((st = dalloc(&m->d_ext, 3, b))) return st;
+  if ((st = dalloc(&m->d_side_ctr, 2, b))) return st;
+  TSG_CUDA(cudaMemsetAsync(m->d_side_ctr, 0, 2 * sizeof(uint32_t), s));
+  TSG_CUDA(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->ctx->device));
   for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
   while (m->n_hub_fast < static_cast<int64_t>(hm.large.size()) &&
          hm.off[hm.large[m->n_hub_fast] + 1] - hm.off[hm.large[m->n_hub_fast]] > static_cast<uint32_t>(kHubFastMin))
     ++m->n_hub_fast;
+  {
+    // AUTO side schedule: the persistent side_rows kernel when its estimated time fits inside
+    // the tile grid's.  Calibrated on cfg3 (B200): the tile grid runs ~36 G vertices/s on 148
+    // SMs; a side warp (32 registers, beside the tile grid) takes ~0.09 us per row entry plus
+    // ~40 entries' worth per row; one warp per SM sub-partition.  Rows whose single-warp time
+    // would exceed half the tile grid's keep a CTA each (hub_fast_update after the tile grid).
+    const double sms = std::max(1, m->num_sms);
+    const double tile_us = static_cast<double>(hm.nv) / 36e3 * (148.0 / sms);
+    double entries = 0.0;
+    for (int32_t r : hm.large) entries += static_cast<double>(hm.off[r + 1] - hm.off[r]) + 40.0;
+    const double side_us = 0.09 * entries / (kSideWarps * sms);
+    const double row_cap = std::max<double>(kHubFastMin, 0.5 * tile_us / 0.16);
+    while (m->n_side_cta < static_cast<int64_t>(hm.large.size()) &&
+           hm.off[hm.large[m->n_side_cta] + 1] - hm.off[hm.large[m->n_side_cta]] > row_cap)
+      ++m->n_side_cta;
+    m->side_persist_auto = !hm.large.empty() && side_us <= tile_us;
+    if (std::getenv("TSG_DIAG"))
+      std::fprintf(stderr, "[tsg] side rows %zu: est %.0f us vs tile grid %.0f us -> %s (%lld CTA rows)\n",
+                   hm.large.size(), side_us, tile_us, m->side_persist_auto ? "persistent" : "kernels",
+                   static_cast<long long>(m->n_side_cta));
+  }
   if ((st = ensure_stats_capacity(m.get(), 128))) return st;
   st = dispatch(m.get(), [&](auto E) { return decltype(E)::set_coords(m.get(), d->xy); });
   if (st) return st;
@@ -1090,7 +1142,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_tmeta, m->d_tile_rec, m->d_ext_off, m->d_tile_ext, m->d_trec, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_large, m->d_maxabs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
-                  m->d_ext, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
+                  m->d_ext, m->d_side_ctr, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
   for (void* p : ptrs) cudaFree(p);
   for (int b = 0; b < 2; ++b) {
     cudaFree(m->d_batch_in[b]);
@@ -1568,6 +1620,16 @@ tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, c
   TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
   m->n_send = n_send;
   m->n_recv = n_recv;
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_side_schedule(tsg_mesh* m, int32_t mode) {
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  if (mode < TSG_SIDE_AUTO || mode > TSG_SIDE_PERSIST) return fail(TSG_ERR_INVALID, "unknown side-row schedule");
+  if (m->side_mode != mode) {
+    m->side_mode = mode;
+    m->gc.reset();  // re-captured by the next call
+  }
   return TSG_OK;
 }
 

@@ -950,6 +950,39 @@ __global__ void __launch_bounds__(kWarps * 32) warp_update(PassArgs<R, kSoA> a) 
   TSG_TRACE_END(2, idx, (threadIdx.x & 31) == 0)
 }
 
+// Rows above the cycle tiers (valence >= 32) as a small persistent kernel that runs BESIDE the
+// tile grid for the whole pass: one CTA of kWarps warps per SM at kRegs registers, sized so that
+// each SM sub-partition (16 K registers) holds one side warp next to its six tile_update warps
+// (6 x 80 x 32 + 32 x 32 = 16 K) — with the maximum shared-memory carveout on both kernels, the
+// tile grid keeps its 3 CTAs per SM.  Warps take rows (degree-descending, the longest first)
+// from a ticket counter; the last warp to leave resets the counter pair, so a launch leaves it
+// zeroed for the next pass.  The 32-register cap spills a little (latency-bound code anyway).
+template <typename R, bool kSoA, int kWarps, int kCap, int kRegs>
+__global__ void __maxnreg__(kRegs) side_rows(PassArgs<R, kSoA> a, uint32_t* ctr) {
+  using R2 = typename Arith<R>::R2;
+  __shared__ R2 ring_s[kWarps * kCap];
+  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  if (state.y) return;
+  Coords<R, kSoA> P, N;
+  select_buffers(a, state.x, P, N);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll 1
+  for (;;) {
+    uint32_t row = 0;
+    if (lane == 0) row = atomicAdd(ctr, 1u);
+    row = __shfl_sync(0xffffffffu, row, 0);
+    if (row >= static_cast<uint64_t>(a.count)) break;
+    TSG_TRACE_BEGIN(state.x, row)
+    warp_row<R, kSoA, kCap>(a, P, N, state.x, a.list[row], ring_s + w * kCap);
+    TSG_TRACE_END(2, row, lane == 0)
+    __syncwarp();
+  }
+  if (lane == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x * kWarps - 1) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 // Fast α/K of the triangle (v, a, b) for one position of v: the rotation formula of the cycle
 // sweep (ring_edge / ring_pair, same operation sequence, same error bound).
 template <typename R>

@@ -129,6 +129,25 @@ def test_high_valence_hubs_vs_oracle(capi, gpu_ctx, ts, port, form, chunks):
         dm.free()
 
 
+@pytest.mark.parametrize("mode", ["kernels", "persist"])
+@pytest.mark.parametrize("layout", ["aos", "soa"])
+def test_side_row_schedules_vs_oracle(capi, gpu_ctx, ts, port, mode, layout):
+    """Form A fused rows of valence >= 32 either as per-tier grids after the tile grid or in the
+    persistent side kernel beside it (ticket counter reused across passes and runs): both
+    reproduce the reference bit for bit."""
+    xy, tri = ts.graded_arrays(60000, 3, 2e-3, 2048)
+    topo = ts.topology(len(xy), tri)
+    want = port.smooth(xy, tri, form="a", chunks=1, max_iters=15, move_tol=0.0)
+    dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, layout=layout, order=capi.hilbert_order(xy))
+    dm.side_schedule(mode)
+    for driver in ("graph", "stream", "graph"):
+        dm.set_coords(xy)
+        got = dm.smooth(capi.make_cfg(form="a", max_iters=15, move_tol=0.0, driver=driver))
+        assert np.array_equal(got["accepted"], want.accepted)
+        assert np.array_equal(dm.get_coords().view(np.uint64), want.xy.view(np.uint64))
+    dm.free()
+
+
 @pytest.mark.parametrize("n", [40, 5000, 9000])
 def test_single_fan_hub_beyond_shared_memory(capi, gpu_ctx, ts, port, n):
     """A valence above the shared-memory staging cap (4096) reads the tail from global memory."""

@@ -1,5 +1,6 @@
 """Interleaved A/B of libtsg builds on one mesh (less box-to-box noise than separate bench runs).
-usage: python tools/ablib.py [--config cfg3] [--reps 4] [--steps 5] lib1.so lib2.so ...
+usage: python tools/ablib.py [--config cfg3] [--reps 4] [--steps 5] lib1.so[:side] lib2.so[:side] ...
+(side = auto | kernels | persist: the mesh's side-row schedule)
 Each library gets its own context + device mesh; rounds alternate between them; prints the
 per-pass time (device events around each 100-pass smooth) per library: median and min."""
 import argparse
@@ -23,7 +24,8 @@ xy, tri, _ = bench.make_mesh(ts, cfg, None)
 topo = ts.topology(len(xy), tri)
 order = capi.hilbert_order(xy)
 runs = []
-for path in args.libs:
+for spec in args.libs:
+    path, _, side = spec.partition(":")
     capi._lib = None
     capi.LIB_PATH = path
     L = capi.lib()
@@ -31,7 +33,9 @@ for path in args.libs:
     dm = capi.DeviceMesh(ctx, xy, tri, topo, order=order, precision=cfg["precision"], layout=cfg["layout"])
     scfg = capi.make_cfg(form=cfg["form"], strategy=cfg["strategy"], max_iters=cfg["passes"], move_tol=0.0,
                          bbox_diag=ts.bbox_diagonal(xy))
-    runs.append((path, L, ctx, dm, scfg, []))
+    if side:
+        dm.side_schedule(side)
+    runs.append((spec, L, ctx, dm, scfg, []))
 for rep in range(args.reps + 1):
     for path, L, ctx, dm, scfg, res in runs:
         capi._lib = L
@@ -41,5 +45,5 @@ for rep in range(args.reps + 1):
             if rep > 0:  # round 0 = warm-up
                 res.append(r["device_ms"] / r["iterations"])
 for path, L, ctx, dm, scfg, res in runs:
-    print(f"{path.split('/')[-1]:24s} ms/pass median {statistics.median(res):.4f} min {min(res):.4f} "
+    print(f"{path.split('/')[-1]:32s} ms/pass median {statistics.median(res):.4f} min {min(res):.4f} "
           f"max {max(res):.4f} (n={len(res)})")
