@@ -654,6 +654,11 @@ struct Engine {
       TSG_CUDA(cudaGetLastError());
       ++*kernels;
     }
+    // The persistent side kernel is enqueued AFTER the tile grid: in the captured graph the two
+    // forked branches are then dispatched side kernel first (measured: all of its CTAs resident
+    // at t = 0, the tile grid from 0.1 us, profiles/r01s3c_cfg3_timeline.txt); enqueued before
+    // the tile grid, it was dispatched behind it and ran alone after it (0.70 ms per pass).  The
+    // stream driver (diagnostics) has no such order: there it mostly runs after the tile grid.
     const bool persist = nlarge > 0 && side_persistent(m);
     if (persist) {
       Args a = base;
