@@ -617,7 +617,10 @@ struct Engine {
 
   // Form A, fused: tile-staged cycle sweep (thread per vertex) over every slot with deg <=
   // kMaxCycleDeg; warp per vertex above, on the side stream.
-  static tsg_status launch_form_a_fused(tsg_mesh* m, const Args& base, cudaStream_t s, int64_t* kernels) {
+  // graph: the pass is being captured into the WHILE graph (the persistent side kernel needs the
+  // graph's dispatch order, see below; plain stream launches use the per-tier grids).
+  static tsg_status launch_form_a_fused(tsg_mesh* m, const Args& base, cudaStream_t s, int64_t* kernels,
+                                        bool graph) {
     tsg_context* ctx = m->ctx;
     const int64_t nv = m->hm.nv, nlarge = static_cast<int64_t>(m->hm.large.size());
     const int64_t nhub = m->n_hub_fast, nwarp = nlarge - nhub;
@@ -658,8 +661,9 @@ struct Engine {
     // forked branches are then dispatched side kernel first (measured: all of its CTAs resident
     // at t = 0, the tile grid from 0.1 us, profiles/r01s3c_cfg3_timeline.txt); enqueued before
     // the tile grid, it was dispatched behind it and ran alone after it (0.70 ms per pass).  The
-    // stream driver (diagnostics) has no such order: there it mostly runs after the tile grid.
-    const bool persist = nlarge > 0 && side_persistent(m);
+    // stream driver and the partitioned driver's plain launches have no such order (there it ran
+    // after the tile grid: 0.69 ms per pass), so they use the per-tier grids.
+    const bool persist = nlarge > 0 && graph && side_persistent(m);
     if (persist) {
       Args a = base;
       a.list = m->d_large + m->n_side_cta;
@@ -723,7 +727,7 @@ struct Engine {
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
     if (ev_begin) TSG_CUDA(cudaEventRecord(ev_begin, s));
     if (!kFormB && !kTwoPhase) {
-      tsg_status st = launch_form_a_fused(m, base, s, kernels);
+      tsg_status st = launch_form_a_fused(m, base, s, kernels, use_handle != 0);
       if (st) return st;
     } else if (!kFormB) {
       tsg_status st = launch_phase<false, kTwoPhase>(m, base, nullptr, nv, m->d_medium,
