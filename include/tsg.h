@@ -202,8 +202,9 @@ tsg_status tsg_dist_end(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, int32_t* acce
                         int64_t* launches_out);
 
 /* Form B schedule: AUTO (default) walks the dependency levels inside one CTA per chunk when the
- * levels are narrow (mean width < 4096 vertices: serial Form B on small meshes), else launches
- * one set of tier kernels per level; LEVELS / CHUNKS force one of the two (identical results). */
+ * per-level cost model says so (narrow levels per chunk: serial Form B, or many chunks on a deep
+ * level structure), else launches one set of tier kernels per level; LEVELS / CHUNKS force one
+ * of the two (identical results). */
 enum { TSG_FORMB_AUTO = 0, TSG_FORMB_LEVELS = 1, TSG_FORMB_CHUNKS = 2 };
 tsg_status tsg_mesh_formb_schedule(tsg_mesh* mesh, int32_t mode);
 

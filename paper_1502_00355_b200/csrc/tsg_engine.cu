@@ -46,9 +46,8 @@ constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
 constexpr int kTileRecCap = 12288;  // ... row words staged in shared memory (multiple of 4)
-constexpr int64_t kFormBChunkWidth = 4096;
 // formb_chunk_update: record double buffer + per-thread pass-start / view rings (f64 pairs)
-constexpr int kChunkRecSmem = 2 * 256 * tsg::kChunkRecWords * 4 + 2 * tsg::kChunkRecMaxDeg * 256 * 16;  // Form B: chunk kernel below this mean level width
+constexpr int kChunkRecSmem = 2 * 256 * tsg::kChunkRecWords * 4 + 2 * tsg::kChunkRecMaxDeg * 256 * 16;
 #ifndef TSG_WARP_TIER_WARPS
 #define TSG_WARP_TIER_WARPS 1
 #endif
@@ -496,12 +495,22 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   TSG_CUDA(cudaStreamSynchronize(s));
   m->fb_nchunks = static_cast<int64_t>(sch.chunk_lvl.size()) - 1;
   {
-    // A launch per level costs a few microseconds; below ~4K vertices per level the chunk
-    // kernel (levels walked inside one CTA per chunk) is faster (cfg1: 195 levels of ~51).
+    // Per-level cost models fitted on B200 (cfg1 W = 1, 8; cfg2 W = 16, 148; cfg3 W = 64, 148):
+    //   launch per level:        ~6 us + 8e-5 us x (vertices in the level)
+    //   one CTA per chunk:       ~2.4 us + 0.04 us x (vertices of one chunk in the level)
+    // e.g. cfg3 W = 148 (1025 levels, 106 per chunk): chunks 7.9 ms vs levels 10.5 ms per pass;
+    // cfg3 W = 64 (163 per chunk): levels 12.8 vs chunks 17.0; cfg2 W = 148: levels 0.10 vs 0.28.
     const int64_t movable = static_cast<int64_t>(sch.cb_order.size());
     const int64_t nlev = static_cast<int64_t>(sch.levels.size());
-    m->fb_use_chunks = m->fb_mode == TSG_FORMB_AUTO ? (nlev > 0 && movable < kFormBChunkWidth * nlev)
-                                                    : m->fb_mode == TSG_FORMB_CHUNKS;
+    const double w_total = nlev ? double(movable) / nlev : 0.0;
+    const double w_chunk = nlev && m->fb_nchunks ? w_total / double(m->fb_nchunks) : 0.0;
+    const bool chunks_faster = nlev > 0 && 2.4 + 0.04 * w_chunk < 6.0 + 8e-5 * w_total;
+    m->fb_use_chunks = m->fb_mode == TSG_FORMB_AUTO ? chunks_faster : m->fb_mode == TSG_FORMB_CHUNKS;
+    if (std::getenv("TSG_DIAG"))
+      std::fprintf(stderr, "[tsg] Form B W=%d: %lld levels, %lld chunks, mean level width %.0f (%.1f per chunk) -> %s\n",
+                   chunks, static_cast<long long>(nlev), static_cast<long long>(m->fb_nchunks),
+                   w_total, w_chunk,
+                   m->fb_use_chunks ? "chunks" : "levels");
   }
   m->fb_levels = std::move(sch.levels);
   m->fb_bytes = b;
