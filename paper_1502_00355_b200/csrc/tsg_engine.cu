@@ -143,9 +143,17 @@ __global__ void coords_to_orig_parity(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kS
 
 __global__ void save_state(const tsg::PassState* st, tsg::PassState* out) { *out = *st; }
 
-__global__ void reset_pass_state(tsg::PassState* st, int32_t* slot_acc, unsigned long long* slot_md, int64_t n) {
+// Start of a smooth: pass state, per-pass stat slots, and the side_rows ticket pair (normally
+// left zeroed by each launch's last warp; reset here too so an aborted run cannot leak into the
+// next).
+__global__ void reset_pass_state(tsg::PassState* st, int32_t* slot_acc, unsigned long long* slot_md, int64_t n,
+                                 uint32_t* side_ctr) {
   const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i0 == 0) *st = tsg::PassState{0, 0, 0, 0};
+  if (i0 == 0) {
+    *st = tsg::PassState{0, 0, 0, 0};
+    side_ctr[0] = 0;
+    side_ctr[1] = 0;
+  }
   for (int64_t i = i0; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     slot_acc[i] = 0;
     slot_md[i] = 0ull;
@@ -1297,7 +1305,7 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
   // (zeroed by a kernel: memsets may be served by a copy engine, where they would queue behind
   // the host<->device copies tsg_smooth_host_batch overlaps with this stream)
   reset_pass_state<<<grid_for(int64_t{tsg::kStatSlots} * c->max_iters, 256), 256, 0, s>>>(
-      m->d_state, m->d_sacc, m->d_smd, int64_t{tsg::kStatSlots} * c->max_iters);
+      m->d_state, m->d_sacc, m->d_smd, int64_t{tsg::kStatSlots} * c->max_iters, m->d_side_ctr);
   TSG_CUDA(cudaGetLastError());
   GraphCache& g = m->gc;
   if (!(g.valid && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
