@@ -1144,7 +1144,15 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     while (m->n_side_cta < static_cast<int64_t>(hm.large.size()) &&
            hm.off[hm.large[m->n_side_cta] + 1] - hm.off[hm.large[m->n_side_cta]] > row_cap)
       ++m->n_side_cta;
-    m->side_persist_auto = !hm.large.empty() && side_us <= tile_us;
+    // ... and only when one side CTA fits in the shared memory left by kTileMinBlocks tile CTAs
+    // (dynamic + ~3 KB static + 1 KB reserved each; 228 KB per SM).
+    const size_t pair = 2 * m->rsize;
+    const size_t tile_smem = pair * (tsg::kTile + std::min(hm.max_ext, kTileExtCap)) +
+                             4 * static_cast<size_t>(std::min(hm.max_rec_words, kTileRecCap)) + 4 * tsg::kTile +
+                             4096;
+    const size_t side_smem = kSideWarps * static_cast<size_t>(kWarpTierCap) * pair + 1024;
+    const bool fits = tsg::kTileMinBlocks * tile_smem + side_smem <= 228 * 1024;
+    m->side_persist_auto = !hm.large.empty() && side_us <= tile_us && fits;
     if (std::getenv("TSG_DIAG"))
       std::fprintf(stderr, "[tsg] side rows %zu: est %.0f us vs tile grid %.0f us -> %s (%lld CTA rows)\n",
                    hm.large.size(), side_us, tile_us, m->side_persist_auto ? "persistent" : "kernels",
