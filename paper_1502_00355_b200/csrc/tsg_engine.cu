@@ -390,7 +390,7 @@ struct tsg_context {
   std::vector<cudaEvent_t> pass_events;  // stream-timed driver
   // Side stream for the medium / hub tiers, forked from and joined back into `stream` so
   // the tiers of one pass (or one Form B level) run concurrently (also inside graphs).
-  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaStream_t side = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // tsg_smooth_host_batch
   cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
   std::vector<cudaEvent_t> fork_events;
@@ -641,17 +641,14 @@ struct Engine {
     tsg_context* ctx = m->ctx;
     const int64_t nv = m->hm.nv, nlarge = static_cast<int64_t>(m->hm.large.size());
     const int64_t nhub = m->n_hub_fast, nwarp = nlarge - nhub;
-    static const bool serial = std::getenv("TSG_SERIAL_TIERS") != nullptr;  // experiment knob
-    static const bool two_side = std::getenv("TSG_TWO_SIDE_STREAMS") != nullptr;  // experiment knob
-    // Stream of each side tier: the side tiers run on a stream forked inside the captured graph,
-    // concurrently with the tile kernel (hub and warp tiers on two streams: -1 %, measured).
+    // The side tiers run on one stream forked (and joined) inside the captured graph, concurrently
+    // with the tile grid (measured alternatives: serial tiers -4 %, hub and warp tiers on two
+    // streams -1 %).
     cudaStream_t th = s, tw = s;
-    if (!serial && nlarge > 0) th = tw = ctx->side;
-    if (two_side && nhub > 0 && nwarp > 0) th = ctx->side2;
-    cudaStream_t forked[2];
+    if (nlarge > 0) th = tw = ctx->side;
+    cudaStream_t forked[1];
     int nf = 0;
-    for (cudaStream_t t : {th, tw})
-      if (t != s && (nf == 0 || forked[0] != t)) forked[nf++] = t;
+    if (nlarge > 0) forked[nf++] = ctx->side;
     for (int i = 0; i < nf; ++i) {
       cudaStream_t t = forked[i];
       cudaEvent_t e;
@@ -996,7 +993,6 @@ tsg_status tsg_context_create(int32_t device, tsg_context** out) {
   TSG_CUDA(cudaEventCreate(&ctx->ev0));
   TSG_CUDA(cudaEventCreate(&ctx->ev1));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-  TSG_CUDA(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
   TSG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b)
@@ -1014,7 +1010,6 @@ tsg_status tsg_context_destroy(tsg_context* ctx) {
   cudaEventDestroy(ctx->ev1);
   for (cudaEvent_t e : ctx->fork_events) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->side);
-  cudaStreamDestroy(ctx->side2);
   cudaStreamDestroy(ctx->copy_in);
   cudaStreamDestroy(ctx->copy_out);
   for (int b = 0; b < 2; ++b)
