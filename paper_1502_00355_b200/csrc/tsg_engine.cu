@@ -104,7 +104,8 @@ __global__ void coords_from_orig(const double* __restrict__ xy, const int64_t* _
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t v = order ? order[s] : s;
-    const double x = xy[2 * v], y = xy[2 * v + 1];
+    const double2 q = reinterpret_cast<const double2*>(xy)[v];  // one 16-B gather (staging buffers are cudaMalloc'd)
+    const double x = q.x, y = q.y;
     const auto p = tsg::Arith<R>::make(static_cast<R>(x), static_cast<R>(y));
     b0.store(s, p);
     b1.store(s, p);
@@ -120,8 +121,7 @@ __global__ void coords_to_orig(tsg::Coords<R, kSoA> b, const int64_t* __restrict
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t v = order ? order[s] : s;
     const auto p = b.load_mut(s);
-    xy[2 * v] = static_cast<double>(p.x);
-    xy[2 * v + 1] = static_cast<double>(p.y);
+    reinterpret_cast<double2*>(xy)[v] = make_double2(static_cast<double>(p.x), static_cast<double>(p.y));
   }
 }
 
@@ -136,8 +136,7 @@ __global__ void coords_to_orig_parity(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kS
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t v = order ? order[s] : s;
     const auto p = b.load_mut(s);
-    xy[2 * v] = static_cast<double>(p.x);
-    xy[2 * v + 1] = static_cast<double>(p.y);
+    reinterpret_cast<double2*>(xy)[v] = make_double2(static_cast<double>(p.x), static_cast<double>(p.y));
   }
 }
 
