@@ -423,6 +423,10 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
 
     if args.profile:
+        # ncu does not profile kernel nodes inside the conditional WHILE graph, so the profile run
+        # issues the same kernels as plain launches; the side rows are forced into the persistent
+        # kernel the graph path uses on cfg3 (AUTO picks it there; serialised under ncu anyway).
+        dm.side_schedule(os.environ.get("TSG_PROFILE_SIDE", "persist"))
         dm.restore_coords()
         dm.smooth(mk("stream"))
         torch.cuda.synchronize()

@@ -675,8 +675,9 @@ struct Engine {
     // at t = 0, the tile grid from 0.1 us, profiles/r01s3c_cfg3_timeline.txt); enqueued before
     // the tile grid, it was dispatched behind it and ran alone after it (0.70 ms per pass).  The
     // stream driver and the partitioned driver's plain launches have no such order (there it ran
-    // after the tile grid: 0.69 ms per pass), so they use the per-tier grids.
-    const bool persist = nlarge > 0 && graph && side_persistent(m);
+    // after the tile grid: 0.69 ms per pass), so there AUTO uses the per-tier grids (a forced
+    // TSG_SIDE_PERSIST still applies: tests, profiling).
+    const bool persist = nlarge > 0 && (m->side_mode == TSG_SIDE_PERSIST || (graph && side_persistent(m)));
     if (persist) {
       Args a = base;
       a.list = m->d_large + m->n_side_cta;
