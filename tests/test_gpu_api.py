@@ -107,3 +107,22 @@ def test_smooth_host_batch_equals_single_calls(capi, gpu_ctx, ts, port):
     dm.smooth_host_batch(ins[:1], cfg, outs)
     assert np.array_equal(outs[0].view(np.uint64), want.xy.view(np.uint64))
     dm.free()
+
+
+def test_smooth_host_batch_with_persistent_side_rows(capi, gpu_ctx, ts, port):
+    """The batch path (graph driver) with the high-valence rows in the persistent side kernel:
+    every item equals the reference (the side kernel's ticket counter is reused across items)."""
+    xy, tri = ts.graded_arrays(30000, 5, 2e-3, 600)
+    topo = ts.topology(len(xy), tri)
+    assert np.diff(topo["nbr_off"]).max() > 256
+    dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, order=capi.hilbert_order(xy))
+    dm.side_schedule("persist")
+    cfg = capi.make_cfg(form="a", max_iters=12, move_tol=0.0, bbox_diag=ts.bbox_diagonal(xy))
+    rng = np.random.default_rng(5)
+    ins = [np.ascontiguousarray(xy + rng.normal(0, 1e-5, xy.shape) * k) for k in range(3)]
+    outs = [np.empty_like(xy) for _ in ins]
+    dm.smooth_host_batch(ins, cfg, outs)
+    for k in range(3):
+        want = port.smooth(ins[k], tri, form="a", max_iters=12, move_tol=0.0)
+        assert np.array_equal(outs[k].view(np.uint64), want.xy.view(np.uint64)), k
+    dm.free()
