@@ -29,15 +29,19 @@ tsg: $(TSG_SO)
 host: $(TS_SO)
 module: $(MOD_SO)
 
-build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp include/tsg.h
+build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp $(CSRC)/tsg_internal.hpp include/tsg.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+build/tsg_quality.o: $(CSRC)/tsg_quality.cu $(CSRC)/tsg_device.cuh $(CSRC)/tsg_internal.hpp include/tsg.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_quality.log || (cat build/ptxas_quality.log; false)
 
 build/tsg_prep.o: $(CSRC)/tsg_prep.cpp $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp include/tsg.h
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(TSG_SO): build/tsg_engine.o build/tsg_prep.o
+$(TSG_SO): build/tsg_engine.o build/tsg_quality.o build/tsg_prep.o
 	$(NVCC) -shared $(ARCH) -Xcompiler -fPIC -o $@ $^ -lpthread
 
 build/host/%.o: $(CSRC)/host/%.cpp $(wildcard include/trismooth/*.hpp) include/tsg.h

@@ -26,6 +26,7 @@ scaling of the same mesh.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -84,6 +85,13 @@ def algorithmic_bytes_per_pass(nv, nt, sum_deg, precision):
     """every array element counted once per pass, in the reference data model."""
     c = 16 if precision == "f64" else 8
     return 2 * c * nv + 4 * (nv + 1) + 4 * sum_deg + 4 * (nv + 1) + 12 * nt + 12 * nt + nv
+
+
+def roofline_kernel(cfg):
+    if cfg["form"] == "b":
+        return "Form B: formb_chunk_update / node_update level kernels"
+    return ("tile_update (tile-staged, thread per vertex, valence <= 31) + side_rows (valence >= 32, "
+            "persistent beside the tile grid) or warp_update / hub_fast_update grids (AUTO)")
 
 
 def measured_peak():
@@ -151,70 +159,129 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_rate(xy, tri, cfg, budget_s=20.0):
-    """The reference itself (oracle/_ref/libtsref.so: proj/src compiled out-of-tree) on host cores:
-    smooth() with Backend::Parallel and all hardware threads (Form A is bit-identical to serial;
-    Form B with W chunks is the semantics the W-chunk GPU run matches).  node-updates/s from the
-    reference's own iter_ms.  Falls back to the single-threaded oracle port if _ref is absent."""
+# Passes per reference sample (the reference arm's step, the cpu_baseline leg and the parity
+# digest): bounded so a step is seconds of host work; the full workload is `passes` per step.
+REF_PASSES = {"cfg1": 100, "cfg2": 10, "cfg3": 3, "cfg4": 2, "cfg5": 1}
+REF_UNAVAILABLE = {"cfg5": "the reference cannot hold this mesh: its raw adjacency list uses int32 offsets "
+                           "and 6*nt = 3.1e9 > INT32_MAX (proj/src/topology.cpp:18-31, SURVEY K6)"}
+
+
+def digest(xy: np.ndarray) -> str:
+    """sha256 over the little-endian float64 (x, y) pairs in original vertex order (the digest
+    tests/golden uses)."""
+    return hashlib.sha256(np.ascontiguousarray(xy, dtype="<f8").tobytes()).hexdigest()
+
+
+def workload_config(args, cfg, nv, nt, gargs, max_valence, b_pass):
+    """The `config` object both arms print (identical keys and values): what is computed, not
+    how.  Implementation details go to `impl_config`."""
+    return {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": nt,
+            "passes_per_step": cfg["passes"], "form": cfg["form"], "strategy": cfg["strategy"],
+            "chunks": cfg["chunks"], "layout": cfg["layout"], "precision": cfg["precision"],
+            "move_tol": cfg["move_tol"], "generator_args": list(gargs), "max_valence": int(max_valence),
+            "l2": "per-pass working set exceeds L2 (126 MB); no flush" if b_pass > 126e6
+            else "per-pass working set fits L2: passes re-read L2-resident data"}
+
+
+def ref_backend(ref, cfg):
+    """Reference Backend for a sample: Form A with all host threads (bitwise equal to serial);
+    Form B with the workload's chunk count W (Backend::Parallel with W workers IS the W-chunk
+    semantics); serial Form B stays serial."""
+    cores = ref.hardware_concurrency() or os.cpu_count() or 1
+    if cfg["form"] == "b":
+        return ("serial", 1) if cfg["chunks"] == 1 else ("parallel", cfg["chunks"])
+    return ("parallel", cores) if cores > 1 else ("serial", 1)
+
+
+def reference_sample(ref, xy, tri, cfg, passes):
+    backend, workers = ref_backend(ref, cfg)
+    return ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=workers,
+                      max_iters=passes, move_tol=cfg["move_tol"] if passes == cfg["passes"] else 0.0,
+                      layout=cfg["layout"]), backend, workers
+
+
+def cpu_reference_rate(xy, tri, cfg, config_name):
+    """The reference itself (oracle/_ref/libtsref.so: proj/src compiled out-of-tree) on host
+    cores, on the same mesh, REF_PASSES passes (a bounded sample); node-updates/s from the
+    reference's own iter_ms.  Returns (cpu_baseline dict, the reference's output coordinates,
+    passes) — the coordinates are the parity check of the bench line.  Falls back to the
+    single-threaded oracle port if _ref is absent (no parity digest then)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import REF_SO, Port, Ref
 
     nv = len(xy)
-    if os.path.exists(REF_SO):
+    passes = min(cfg["passes"], REF_PASSES.get(config_name, 3))
+    if os.path.exists(REF_SO) and config_name not in REF_UNAVAILABLE:
         ref = Ref()
-        cores = ref.hardware_concurrency() or os.cpu_count() or 1
-        # probe one pass, then size the sample to the budget
-        backend = "parallel" if cores > 1 else "serial"
-        if cfg["form"] == "b" and cfg["chunks"] == 1:
-            backend, cores_used = "serial", 1
-        else:
-            cores_used = cores
-        probe = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend,
-                           workers=cores_used, max_iters=1, move_tol=0.0, layout=cfg["layout"])
-        per_pass = max(probe.stats["iter_ms"], 1e-3) / 1000.0
-        passes = int(max(1, min(cfg["passes"], budget_s / per_pass)))
-        r = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=cores_used,
-                       max_iters=passes, move_tol=0.0, layout=cfg["layout"])
+        r, backend, workers = reference_sample(ref, xy, tri, cfg, passes)
         rate = nv * r.iterations / (r.stats["iter_ms"] / 1000.0)
-        return dict(value=rate, unit="node-updates/s", cores=cores_used, kind="reference",
+        return dict(value=rate, unit="node-updates/s", cores=workers, kind="reference",
                     sample=f"{r.iterations} passes of reference smooth() (form {cfg['form']}, {backend}, "
-                           f"W={cores_used}) on the same {nv}-node mesh; rate from its iter_ms "
-                           f"({r.stats['iter_ms']:.0f} ms); prep {r.stats['topo_ms'] + r.stats['init_ms'] + r.stats['constr_ms']:.0f} ms excluded")
+                           f"W={workers}) on the same {nv}-node mesh; rate from its iter_ms "
+                           f"({r.stats['iter_ms']:.0f} ms); prep {r.stats['topo_ms'] + r.stats['init_ms'] + r.stats['constr_ms']:.0f} ms excluded"), r, r.iterations
     port = Port()
     t0 = time.time()
     r = port.smooth(xy, tri, form=cfg["form"], chunks=cfg["chunks"], max_iters=1, move_tol=0.0)
     dt = time.time() - t0
     return dict(value=nv / dt, unit="node-updates/s", cores=1, kind="port",
-                sample=f"1 pass of the oracle restatement incl. its topology build on {nv} nodes")
+                sample=f"1 pass of the oracle restatement incl. its topology build on {nv} nodes"), None, 0
+
+
+def emit_mesh(args, cfg, out_dir):
+    """--emit-mesh (child process of the reference arm): generate the workload's mesh with this
+    repo's generators (the reference's own generator cannot build >1M-node meshes, K6) and write
+    it as .npy plus the workload config, so the reference arm's process never maps this repo's
+    libraries."""
+    import paper_1502_00355_b200 as ts
+
+    xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
+    topo = ts.topology(len(xy), tri)
+    deg = np.diff(topo["nbr_off"])
+    b_pass = algorithmic_bytes_per_pass(len(xy), len(tri), int(topo["nbr_off"][-1]), cfg["precision"])
+    os.makedirs(out_dir, exist_ok=True)
+    np.save(os.path.join(out_dir, "xy.npy"), xy)
+    np.save(os.path.join(out_dir, "tri.npy"), tri)
+    with open(os.path.join(out_dir, "config.json"), "w") as f:
+        json.dump(workload_config(args, cfg, len(xy), len(tri), gargs, deg.max() if len(deg) else 0, b_pass), f)
 
 
 def run_reference_arm(args, cfg):
-    """--impl reference: the reference CPU implementation, rank 0 only."""
+    """--impl reference: the reference's CPU implementation (oracle/_ref: proj/src compiled
+    out-of-tree), rank 0 only.  The mesh comes from a child process (--emit-mesh); this process
+    loads only oracle/_ref."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_1502_00355_b200 as ts  # fixture generator only (reference cannot build >1M meshes)
+    if args.config in REF_UNAVAILABLE:
+        print(json.dumps({"impl": "reference", "unavailable": REF_UNAVAILABLE[args.config]}))
+        return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import REF_SO, Ref
 
-    xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
-    nv = len(xy)
     if not os.path.exists(REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtsref.so was not built"}))
         return
+    cache = os.path.join("/tmp", f"tsg_bench_mesh_{args.config}_{args.nodes or 0}_{os.getpid()}")
+    cmd = [sys.executable, os.path.abspath(__file__), "--emit-mesh", cache, "--config", args.config]
+    if args.nodes:
+        cmd += ["--nodes", str(args.nodes)]
+    for k in ("passes", "layout", "precision", "form", "strategy", "chunks"):
+        if getattr(args, k) is not None:
+            cmd += [f"--{k}", str(getattr(args, k))]
+    subprocess.run(cmd, check=True)
+    xy = np.load(os.path.join(cache, "xy.npy"))
+    tri = np.load(os.path.join(cache, "tri.npy"))
+    with open(os.path.join(cache, "config.json")) as f:
+        config = json.load(f)
+    for name in ("xy.npy", "tri.npy", "config.json"):
+        os.remove(os.path.join(cache, name))
+    os.rmdir(cache)
+    nv = len(xy)
     ref = Ref()
-    cores = ref.hardware_concurrency() or 1
-    serial_b = cfg["form"] == "b" and cfg["chunks"] == 1
-    backend, workers = ("serial", 1) if serial_b or cores == 1 else ("parallel", cores)
-    probe = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=workers,
-                       max_iters=1, move_tol=0.0, layout=cfg["layout"])
-    per_pass = max(probe.stats["iter_ms"], 1e-3) / 1000.0
-    passes = int(max(1, min(cfg["passes"], args.ref_budget / per_pass)))
+    passes = min(cfg["passes"], REF_PASSES.get(args.config, 3))
     total_updates, total_ms = 0, 0.0
     for i in range(args.warmup + args.steps):
-        r = ref.smooth(xy, tri, form=cfg["form"], strategy=cfg["strategy"], backend=backend, workers=workers,
-                       max_iters=passes, move_tol=cfg["move_tol"] if cfg["passes"] == passes else 0.0,
-                       layout=cfg["layout"])
+        r, backend, workers = reference_sample(ref, xy, tri, cfg, passes)
         if i >= args.warmup:
             total_updates += nv * r.iterations
             total_ms += r.stats["iter_ms"]
@@ -224,13 +291,17 @@ def run_reference_arm(args, cfg):
         "unit": "node-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": len(tri),
-                   "passes_per_step": passes, "form": cfg["form"], "layout": cfg["layout"],
-                   "generator_args": list(gargs)},
+        "config": config,
+        "impl_config": {"backend": backend, "workers": workers, "passes_per_sample": passes,
+                        "mesh": "generated by a child process (bench.py --emit-mesh) with this repo's "
+                                "generators; this process maps only oracle/_ref/libtsref.so"},
         "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": workers, "kind": "reference",
-                         "sample": f"{passes} passes per step of the reference smooth() (prep excluded: "
-                                   f"rate from its iter_ms), {backend} backend, W={workers}"},
+                         "sample": f"{passes} passes per step of the reference smooth() from the workload's "
+                                   f"initial mesh (prep excluded: rate from its iter_ms), {backend} backend, "
+                                   f"W={workers}"},
         "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "check": {"passes": int(r.iterations), "xy_sha256": digest(r.xy),
+                  "accepted": [int(a) for a in r.accepted]},
     }
     print(json.dumps(out))
 
@@ -277,9 +348,11 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     updates = 0
+    passes_run = 0
     for _ in range(args.steps):
         it, _, _, _ = step()
         updates += nv * it
+        passes_run += it
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -312,7 +385,7 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     dist.all_reduce(io, op=dist.ReduceOp.SUM)
     sum_deg = int(topo["nbr_off"][-1])
     b_pass = algorithmic_bytes_per_pass(nv, nt, sum_deg, cfg["precision"])
-    pass_ms = elapsed_ms / max(1, args.steps * passes)
+    pass_ms = elapsed_ms / max(1, passes_run)
     peak, peak_src = measured_peak()
     achieved = b_pass / world / (pass_ms / 1000.0) / 1e9  # per GPU, pass time incl. the exchange
     if rank == 0:
@@ -321,11 +394,10 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": nt,
-                       "passes_per_step": passes, "form": "a", "layout": cfg["layout"],
-                       "parallelism": f"partitioned x{world} (Hilbert ranges, one-ring halo, "
-                                      f"{args.transport} all-to-all per pass)",
-                       "max_halo_vertices_per_rank": int(halo.item()), "generator_args": list(gargs)},
+            "config": workload_config(args, cfg, nv, nt, gargs, np.diff(topo["nbr_off"]).max(), b_pass),
+            "impl_config": {"parallelism": f"partitioned x{world} (Hilbert ranges, one-ring halo, "
+                                           f"{args.transport} all-to-all per pass)",
+                            "max_halo_vertices_per_rank": int(halo.item()), "passes_run": passes_run},
             "ms_per_pass": pass_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
@@ -363,6 +435,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=2.0, help="reference arm: target seconds of passes per step")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no e2e / baseline")
+    ap.add_argument("--emit-mesh", default=None, help=argparse.SUPPRESS)  # reference arm's mesh child
     ap.add_argument("--transport", choices=["nccl", "gloo"], default="nccl",
                     help="N>1 halo exchange: NCCL device buffers (default) or gloo host buffers "
                          "(lets N ranks share one GPU for testing)")
@@ -375,6 +448,9 @@ def main():
     if args.no_reorder or cfg["form"] == "b":
         cfg["reorder"] = False
 
+    if args.emit_mesh:
+        emit_mesh(args, cfg, args.emit_mesh)
+        return
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
@@ -416,9 +492,11 @@ def main():
         f"hubs(>16) {int(((deg > 16) & movable).sum())}")
     diag = ts.bbox_diagonal(xy)
     passes = cfg["passes"]
-    mk = lambda driver="graph": capi.make_cfg(form=cfg["form"], strategy=cfg["strategy"], chunks=cfg["chunks"],
-                                              swap=args.swap, max_iters=passes, driver=driver,
-                                              move_tol=cfg["move_tol"], bbox_diag=diag)
+    mk = lambda driver="graph", n=passes: capi.make_cfg(form=cfg["form"], strategy=cfg["strategy"],
+                                                        chunks=cfg["chunks"], swap=args.swap, max_iters=n,
+                                                        driver=driver,
+                                                        move_tol=cfg["move_tol"] if n == passes else 0.0,
+                                                        bbox_diag=diag)
     scfg = mk()
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
 
@@ -517,37 +595,54 @@ def main():
                "path": "tsg_smooth_host_batch (C ABI): per step pinned host xy -> device -> passes -> host xy, "
                             "copies of neighbouring steps overlapped with the passes"}
 
-    cpu = None
+    cpu, check = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_rate(xy, tri, cfg)
+            cpu, want, ref_passes = cpu_reference_rate(xy, tri, cfg, args.config)
         except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "error": str(exc)}
+            cpu, want, ref_passes = {"value": None, "error": str(exc)}, None, 0
+        if want is not None:
+            # Parity of this build on this workload: the same number of passes from the same
+            # initial coordinates through the same device mesh and configuration as the timed
+            # steps, against the reference's own smooth() output above.
+            dm.restore_coords()
+            rc = dm.smooth(mk("graph", ref_passes))
+            got = dm.get_coords()
+            ours, theirs = digest(got), digest(want.xy)
+            check = {"passes": int(rc["iterations"]), "xy_sha256": ours, "reference_xy_sha256": theirs,
+                     "accepted_match": bool(np.array_equal(rc["accepted"], want.accepted)),
+                     "max_disp_match": bool(np.array_equal(rc["max_disp"].view(np.uint64),
+                                                           want.max_disp.view(np.uint64))),
+                     "match": bool(ours == theirs and rc["iterations"] == want.iterations),
+                     "differing_vertices": int((got.view(np.uint64) != want.xy.view(np.uint64)).any(axis=1).sum())}
+            del want, got
 
     if rank == 0:
+        measured_frac = None
+        if traffic:
+            measured_frac = traffic / (node_ms_per_launch / 1000.0) / 1e9 / peak
         out = {
             "metric": "node-updates/sec (Smart Laplacian)", "value": value, "unit": "node-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg['label']}", "nodes": nv, "triangles": nt,
-                       "passes_per_step": iters_per_step, "form": cfg["form"], "strategy": cfg["strategy"],
-                       "layout": cfg["layout"], "swap": args.swap, "chunks": cfg["chunks"],
-                       "locality_order": "hilbert" if cfg["reorder"] else "none",
-                       "generator_args": list(gargs), "max_valence": int(deg.max()),
-                       "l2": "per-pass working set exceeds L2 (126 MB); no flush" if b_pass > 126e6
-                       else "per-pass working set fits L2: passes re-read L2-resident data",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "driver": "conditional-WHILE CUDA graph, 1 launch per step"},
+            "config": workload_config(args, cfg, nv, nt, gargs, deg.max(), b_pass),
+            "impl_config": {"swap": args.swap, "locality_order": "hilbert" if cfg["reorder"] else "none",
+                            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                            "driver": "conditional-WHILE CUDA graph, 1 launch per step",
+                            "passes_run_per_step": iters_per_step},
             "ms_per_pass": pass_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "tile_update (tile-staged, thread per vertex) + warp_update + hub_fast_update",
+                         "kernel": roofline_kernel(cfg),
                          "bytes_per_launch": b_pass, "launch_ms": node_ms_per_launch,
                          "launch_ms_stream_driver": node_ms_stream,
-                         "bytes_model": "SURVEY 8(d) B_pass: 2c*nv + 8(nv+1) + 4*sum_deg + 24*nt + nv"},
+                         "bytes_model": "algorithmic: SURVEY 8(d) B_pass = 2c*nv + 8(nv+1) + 4*sum_deg + 24*nt + nv "
+                                        "(reference data model); frac = B_pass / launch_ms / peak",
+                         "frac_of_measured_traffic": measured_frac},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "check": check,
             "clocks": clocks,
             "gpu_launches": launches,
             "launches_per_step": launches_per_step,

@@ -6,8 +6,9 @@
  * and the sm_100a kernels.  Plain C: explicit int64 counts, caller-owned host
  * buffers, library-owned device buffers behind opaque handles, integer status
  * (TSG_OK = 0) plus a thread-local message (tsg_last_error).  No exceptions and no
- * torch types cross this boundary.  One host thread drives a context at a time
- * (the reference's single-orchestrator rule, proj/include/trismooth/parallel.hpp:26-28).
+ * torch types cross this boundary.  Calls on one context are serialised by a per-context
+ * lock, so host threads may share a context (the drop-in smooth() does); each call is still
+ * single-orchestrator (proj/include/trismooth/parallel.hpp:26-28).
  *
  * Reference interfaces each entry point replaces (paths under /root/reference/proj):
  *   tsg_mesh_upload        the in-memory Mesh + Adjacency after find_neighbors /
@@ -21,6 +22,11 @@
  *   tsg_mesh_get_coords    (include/trismooth/mesh.hpp:61-70, :203-212)
  *   tsg_smooth_host        smooth() minus host topology prep (src/smoothing.cpp:146-182):
  *                          host coords in -> passes -> host coords + stats out
+ *   tsg_quality_tri_alpha  compute_all_qualities on a bare (xy, tri) pair plus the reductions
+ *                          of quality_summary / `trismooth quality` (src/quality.cpp:27-32,
+ *                          bindings/module.cpp:157-185, tools/main.cpp:151-208)
+ *   tsg_quality_vertex_minima  reduce_vertex_minima over a caller's incident CSR and stored
+ *                          α field (src/quality.cpp:60-65, include/trismooth/quality.hpp:78-89)
  */
 #ifndef TSG_H_
 #define TSG_H_
@@ -98,6 +104,17 @@ typedef struct {
   double node_kernel_ms; /* CUDA-event time summed over node-update launches (stream driver) */
   int64_t launches;      /* kernels launched by this call */
 } tsg_smooth_stats;
+
+/* Reductions of the quality audit (folds as the reference writes them: min / max start
+ * at 2.0 / -2.0, NaN never replaces, ties keep the first triangle; histogram bins of width
+ * 0.1 over [-1, 1], bin = (int)((alpha + 1) * 10) clamped to [0, 19]). */
+#define TSG_QUALITY_BINS 20
+typedef struct {
+  double min_alpha;
+  double max_alpha;
+  int64_t non_positive;               /* alpha <= 0 */
+  int64_t histogram[TSG_QUALITY_BINS];
+} tsg_quality_report;
 
 /* ---- context ---- */
 int32_t tsg_abi_version(void);
@@ -239,6 +256,17 @@ tsg_status tsg_debug_trace(void* out, int64_t bytes);
 /* order_out[s] = original id for slot s: vertices sorted along a Hilbert curve over the
  * bounding box (ties by original id).  Pure host code, deterministic. */
 tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
+
+/* ---- quality audit on the device (no tsg_mesh needed) ----
+ * tsg_quality_tri_alpha: alpha_out[t] = triangle_alpha of triangle t (bit-exact), plus the
+ * report (may be NULL).  xy: 2*nv interleaved, tri: 3*nt.  Corner ids are range-checked.
+ * tsg_quality_vertex_minima: vmin_out[v] = min of alpha[inc[j]] over v's row of the
+ * incident CSR (inc_off: nv+1 entries from 0), NaN for an empty row. */
+tsg_status tsg_quality_tri_alpha(tsg_context* ctx, int64_t nv, const double* xy, int64_t nt,
+                                 const int32_t* tri, double* alpha_out, tsg_quality_report* report);
+tsg_status tsg_quality_vertex_minima(tsg_context* ctx, int64_t nv, const int64_t* inc_off,
+                                     const int32_t* inc, int64_t nt, const double* alpha,
+                                     double* vmin_out);
 
 #ifdef __cplusplus
 }

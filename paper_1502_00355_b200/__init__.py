@@ -40,6 +40,10 @@ triangulate = _core.triangulate
 topology = _core.topology
 bbox_diagonal = _core.bbox_diagonal
 device_count = _core.device_count
+quality_report = _core.quality_report
+compute_all_qualities = _core.compute_all_qualities
+reduce_vertex_minima = _core.reduce_vertex_minima
+update_two_phase = _core.update_two_phase
 
 LIB_DIR = _HERE
 

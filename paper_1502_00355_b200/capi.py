@@ -34,7 +34,7 @@ EXPORTS = (
     "tsg_pass_lockstep", "tsg_smooth_host_batch", "tsg_hilbert_order", "tsg_selftest_alpha", "tsg_selftest_alpha_cycle", "tsg_pass", "tsg_halo_plan",
     "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
-    "tsg_debug_trace", "tsg_mesh_side_schedule",
+    "tsg_debug_trace", "tsg_mesh_side_schedule", "tsg_quality_tri_alpha", "tsg_quality_vertex_minima",
 )
 
 
@@ -49,6 +49,14 @@ class SmoothCfg(C.Structure):
     _fields_ = [("form", C.c_int32), ("strategy", C.c_int32), ("chunks", C.c_int32),
                 ("swap", C.c_int32), ("max_iters", C.c_int32), ("driver", C.c_int32),
                 ("move_tol", C.c_double), ("bbox_diag", C.c_double)]
+
+
+QUALITY_BINS = 20
+
+
+class QualityReport(C.Structure):
+    _fields_ = [("min_alpha", C.c_double), ("max_alpha", C.c_double), ("non_positive", C.c_int64),
+                ("histogram", C.c_int64 * QUALITY_BINS)]
 
 
 class SmoothStats(C.Structure):
@@ -103,6 +111,8 @@ def lib() -> C.CDLL:
             "tsg_dist_finalize": (i32, [P, C.POINTER(SmoothCfg), C.c_void_p, i32]),
             "tsg_dist_status": (i32, [P, P, P, P]),
             "tsg_dist_end": (i32, [P, C.POINTER(SmoothCfg), P, P, i32, P, P, P]),
+            "tsg_quality_tri_alpha": (i32, [P, i64, P, i64, P, P, C.POINTER(QualityReport)]),
+            "tsg_quality_vertex_minima": (i32, [P, i64, P, P, i64, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -148,6 +158,26 @@ class Context:
         check(lib().tsg_selftest_alpha_cycle(self.h, n, seed, C.byref(err), C.byref(bad)),
               "tsg_selftest_alpha_cycle")
         return err.value, bad.value
+
+    def quality_tri_alpha(self, xy, tri):
+        """Device quality audit of a bare (xy, tri) pair: (alpha per triangle, report dict)."""
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        alpha = np.empty(len(tri))
+        rep = QualityReport()
+        check(lib().tsg_quality_tri_alpha(self.h, len(xy), _ptr(xy), len(tri), _ptr(tri), _ptr(alpha),
+                                          C.byref(rep)), "tsg_quality_tri_alpha")
+        return alpha, dict(min_alpha=rep.min_alpha, max_alpha=rep.max_alpha, non_positive=rep.non_positive,
+                           histogram=list(rep.histogram))
+
+    def quality_vertex_minima(self, inc_off, inc, alpha):
+        inc_off = np.ascontiguousarray(inc_off, dtype=np.int64)
+        inc = np.ascontiguousarray(inc, dtype=np.int32)
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        out = np.empty(len(inc_off) - 1)
+        check(lib().tsg_quality_vertex_minima(self.h, len(out), _ptr(inc_off), _ptr(inc), len(alpha), _ptr(alpha),
+                                              _ptr(out)), "tsg_quality_vertex_minima")
+        return out
 
     def close(self):
         if self.h:

@@ -266,7 +266,14 @@ PYBIND11_MODULE(_trismooth, m) {
          const std::string& reorder, const std::string& swap, bool use_graph, bool detailed) {
         const SmoothConfig cfg = make_config(form, strategy, backend, workers, max_iters, move_tol,
                                              precision, reorder, swap, use_graph);
-        return stats_dict(smooth(mesh, cfg), detailed);
+        RunStats rs;
+        {
+          // the passes take the device for a while: let other Python threads run (calls on
+          // the shared device context are serialised inside libtsg)
+          py::gil_scoped_release nogil;
+          rs = smooth(mesh, cfg);
+        }
+        return stats_dict(rs, detailed);
       },
       py::arg("mesh"), py::arg("form") = "b", py::arg("strategy") = "twophase",
       py::arg("backend") = "serial", py::arg("workers") = 1, py::arg("max_iters") = 100,
@@ -274,35 +281,57 @@ PYBIND11_MODULE(_trismooth, m) {
       py::arg("swap") = "pingpong", py::arg("use_graph") = true, py::arg("detailed") = false,
       "Smooth in place on the GPU; returns run statistics.");
 
+  // quality_summary (proj/bindings/module.cpp:157-185): same keys and values; the α field and
+  // its min / max / non-positive count come from the device audit (csrc/tsg_quality.cu), the
+  // mean is the sequential sum in triangle order, the flags from the host topology.
   m.def(
       "quality_summary",
       [](Mesh& mesh) {
         init_flags(mesh);
-        compute_all_qualities(mesh);
+        const QualityReport q = audit_tri_alphas(mesh);
         const Adjacency adj = find_neighbors(mesh);
         determine_constraints(mesh, adj);
-        double lo = 2.0, hi = -2.0, sum = 0.0;
-        int nonpos = 0, pinned = 0;
+        int pinned = 0;
         mesh.visit([&](const auto& s) {
-          for (int t = 0; t < s.triangle_count(); ++t) {
-            const double q = s.tri_quality(t);
-            lo = std::min(lo, q);
-            hi = std::max(hi, q);
-            sum += q;
-            nonpos += q <= 0.0 ? 1 : 0;
-          }
           for (int v = 0; v < s.vertex_count(); ++v) pinned += s.is_boundary(v) ? 1 : 0;
         });
         py::dict d;
-        d["min_alpha"] = lo;
-        d["mean_alpha"] = sum / mesh.triangle_count();
-        d["max_alpha"] = hi;
-        d["non_positive"] = nonpos;
+        d["min_alpha"] = q.min_alpha;
+        d["mean_alpha"] = q.mean_alpha;
+        d["max_alpha"] = q.max_alpha;
+        d["non_positive"] = q.non_positive;
         d["boundary_vertices"] = pinned;
         d["interior_vertices"] = mesh.vertex_count() - pinned;
         return d;
       },
       py::arg("mesh"));
+
+  // B200 addition: the `trismooth quality` report (proj/tools/main.cpp:151-208) without the
+  // CLI: quality_summary's keys plus the 20-bin histogram, on the device.
+  m.def(
+      "quality_report",
+      [](Mesh& mesh) {
+        const QualityReport q = audit_tri_alphas(mesh);
+        py::dict d;
+        d["triangles"] = mesh.triangle_count();
+        d["vertices"] = mesh.vertex_count();
+        d["min_alpha"] = q.min_alpha;
+        d["mean_alpha"] = q.mean_alpha;
+        d["max_alpha"] = q.max_alpha;
+        d["non_positive"] = q.non_positive;
+        d["histogram_bins"] = q.histogram;
+        return d;
+      },
+      py::arg("mesh"));
+
+  m.def(
+      "compute_all_qualities", [](Mesh& mesh) { compute_all_qualities(mesh); }, py::arg("mesh"),
+      "α of every triangle into the mesh (device audit kernel).");
+  m.def(
+      "reduce_vertex_minima", [](Mesh& mesh) { reduce_vertex_minima(mesh); }, py::arg("mesh"),
+      "Per-vertex minimum of the stored incident α (device audit kernel); needs adjacency.");
+  m.def(
+      "update_two_phase", [](Mesh& mesh) { update_two_phase(mesh); }, py::arg("mesh"));
 
   m.def(
       "read_mesh",

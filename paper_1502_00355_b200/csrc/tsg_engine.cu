@@ -13,29 +13,19 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "tsg.h"
 #include "tsg_kernels.cuh"
+#include "tsg_internal.hpp"
 #include "tsg_prep.hpp"
 
 namespace {
 
-thread_local std::string g_err;
-
-tsg_status fail(tsg_status code, const std::string& msg) {
-  g_err = msg;
-  return code;
-}
-
-#define TSG_CUDA(call)                                                                  \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      return fail(e_ == cudaErrorMemoryAllocation ? TSG_ERR_NOMEM : TSG_ERR_CUDA,       \
-                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
-  } while (0)
+using tsg_abi::fail;
+using tsg_abi::g_err;
 
 // Valence tiers: thread-per-vertex (<= 12, CTA of 128, every slot in Form A), thread-per-vertex
 // over a list (13..31, CTA of 64: larger per-thread ring), CTA-per-vertex hubs (>= 32).
@@ -382,19 +372,6 @@ struct GraphCache {
 
 }  // namespace
 
-struct tsg_context {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  std::vector<cudaEvent_t> pass_events;  // stream-timed driver
-  // Side stream for the medium / hub tiers, forked from and joined back into `stream` so
-  // the tiers of one pass (or one Form B level) run concurrently (also inside graphs).
-  cudaStream_t side = nullptr;
-  cudaStream_t copy_in = nullptr, copy_out = nullptr;  // tsg_smooth_host_batch
-  cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
-  std::vector<cudaEvent_t> fork_events;
-  size_t fork_next = 0;
-};
 
 struct tsg_mesh {
   tsg_context* ctx = nullptr;
@@ -458,6 +435,8 @@ struct tsg_mesh {
   int64_t n_send = 0, n_recv = 0;
   double* d_halo_stage = nullptr;  // 2 * max(n_send, n_recv) doubles (host-pointer transfers)
 };
+
+#define TSG_LOCK_MESH(m) tsg_abi::CtxLock tsg_ctx_lock_((m) ? (m)->ctx : nullptr)
 
 namespace {
 
@@ -1030,6 +1009,7 @@ tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
 
 tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_t newton_steps,
                               double* max_abs_err_out, int64_t* nonfinite_out) {
+  TSG_LOCK_CTX(ctx);
   if (!ctx || n < 0) return fail(TSG_ERR_INVALID, "bad arguments");
   TSG_CUDA(cudaSetDevice(ctx->device));
   unsigned long long* d = nullptr;
@@ -1048,6 +1028,7 @@ tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_
 
 tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, double* max_abs_err_out,
                                     int64_t* nonfinite_out) {
+  TSG_LOCK_CTX(ctx);
   if (!ctx || n < 0) return fail(TSG_ERR_INVALID, "bad arguments");
   TSG_CUDA(cudaSetDevice(ctx->device));
   unsigned long long* d = nullptr;
@@ -1065,6 +1046,7 @@ tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, 
 }
 
 tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** out) {
+  TSG_LOCK_CTX(ctx);
   if (!ctx || !d || !out) return fail(TSG_ERR_INVALID, "null argument");
   if (!d->xy || !d->tri || !d->nbr_off || !d->nbr || !d->inc_off || !d->inc || !d->boundary)
     return fail(TSG_ERR_INVALID, "mesh description has null arrays");
@@ -1164,6 +1146,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
 }
 
 tsg_status tsg_mesh_free(tsg_mesh* m) {
+  TSG_LOCK_MESH(m);
   if (!m) return TSG_OK;
   cudaSetDevice(m->ctx->device);
   m->gc.reset();
@@ -1195,6 +1178,7 @@ tsg_status tsg_mesh_set_coords(tsg_mesh* m, const double* xy) {
 }
 
 tsg_status tsg_mesh_restore_coords(tsg_mesh* m) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   const size_t bytes = 2 * m->hm.nv * m->rsize;
@@ -1205,12 +1189,14 @@ tsg_status tsg_mesh_restore_coords(tsg_mesh* m) {
 }
 
 tsg_status tsg_mesh_get_coords(tsg_mesh* m, double* xy_out) {
+  TSG_LOCK_MESH(m);
   if (!m || !xy_out) return fail(TSG_ERR_INVALID, "null argument");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   return dispatch(m, [&](auto E) { return decltype(E)::get_coords(m, xy_out); });
 }
 
 tsg_status tsg_tri_alpha(tsg_mesh* m, double* alpha_out) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   cudaStream_t s = m->ctx->stream;
@@ -1244,6 +1230,7 @@ tsg_status tsg_tri_alpha(tsg_mesh* m, double* alpha_out) {
 }
 
 tsg_status tsg_vertex_minima(tsg_mesh* m, double* vmin_out) {
+  TSG_LOCK_MESH(m);
   if (!m || !vmin_out) return fail(TSG_ERR_INVALID, "null argument");
   tsg_status st = tsg_tri_alpha(m, nullptr);
   if (st) return st;
@@ -1264,6 +1251,7 @@ tsg_status tsg_vertex_minima(tsg_mesh* m, double* vmin_out) {
 }
 
 tsg_status tsg_alpha_extrema(tsg_mesh* m, double* min_out, double* max_out, int64_t* nonpos_out) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   tsg_status st = tsg_tri_alpha(m, nullptr);
   if (st) return st;
@@ -1355,6 +1343,7 @@ extern "C" {
 
 tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* stats,
                       int32_t* accepted_per_pass, double* max_disp_per_pass, int32_t capacity) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   tsg_status st = validate_cfg(c);
   if (st) return st;
@@ -1462,6 +1451,7 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
 
 tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy_in, const tsg_smooth_cfg* c,
                                  double* const* xy_out, int32_t* iterations_out, int32_t* stop_out) {
+  TSG_LOCK_MESH(m);
   if (!m || n < 0 || (n > 0 && (!xy_in || !xy_out))) return fail(TSG_ERR_INVALID, "bad batch arguments");
   tsg_status st = validate_cfg(c);
   if (st) return st;
@@ -1531,6 +1521,7 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
 tsg_status tsg_smooth_host(tsg_mesh* m, const double* xy_in, const tsg_smooth_cfg* c, double* xy_out,
                            tsg_smooth_stats* stats, int32_t* accepted_per_pass,
                            double* max_disp_per_pass, int32_t capacity) {
+  TSG_LOCK_MESH(m);
   if (!m || !xy_in || !xy_out) return fail(TSG_ERR_INVALID, "null argument");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::set_coords(m, xy_in); });
@@ -1541,6 +1532,7 @@ tsg_status tsg_smooth_host(tsg_mesh* m, const double* xy_in, const tsg_smooth_cf
 
 tsg_status tsg_pass_lockstep(tsg_mesh* m, int32_t form, int32_t chunks, int8_t* decision_out,
                              int32_t* accepted_out, double* max_disp_out) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   tsg_smooth_cfg c{};
   c.form = form;
@@ -1586,6 +1578,7 @@ tsg_status tsg_pass_lockstep(tsg_mesh* m, int32_t form, int32_t chunks, int8_t* 
 }
 
 tsg_status tsg_pass(tsg_mesh* m, const tsg_smooth_cfg* c, int32_t* accepted_out, double* max_disp_out) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   tsg_status st = validate_cfg(c);
   if (st) return st;
@@ -1624,6 +1617,7 @@ tsg_status tsg_pass(tsg_mesh* m, const tsg_smooth_cfg* c, int32_t* accepted_out,
 
 tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, const int64_t* recv_ids,
                          int64_t n_recv) {
+  TSG_LOCK_MESH(m);
   if (!m || n_send < 0 || n_recv < 0 || (n_send && !send_ids) || (n_recv && !recv_ids))
     return fail(TSG_ERR_INVALID, "bad halo plan");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
@@ -1653,6 +1647,7 @@ tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, c
 }
 
 tsg_status tsg_mesh_side_schedule(tsg_mesh* m, int32_t mode) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   if (mode < TSG_SIDE_AUTO || mode > TSG_SIDE_PERSIST) return fail(TSG_ERR_INVALID, "unknown side-row schedule");
   if (m->side_mode != mode) {
@@ -1663,6 +1658,7 @@ tsg_status tsg_mesh_side_schedule(tsg_mesh* m, int32_t mode) {
 }
 
 tsg_status tsg_mesh_formb_schedule(tsg_mesh* m, int32_t mode) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   if (mode < TSG_FORMB_AUTO || mode > TSG_FORMB_CHUNKS) return fail(TSG_ERR_INVALID, "unknown Form B schedule");
   if (m->fb_mode != mode) {
@@ -1674,6 +1670,7 @@ tsg_status tsg_mesh_formb_schedule(tsg_mesh* m, int32_t mode) {
 }
 
 tsg_status tsg_dist_begin(tsg_mesh* m, const tsg_smooth_cfg* c) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   tsg_status st = validate_cfg(c);
   if (st) return st;
@@ -1691,6 +1688,7 @@ tsg_status tsg_dist_begin(tsg_mesh* m, const tsg_smooth_cfg* c) {
 }
 
 tsg_status tsg_dist_pass(tsg_mesh* m, const tsg_smooth_cfg* c, double* stats_dev) {
+  TSG_LOCK_MESH(m);
   if (!m || !stats_dev) return fail(TSG_ERR_INVALID, "null argument");
   tsg_status st = validate_cfg(c);
   if (st) return st;
@@ -1709,6 +1707,7 @@ tsg_status tsg_dist_pass(tsg_mesh* m, const tsg_smooth_cfg* c, double* stats_dev
 }
 
 tsg_status tsg_dist_halo_pack(tsg_mesh* m, const tsg_smooth_cfg* c, double* out_dev) {
+  TSG_LOCK_MESH(m);
   if (!m || !c || (m->n_send && !out_dev)) return fail(TSG_ERR_INVALID, "bad halo pack arguments");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   if (m->n_send == 0) return TSG_OK;
@@ -1731,6 +1730,7 @@ tsg_status tsg_dist_halo_pack(tsg_mesh* m, const tsg_smooth_cfg* c, double* out_
 }
 
 tsg_status tsg_dist_halo_unpack(tsg_mesh* m, const double* in_dev) {
+  TSG_LOCK_MESH(m);
   if (!m || (m->n_recv && !in_dev)) return fail(TSG_ERR_INVALID, "bad halo unpack arguments");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   if (m->n_recv == 0) return TSG_OK;
@@ -1753,6 +1753,7 @@ tsg_status tsg_dist_halo_unpack(tsg_mesh* m, const double* in_dev) {
 }
 
 tsg_status tsg_dist_finalize(tsg_mesh* m, const tsg_smooth_cfg* c, const double* gathered_dev, int32_t n_parts) {
+  TSG_LOCK_MESH(m);
   if (!m || !c || !gathered_dev || n_parts < 1) return fail(TSG_ERR_INVALID, "bad finalize arguments");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
@@ -1764,6 +1765,7 @@ tsg_status tsg_dist_finalize(tsg_mesh* m, const tsg_smooth_cfg* c, const double*
 }
 
 tsg_status tsg_dist_status(tsg_mesh* m, int32_t* iterations, int32_t* done, int32_t* stop) {
+  TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   tsg::PassState hs;
@@ -1777,6 +1779,7 @@ tsg_status tsg_dist_status(tsg_mesh* m, int32_t* iterations, int32_t* done, int3
 
 tsg_status tsg_dist_end(tsg_mesh* m, const tsg_smooth_cfg* c, int32_t* accepted_per_pass, double* max_disp_per_pass,
                         int32_t capacity, int32_t* iterations_out, int32_t* stop_out, int64_t* launches_out) {
+  TSG_LOCK_MESH(m);
   if (!m || !c) return fail(TSG_ERR_INVALID, "null argument");
   int32_t it = 0, done = 0, stop = 0;
   tsg_status st = tsg_dist_status(m, &it, &done, &stop);
@@ -1798,6 +1801,7 @@ tsg_status tsg_dist_end(tsg_mesh* m, const tsg_smooth_cfg* c, int32_t* accepted_
 }
 
 tsg_status tsg_halo_pack(tsg_mesh* m, double* out, int32_t out_is_host) {
+  TSG_LOCK_MESH(m);
   if (!m || (m->n_send && !out)) return fail(TSG_ERR_INVALID, "bad halo pack arguments");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   cudaStream_t s = m->ctx->stream;
@@ -1822,6 +1826,7 @@ tsg_status tsg_halo_pack(tsg_mesh* m, double* out, int32_t out_is_host) {
 }
 
 tsg_status tsg_halo_unpack(tsg_mesh* m, const double* in, int32_t in_is_host) {
+  TSG_LOCK_MESH(m);
   if (!m || (m->n_recv && !in)) return fail(TSG_ERR_INVALID, "bad halo unpack arguments");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   cudaStream_t s = m->ctx->stream;

@@ -197,10 +197,58 @@ void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
   for (int64_t s = 0; s < nv; ++s) order_out[s] = static_cast<int64_t>(keys[s] & 0xffffffffu);
 }
 
+// Structural checks of a caller-supplied description before anything indexes through it
+// (the reference's build_mesh raises StructuralError on the same conditions,
+// proj/src/mesh.cpp:69-81): corner ids in range, CSR offsets starting at 0 and
+// non-decreasing, entries in range, neighbour rows strictly ascending.  Runs in parallel
+// chunks; returns the first problem found.
+static std::string validate_desc(const tsg_mesh_desc& d) {
+  const int64_t nv = d.nv, nt = d.nt;
+  std::atomic<int> bad{0};  // bit 0 tri, 1 nbr, 2 inc
+  parallel_ranges(nt, [&](int64_t b, int64_t e) {
+    for (int64_t i = 3 * b; i < 3 * e; ++i)
+      if (d.tri[i] < 0 || d.tri[i] >= nv) {
+        bad.fetch_or(1);
+        return;
+      }
+  });
+  if (bad.load() & 1) return "triangle corner index out of range";
+  if (d.nbr_off[0] != 0 || d.inc_off[0] != 0) return "CSR offsets must start at 0";
+  parallel_ranges(nv, [&](int64_t b, int64_t e) {
+    for (int64_t v = b; v < e; ++v) {
+      const int64_t n0 = d.nbr_off[v], n1 = d.nbr_off[v + 1];
+      const int64_t i0 = d.inc_off[v], i1 = d.inc_off[v + 1];
+      if (n1 < n0) {
+        bad.fetch_or(2);
+        return;
+      }
+      if (i1 < i0) {
+        bad.fetch_or(4);
+        return;
+      }
+      for (int64_t j = n0; j < n1; ++j)
+        if (d.nbr[j] < 0 || d.nbr[j] >= nv || (j > n0 && d.nbr[j] <= d.nbr[j - 1])) {
+          bad.fetch_or(2);
+          return;
+        }
+      for (int64_t j = i0; j < i1; ++j)
+        if (d.inc[j] < 0 || d.inc[j] >= nt) {
+          bad.fetch_or(4);
+          return;
+        }
+    }
+  });
+  const int f = bad.load();
+  if (f & 2) return "neighbour CSR malformed (offsets decreasing, id out of range or row not strictly ascending)";
+  if (f & 4) return "incident CSR malformed (offsets decreasing or triangle id out of range)";
+  return {};
+}
+
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm) {
   const int64_t nv = d.nv, nt = d.nt;
   if (nv <= 0 || nt <= 0) return "mesh must have vertices and triangles";
   if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
+  if (std::string e = validate_desc(d); !e.empty()) return e;
   hm.nv = nv;
   hm.nt = nt;
   hm.order.resize(nv);

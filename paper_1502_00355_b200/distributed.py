@@ -150,6 +150,7 @@ class DeviceEngine:
         self.part = part
 
     def run_pass(self, cfg):
+        _require_form_a(cfg)
         return self.mesh.run_pass(cfg)
 
     def pack(self, buf):
@@ -200,9 +201,18 @@ class Exchanger:
         return int(self.stat_sum.item()), float(self.stat_max.item())
 
 
+def _require_form_a(cfg):
+    """Partitions are exact for Form A only: a Form B vertex reads in-chunk values written
+    earlier in the same pass, so a partition boundary inside a chunk would change results."""
+    if cfg.form != 0:
+        raise ValueError("partitioned smoothing supports Form A only (Form B reads live in-chunk "
+                         "values; see DESIGN.md §6)")
+
+
 def smooth_partitioned(engine, exchanger: Exchanger, cfg, max_iters: int, move_tol: float, bbox_diag: float):
     """The reference pass loop (src/smoothing.cpp:98-141) over partitions.  Returns
     (iterations, stop, accepted_per_pass, max_disp_per_pass)."""
+    _require_form_a(cfg)
     tol_abs = move_tol * bbox_diag
     accepted, max_disp = [], []
     stop = "max_iters"

@@ -126,3 +126,66 @@ def test_smooth_host_batch_with_persistent_side_rows(capi, gpu_ctx, ts, port):
         want = port.smooth(ins[k], tri, form="a", max_iters=12, move_tol=0.0)
         assert np.array_equal(outs[k].view(np.uint64), want.xy.view(np.uint64)), k
     dm.free()
+
+
+def test_upload_rejects_malformed_descriptions(capi, gpu_ctx, ts):
+    """tsg_mesh_upload validates caller arrays before indexing through them (the reference's
+    build_mesh raises StructuralError on bad corner ids, proj/src/mesh.cpp:69-81)."""
+    xy, tri = ts.delaunay_arrays(500, 1)
+    topo = ts.topology(len(xy), tri)
+
+    def upload(tri_=tri, **over):
+        t = {k: np.array(v, copy=True) for k, v in topo.items()}
+        t.update(over)
+        return capi.DeviceMesh(gpu_ctx, xy, tri_, t)
+
+    bad_tri = tri.copy()
+    bad_tri[3, 1] = len(xy)
+    with pytest.raises(RuntimeError, match="corner index out of range"):
+        upload(bad_tri)
+    nbr = topo["nbr"].copy()
+    r = int(np.argmax(np.diff(topo["nbr_off"]) > 2))
+    a = int(topo["nbr_off"][r])
+    nbr[a], nbr[a + 1] = nbr[a + 1], nbr[a]
+    with pytest.raises(RuntimeError, match="neighbour CSR malformed"):
+        upload(nbr=nbr)
+    inc = topo["inc"].copy()
+    inc[7] = len(tri) + 3
+    with pytest.raises(RuntimeError, match="incident CSR malformed"):
+        upload(inc=inc)
+    off = topo["inc_off"].copy()
+    off[10] = off[12]
+    with pytest.raises(RuntimeError, match="incident CSR malformed"):
+        upload(inc_off=off)
+    upload().free()  # the untouched description still uploads
+
+
+def test_concurrent_smooth_calls_share_the_default_context(ts):
+    """The drop-in smooth() shares one process-wide device context; concurrent calls on
+    distinct meshes from several host threads (the GIL is released) give the sequential
+    results (tsg_context::mu serialises the C-ABI calls)."""
+    import threading
+
+    seeds = [3, 4, 5, 6]
+    want = []
+    for s in seeds:
+        m = ts.generate_delaunay(8000, seed=s)
+        ts.smooth(m, form="a", max_iters=20, move_tol=0.0)
+        want.append(m.points())
+    meshes = [ts.generate_delaunay(8000, seed=s) for s in seeds]
+    errors = []
+
+    def work(m):
+        try:
+            ts.smooth(m, form="a", max_iters=20, move_tol=0.0)
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(m,)) for m in meshes]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for m, w in zip(meshes, want):
+        assert m.points() == w

@@ -36,14 +36,18 @@ def test_triangle_alpha_values():
     assert ts.triangle_alpha((0, 0), (0, 1), (1, 0)) == pytest.approx(-math.sqrt(3) / 2)
 
 
-def test_quality_summary_keys():
+def test_quality_audit_needs_the_device():
+    """quality_summary / compute_all_qualities run on the device audit kernels: without a
+    CUDA device they raise (no CPU fallback).  GPU parity: tests/test_gpu_quality.py."""
+    import paper_1502_00355_b200 as core
+
+    if core.device_count() > 0:
+        pytest.skip("a CUDA device is visible; covered by test_gpu_quality.py")
     m = ts.generate_delaunay(200, seed=2)
-    q = ts.quality_summary(m)
-    assert set(q) == {"min_alpha", "mean_alpha", "max_alpha", "non_positive", "boundary_vertices",
-                      "interior_vertices"}
-    assert -1.0 <= q["min_alpha"] <= q["mean_alpha"] <= q["max_alpha"] <= 1.0
-    assert q["non_positive"] == 0
-    assert q["boundary_vertices"] + q["interior_vertices"] == m.vertex_count
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        ts.quality_summary(m)
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        core.compute_all_qualities(m)
 
 
 def test_file_round_trip(tmp_path):
