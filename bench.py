@@ -89,7 +89,8 @@ def algorithmic_bytes_per_pass(nv, nt, sum_deg, precision):
 
 def roofline_kernel(cfg):
     if cfg["form"] == "b":
-        return "Form B: formb_chunk_update / node_update level kernels"
+        return ("Form B: formb_flow (dataflow over (vertex, pass), AUTO on deep narrow level structures) "
+                "or formb_chunk_update / node_update level kernels")
     return ("tile_update (tile-staged, thread per vertex, valence <= 31) + side_rows (valence >= 32, "
             "persistent beside the tile grid) or warp_update / hub_fast_update grids (AUTO)")
 
@@ -432,6 +433,8 @@ def main():
     ap.add_argument("--swap", choices=["pingpong", "copy"], default="pingpong")
     ap.add_argument("--chunks", type=int, default=None)
     ap.add_argument("--no-reorder", action="store_true")
+    ap.add_argument("--formb-schedule", choices=["auto", "levels", "chunks", "flow"], default="auto",
+                    help="Form B schedule (identical results): AUTO = the dataflow kernel for smooth()")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=2.0, help="reference arm: target seconds of passes per step")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no e2e / baseline")
@@ -485,6 +488,8 @@ def main():
     ctx = capi.Context(local_rank)
     dm = capi.DeviceMesh(ctx, xy, tri, topo, layout=cfg["layout"], precision=cfg["precision"], order=order)
     prep_s = time.time() - t0
+    if cfg["form"] == "b":
+        dm.formb_schedule(args.formb_schedule)
     deg = np.diff(topo["nbr_off"])
     sum_deg = int(topo["nbr_off"][-1])
     movable = topo["boundary"] == 0

@@ -218,11 +218,14 @@ tsg_status tsg_dist_end(tsg_mesh* mesh, const tsg_smooth_cfg* cfg, int32_t* acce
                         double* max_disp_per_pass, int32_t capacity, int32_t* iterations_out, int32_t* stop_out,
                         int64_t* launches_out);
 
-/* Form B schedule: AUTO (default) walks the dependency levels inside one CTA per chunk when the
- * per-level cost model says so (narrow levels per chunk: serial Form B, or many chunks on a deep
- * level structure), else launches one set of tier kernels per level; LEVELS / CHUNKS force one
- * of the two (identical results). */
-enum { TSG_FORMB_AUTO = 0, TSG_FORMB_LEVELS = 1, TSG_FORMB_CHUNKS = 2 };
+/* Form B schedule (identical results; tsg_smooth only — the batch and partitioned entry points
+ * use LEVELS / CHUNKS):
+ *   LEVELS  one set of tier kernels per dependency level of each pass;
+ *   CHUNKS  one CTA per chunk walking its levels, one launch per pass;
+ *   FLOW    one persistent launch for many passes: (vertex, pass) dataflow with per-vertex
+ *           pass counters, so pass q+1 pipelines behind pass q (tsg_flow.cuh);
+ *   AUTO    (default) FLOW for tsg_smooth, else CHUNKS or LEVELS by the per-level cost model. */
+enum { TSG_FORMB_AUTO = 0, TSG_FORMB_LEVELS = 1, TSG_FORMB_CHUNKS = 2, TSG_FORMB_FLOW = 3 };
 tsg_status tsg_mesh_formb_schedule(tsg_mesh* mesh, int32_t mode);
 
 /* Form A fused, rows of valence >= 32 (the paper's high-valence nodes): AUTO (default) runs them

@@ -329,7 +329,7 @@ class DeviceMesh:
     def formb_schedule(self, mode: str):
         """Form B schedule: "auto", "levels" (a launch per dependency level) or "chunks" (one CTA
         per chunk walking its levels).  Results are identical."""
-        check(lib().tsg_mesh_formb_schedule(self.h, {"auto": 0, "levels": 1, "chunks": 2}[mode]),
+        check(lib().tsg_mesh_formb_schedule(self.h, {"auto": 0, "levels": 1, "chunks": 2, "flow": 3}[mode]),
               "tsg_mesh_formb_schedule")
 
     def side_schedule(self, mode: str):

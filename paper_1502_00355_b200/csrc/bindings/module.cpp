@@ -8,7 +8,12 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <csignal>
+#include <cstdlib>
 #include <cstring>
+
+#include <execinfo.h>
+#include <unistd.h>
 
 #include "trismooth/gpu.hpp"
 #include "trismooth/io.hpp"
@@ -142,8 +147,20 @@ gpu::Topology64 topology_from_dict(const py::dict& t) {
 
 }  // namespace
 
+namespace {
+// TSG_SEGV_TRACE=1: print the native stack of a crashing thread (debug aid; glibc backtrace).
+void segv_trace(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  backtrace_symbols_fd(frames, n, 2);
+  std::signal(sig, SIG_DFL);
+  std::raise(sig);
+}
+}  // namespace
+
 PYBIND11_MODULE(_trismooth, m) {
   m.doc() = "Smart Laplacian smoothing of planar triangular meshes (B200 engine)";
+  if (std::getenv("TSG_SEGV_TRACE")) std::signal(SIGSEGV, segv_trace);
 
   py::class_<Mesh>(m, "Mesh")
       .def_property_readonly("vertex_count", &Mesh::vertex_count)

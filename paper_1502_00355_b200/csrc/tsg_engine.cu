@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "tsg.h"
+#include "tsg_flow.cuh"
 #include "tsg_kernels.cuh"
 #include "tsg_internal.hpp"
 #include "tsg_prep.hpp"
@@ -424,8 +425,13 @@ struct tsg_mesh {
   std::vector<tsg::Phase> fb_levels;
   int32_t *d_cb_order = nullptr, *d_cb_lvl = nullptr, *d_cb_chunk = nullptr;  // chunk schedule
   uint32_t* d_cb_rec = nullptr;
+  uint32_t* d_flow_rec = nullptr;   // dataflow schedule (tsg_flow.cuh): records in level order
+  uint32_t* d_flow_done = nullptr;  // per slot: passes completed in the running launch
+  void* d_flow_save = nullptr;      // round-start coordinates (displacement-stop replay)
+  int64_t flow_n = 0;
   int64_t fb_nchunks = 0;
   bool fb_use_chunks = false;  // narrow levels: one CTA per chunk instead of a launch per level
+  bool fb_auto_flow = false;   // AUTO picks the dataflow kernel for tsg_smooth (cost model)
   int32_t fb_mode = TSG_FORMB_AUTO;
   int64_t fb_bytes = 0;
   GraphCache gc;
@@ -451,8 +457,13 @@ void free_form_b(tsg_mesh* m) {
   cudaFree(m->d_cb_lvl);
   cudaFree(m->d_cb_chunk);
   cudaFree(m->d_cb_rec);
+  cudaFree(m->d_flow_rec);
+  cudaFree(m->d_flow_done);
+  cudaFree(m->d_flow_save);
   m->d_cb_order = m->d_cb_lvl = m->d_cb_chunk = nullptr;
-  m->d_cb_rec = nullptr;
+  m->d_cb_rec = m->d_flow_rec = m->d_flow_done = nullptr;
+  m->d_flow_save = nullptr;
+  m->flow_n = 0;
   m->d_nbr_fresh = nullptr;
   m->bytes -= m->fb_bytes;
   m->fb_bytes = 0;
@@ -478,6 +489,12 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   if ((st = upload(&m->d_cb_lvl, sch.lvl_off, &b, s))) return st;
   if ((st = upload(&m->d_cb_chunk, sch.chunk_lvl, &b, s))) return st;
   if ((st = upload(&m->d_cb_rec, sch.cb_rec, &b, s))) return st;
+  if ((st = upload(&m->d_flow_rec, sch.flow_rec, &b, s))) return st;
+  m->flow_n = static_cast<int64_t>(sch.flow_rec.size() / tsg::kChunkRecWords);
+  TSG_CUDA(cudaMalloc(&m->d_flow_done, sizeof(uint32_t) * m->hm.nv));
+  TSG_CUDA(cudaMemsetAsync(m->d_flow_done, 0xff, sizeof(uint32_t) * m->hm.nv, s));  // pinned: ~0u
+  TSG_CUDA(cudaMalloc(&m->d_flow_save, 2 * m->hm.nv * m->rsize));
+  b += static_cast<int64_t>(sizeof(uint32_t) * m->hm.nv + 2 * m->hm.nv * m->rsize);
   TSG_CUDA(cudaStreamSynchronize(s));
   m->fb_nchunks = static_cast<int64_t>(sch.chunk_lvl.size()) - 1;
   {
@@ -491,12 +508,21 @@ tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
     const double w_total = nlev ? double(movable) / nlev : 0.0;
     const double w_chunk = nlev && m->fb_nchunks ? w_total / double(m->fb_nchunks) : 0.0;
     const bool chunks_faster = nlev > 0 && 2.4 + 0.04 * w_chunk < 6.0 + 8e-5 * w_total;
-    m->fb_use_chunks = m->fb_mode == TSG_FORMB_AUTO ? chunks_faster : m->fb_mode == TSG_FORMB_CHUNKS;
+    m->fb_use_chunks = (m->fb_mode == TSG_FORMB_AUTO || m->fb_mode == TSG_FORMB_FLOW) ? chunks_faster
+                                                                                  : m->fb_mode == TSG_FORMB_CHUNKS;
+    // Dataflow kernel (tsg_smooth only), fitted on B200: per pass ~ max(0.36 us x levels (the
+    // pipelined critical path: cfg1 serial, 195 levels -> 69 us), 0.68 ns x movable vertices
+    // (throughput: cfg2 1M, W = 1 / 148 -> 0.72 / 0.64 ms)).  Per-level launches: 6 us x levels +
+    // 8e-5 us x movable; per-chunk CTAs as above.
+    const double levels_us = 6.0 * nlev + 8e-5 * movable;
+    const double chunks_us = nlev * (2.4 + 0.04 * w_chunk);
+    const double flow_us = std::max(0.36 * nlev, 6.8e-4 * movable);
+    m->fb_auto_flow = nlev > 0 && flow_us < std::min(levels_us, chunks_us);
     if (std::getenv("TSG_DIAG"))
       std::fprintf(stderr, "[tsg] Form B W=%d: %lld levels, %lld chunks, mean level width %.0f (%.1f per chunk) -> %s\n",
                    chunks, static_cast<long long>(nlev), static_cast<long long>(m->fb_nchunks),
                    w_total, w_chunk,
-                   m->fb_use_chunks ? "chunks" : "levels");
+                   m->fb_auto_flow ? "flow" : m->fb_use_chunks ? "chunks" : "levels");
   }
   m->fb_levels = std::move(sch.levels);
   m->fb_bytes = b;
@@ -823,7 +849,15 @@ struct Engine {
   static tsg_status enqueue_pass(tsg_mesh* m, const tsg_smooth_cfg& c, cudaStream_t s, double tol_abs,
                                  cudaGraphConditionalHandle h, int use_handle, int8_t* decision,
                                  cudaEvent_t e0, cudaEvent_t e1, int64_t* kernels, bool fin = true) {
-    const bool fb = c.form == TSG_FORM_B, tp = c.strategy == TSG_STRATEGY_TWOPHASE;
+    // UpdateStrategy changes the reference's schedule, never its results: TwoPhase reads the
+    // threshold from the α field refreshed at the end of the previous pass
+    // (proj/src/smoothing.cpp:119-120), Fused recomputes the same minimum from the pass-start
+    // coordinates (proj/tests/acceptance.cpp:146-193 checks Fused == TwoPhase
+    // bitwise).  Both run the fused kernels here: the per-pass α sweep and its 8-byte-per-
+    // triangle field are not needed, and the final field is computed once for write-back
+    // (tsg_tri_alpha).  TSG_TWOPHASE_SWEEP=1 keeps the literal two-phase schedule (tests).
+    static const bool literal = std::getenv("TSG_TWOPHASE_SWEEP") != nullptr;
+    const bool fb = c.form == TSG_FORM_B, tp = literal && c.strategy == TSG_STRATEGY_TWOPHASE;
     if (fb && tp) return enqueue_pass_t<true, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
     if (fb) return enqueue_pass_t<true, false>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
     if (tp) return enqueue_pass_t<false, true>(m, c, s, tol_abs, h, use_handle, decision, e0, e1, kernels, fin);
@@ -882,6 +916,45 @@ struct Engine {
                                m->ctx->stream));
       m->cur = 0;
     }
+    return TSG_OK;
+  }
+
+  // One launch of the Form B dataflow kernel over passes [p0, p0 + np) (tsg_flow.cuh).
+  // Cooperative launch: every CTA is co-resident (the kernel's progress argument needs it).
+  static tsg_status flow_launch(tsg_mesh* m, int32_t p0, int32_t np, int64_t* kernels) {
+    cudaStream_t s = m->ctx->stream;
+    const int64_t n = m->flow_n;
+    if (n == 0 || np <= 0) return TSG_OK;
+    tsg::flow_reset<<<grid_for(n, 256), 256, 0, s>>>(m->d_flow_rec, n, m->d_flow_done);
+    TSG_CUDA(cudaGetLastError());
+    int per_sm = 0, sms = 0;
+    constexpr size_t smem = tsg::flow_smem_bytes<R>();
+    TSG_CUDA(cudaFuncSetAttribute(tsg::formb_flow<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsg::formb_flow<R, kSoA>, tsg::kFlowBlock, smem));
+    TSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->ctx->device));
+    const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * sms;
+    const int64_t want = (n + tsg::kFlowBlock - 1) / tsg::kFlowBlock;
+    const unsigned grid = static_cast<unsigned>(std::min(cap, want));
+    tsg::FlowArgs<R> f{};
+    f.buf0 = static_cast<R*>(m->buf[0]);
+    f.buf1 = static_cast<R*>(m->buf[1]);
+    f.nv = m->hm.nv;
+    f.rec = m->d_flow_rec;
+    f.off = m->d_off;
+    f.nbr = m->d_nbr_fresh;
+    f.fan = m->d_fan;
+    f.done = m->d_flow_done;
+    f.n = n;
+    f.p0 = p0;
+    f.np = np;
+    f.slot_acc = m->d_sacc;
+    f.slot_md = m->d_smd;
+    f.maxabs = m->d_maxabs;
+    void* args[] = {&f};
+    TSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tsg::formb_flow<R, kSoA>), dim3(grid),
+                                         dim3(tsg::kFlowBlock), args, smem, s));
+    *kernels += 2;
     return TSG_OK;
   }
 
@@ -1337,6 +1410,84 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
   return TSG_OK;
 }
 
+// Form B through the dataflow kernel: rounds of up to kFlowRound passes per launch when the
+// displacement stop is live (move_tol > 0), else every pass in one launch.  The stop rule
+// (proj/src/smoothing.cpp:132-141) is applied to each round's per-pass totals in the
+// reference's order; a NoMoves pass leaves the state unchanged, so the passes the launch ran
+// after it are no-ops; a Displacement stop inside a round replays the round from its saved
+// start up to the stopping pass (deterministic, so identical statistics).
+constexpr int32_t kFlowRound = 64;
+
+bool flow_selected(const tsg_mesh* m, const tsg_smooth_cfg* c) {
+  if (c->form != TSG_FORM_B) return false;
+  if (m->fb_mode == TSG_FORMB_FLOW) return true;
+  // AUTO: the dataflow kernel where the level schedules are latency-bound — deep, narrow level
+  // structures (cfg1 serial Form B: 195 levels of ~50 vertices per pass); wide levels stay on
+  // the per-level / per-chunk launches (cost model in ensure_form_b).
+  return m->fb_mode == TSG_FORMB_AUTO && m->flow_n > 0 && m->fb_auto_flow;
+}
+
+tsg_status smooth_flow(tsg_mesh* m, const tsg_smooth_cfg* c, double tol_abs, int32_t* it_out, int32_t* stop_out,
+                       std::vector<int32_t>& acc, std::vector<unsigned long long>& md, int64_t* kernels) {
+  cudaStream_t s = m->ctx->stream;
+  const int32_t P = c->max_iters;
+  const int32_t round = tol_abs > 0.0 ? kFlowRound : P;
+  const size_t coord_bytes = 2 * static_cast<size_t>(m->hm.nv) * m->rsize;
+  acc.assign(P, 0);
+  md.assign(P, 0ULL);
+  std::vector<int32_t> sa;
+  std::vector<unsigned long long> sm;
+  int32_t p0 = 0;
+  *it_out = P;
+  *stop_out = tsg::kStopMaxIters;
+  while (p0 < P) {
+    const int32_t np = std::min(round, P - p0);
+    const bool may_replay = tol_abs > 0.0 && np > 1;
+    if (may_replay)
+      TSG_CUDA(cudaMemcpyAsync(m->d_flow_save, m->buf[p0 & 1], coord_bytes, cudaMemcpyDeviceToDevice, s));
+    tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::flow_launch(m, p0, np, kernels); });
+    if (st) return st;
+    sa.resize(static_cast<size_t>(np) * tsg::kStatSlots);
+    sm.resize(static_cast<size_t>(np) * tsg::kStatSlots);
+    TSG_CUDA(cudaMemcpyAsync(sa.data(), m->d_sacc + static_cast<size_t>(p0) * tsg::kStatSlots,
+                             sizeof(int32_t) * sa.size(), cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaMemcpyAsync(sm.data(), m->d_smd + static_cast<size_t>(p0) * tsg::kStatSlots,
+                             sizeof(unsigned long long) * sm.size(), cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    int32_t stop_at = -1;
+    for (int32_t j = 0; j < np && stop_at < 0; ++j) {
+      int32_t a = 0;
+      unsigned long long b = 0;
+      for (int k = 0; k < tsg::kStatSlots; ++k) {
+        a += sa[static_cast<size_t>(j) * tsg::kStatSlots + k];
+        b = std::max(b, sm[static_cast<size_t>(j) * tsg::kStatSlots + k]);
+      }
+      acc[p0 + j] = a;
+      md[p0 + j] = b;
+      double d;
+      std::memcpy(&d, &b, sizeof d);
+      if (a == 0) {
+        stop_at = j;
+        *stop_out = tsg::kStopNoMoves;
+      } else if (d < tol_abs) {
+        stop_at = j;
+        *stop_out = tsg::kStopDisplacement;
+      }
+    }
+    if (stop_at >= 0) {
+      if (*stop_out == tsg::kStopDisplacement && stop_at + 1 < np) {
+        TSG_CUDA(cudaMemcpyAsync(m->buf[p0 & 1], m->d_flow_save, coord_bytes, cudaMemcpyDeviceToDevice, s));
+        st = dispatch(m, [&](auto E) { return decltype(E)::flow_launch(m, p0, stop_at + 1, kernels); });
+        if (st) return st;
+      }
+      *it_out = p0 + stop_at + 1;
+      break;
+    }
+    p0 += np;
+  }
+  return TSG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1359,6 +1510,45 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   TSG_CUDA(cudaMemsetAsync(m->d_sacc, 0, sizeof(int32_t) * tsg::kStatSlots * c->max_iters, s));
   TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
   if (diag_enabled()) TSG_CUDA(cudaMemsetAsync(m->d_rare, 0, sizeof(unsigned long long) * (m->cap + 16), s));
+
+  if (flow_selected(m, c)) {
+    std::vector<int32_t> acc;
+    std::vector<unsigned long long> md;
+    int32_t it = 0, stop = 0;
+    int64_t kernels = 0;
+    TSG_CUDA(cudaEventRecord(ctx->ev0, s));
+    if ((st = smooth_flow(m, c, tol_abs, &it, &stop, acc, md, &kernels))) return st;
+    TSG_CUDA(cudaEventRecord(ctx->ev1, s));
+    // final coordinates are in buf[it & 1]; copy mode keeps them in buf[0]
+    if (c->swap == TSG_SWAP_COPY && (it & 1)) {
+      st = dispatch(m, [&](auto E) {
+        m->cur = 1;
+        return decltype(E)::normalize(m);
+      });
+      if (st) return st;
+    } else {
+      m->cur = c->swap == TSG_SWAP_PINGPONG ? (it & 1) : 0;
+    }
+    const tsg::PassState hs{it, 1, stop, 0};
+    TSG_CUDA(cudaMemcpyAsync(m->d_state, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    float total_ms = 0.f;
+    TSG_CUDA(cudaEventElapsedTime(&total_ms, ctx->ev0, ctx->ev1));
+    const int32_t n = std::min(capacity, it);
+    for (int32_t p = 0; p < n; ++p) {
+      if (accepted_per_pass) accepted_per_pass[p] = acc[p];
+      if (max_disp_per_pass) std::memcpy(max_disp_per_pass + p, &md[p], sizeof(double));
+    }
+    if (stats) {
+      stats->iterations = it;
+      stats->stop = stop;
+      stats->node_updates = m->hm.nv * static_cast<int64_t>(it);
+      stats->device_ms = total_ms;
+      stats->node_kernel_ms = total_ms;
+      stats->launches = kernels;
+    }
+    return TSG_OK;
+  }
 
   int64_t kernels_per_pass = 0;
   double node_ms = -1.0;
@@ -1660,7 +1850,7 @@ tsg_status tsg_mesh_side_schedule(tsg_mesh* m, int32_t mode) {
 tsg_status tsg_mesh_formb_schedule(tsg_mesh* m, int32_t mode) {
   TSG_LOCK_MESH(m);
   if (!m) return fail(TSG_ERR_INVALID, "null mesh");
-  if (mode < TSG_FORMB_AUTO || mode > TSG_FORMB_CHUNKS) return fail(TSG_ERR_INVALID, "unknown Form B schedule");
+  if (mode < TSG_FORMB_AUTO || mode > TSG_FORMB_FLOW) return fail(TSG_ERR_INVALID, "unknown Form B schedule");
   if (m->fb_mode != mode) {
     m->fb_mode = mode;
     m->fb_chunks = 0;  // rebuilt (and the graph re-captured) by the next Form B call

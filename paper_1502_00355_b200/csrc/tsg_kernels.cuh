@@ -994,6 +994,67 @@ __device__ __forceinline__ R rot_fast(typename Arith<R>::R2 qa, typename Arith<R
   return fma(ax, by, -(ay * bx)) * rcp_cubic(la + lb + lab);
 }
 
+// Form B decision of one vertex from staged coordinates (formb_chunk_update, formb_flow):
+// sp[j * bs] / sv[j * bs] = pass-start / view value of row entry j, fan records (i1, i2, k).
+// Ordered neighbour sum through the view (smoothing.hpp:72-80), threshold at the pass-start
+// positions and hypothetical at the candidate with the rotation filter (rot_fast,
+// kGuardCycle), near-ties / degenerate triangles with the literal alpha_at (quality.hpp:15-23).
+template <typename R>
+__device__ __forceinline__ bool formb_decide_staged(typename Arith<R>::R2 pv, int deg, const typename Arith<R>::R2* sp,
+                                                    const typename Arith<R>::R2* sv, int bs, const uint32_t* fan,
+                                                    bool xonly, typename Arith<R>::R2& cand) {
+  using O = Arith<R>;
+  using R2 = typename O::R2;
+  constexpr bool kExact = sizeof(R) == 8;
+  R sx = R(0), sy = R(0);
+  for (int j = 0; j < deg; ++j) {
+    const R2 c = sv[j * bs];
+    sx = O::add(sx, c.x);
+    sy = O::add(sy, c.y);
+  }
+  const R inv = inv_deg<R>(deg);
+  cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
+  R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
+  for (int j = 0; j < deg; ++j) {
+    const uint32_t f = fan[j];
+    const int ia = static_cast<int>(fan_i1(f)) * bs, ib = static_cast<int>(fan_i2(f)) * bs;
+    R tp = rot_fast<R>(sp[ia], sp[ib], pv), tc = rot_fast<R>(sv[ia], sv[ib], cand);
+    if constexpr (!kExact) {
+      tp = isfinite(tp) ? tp : R(0);
+      tc = isfinite(tc) ? tc : R(0);
+    }
+    nan_acc = fma(tp, tc, nan_acc);
+    thr = min_ref(thr, tp);
+    hyp = min_ref(hyp, tc);
+  }
+  const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
+  if constexpr (!kExact) {
+    return hyp > thr;
+  } else {
+    if (!bad && hyp > thr + R(kGuardCycle)) return true;
+    if (!bad && hyp < thr - R(kGuardCycle)) return false;
+    R thr_e = R(INFINITY), hyp_e = R(INFINITY);
+    for (int j = 0; j < deg; ++j) {
+      const uint32_t f = fan[j];
+      const int ia = static_cast<int>(fan_i1(f)) * bs, ib = static_cast<int>(fan_i2(f)) * bs;
+      const int k = fan_k(f);
+      {
+        const R2 qa = sp[ia], qb = sp[ib];
+        const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+        thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
+                                           O::mul(daby, daby)));
+      }
+      {
+        const R2 qa = sv[ia], qb = sv[ib];
+        const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
+        hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
+                                           O::mul(daby, daby)));
+      }
+    }
+    return hyp_e > thr_e;
+  }
+}
+
 // Form B (ChunkView, quality.hpp:40-50; worker_chunk, parallel.hpp:19-24) with one CTA per
 // chunk: the CTA walks its chunk's dependency levels in order with a barrier between levels, so a
 // whole pass is ONE launch (the level-set schedule needs a launch per level: 195 per pass on the
@@ -1093,58 +1154,9 @@ __global__ void __launch_bounds__(256) formb_chunk_update(PassArgs<R, kSoA> a, c
   // The same decision from staged coordinates: sp / sv = pass-start / view value of row entry j
   // at [j * blockDim.x], fan records from the record.
   auto update_staged = [&](int64_t s, int deg, const R2* sp, const R2* sv, const uint32_t* fan) {
-    const int bs = static_cast<int>(blockDim.x);
     const R2 pv = P.load(s);
-    R sx = R(0), sy = R(0);
-    for (int j = 0; j < deg; ++j) {
-      const R2 c = sv[j * bs];
-      sx = O::add(sx, c.x);
-      sy = O::add(sy, c.y);
-    }
-    const R inv = inv_deg<R>(deg);
-    const R2 cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-    R thr = R(INFINITY), hyp = R(INFINITY), nan_acc = R(0);
-    for (int j = 0; j < deg; ++j) {
-      const uint32_t f = fan[j];
-      const int ia = static_cast<int>(fan_i1(f)) * bs, ib = static_cast<int>(fan_i2(f)) * bs;
-      R tp = rot_fast<R>(sp[ia], sp[ib], pv), tc = rot_fast<R>(sv[ia], sv[ib], cand);
-      if constexpr (!kExact) {
-        tp = isfinite(tp) ? tp : R(0);
-        tc = isfinite(tc) ? tc : R(0);
-      }
-      nan_acc = fma(tp, tc, nan_acc);
-      thr = min_ref(thr, tp);
-      hyp = min_ref(hyp, tc);
-    }
-    const bool bad = xonly || !(fabs(nan_acc) < R(1e30));
-    bool acc;
-    if constexpr (!kExact) {
-      acc = hyp > thr;
-    } else if (!bad && hyp > thr + R(kGuardCycle)) {
-      acc = true;
-    } else if (!bad && hyp < thr - R(kGuardCycle)) {
-      acc = false;
-    } else {
-      R thr_e = R(INFINITY), hyp_e = R(INFINITY);
-      for (int j = 0; j < deg; ++j) {
-        const uint32_t f = fan[j];
-        const int ia = static_cast<int>(fan_i1(f)) * bs, ib = static_cast<int>(fan_i2(f)) * bs;
-        const int k = fan_k(f);
-        {
-          const R2 qa = sp[ia], qb = sp[ib];
-          const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
-          thr_e = min_ref(thr_e, alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
-                                             O::mul(daby, daby)));
-        }
-        {
-          const R2 qa = sv[ia], qb = sv[ib];
-          const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
-          hyp_e = min_ref(hyp_e, alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby,
-                                             O::mul(dabx, dabx), O::mul(daby, daby)));
-        }
-      }
-      acc = hyp_e > thr_e;
-    }
+    R2 cand;
+    const bool acc = formb_decide_staged<R>(pv, deg, sp, sv, static_cast<int>(blockDim.x), fan, xonly, cand);
     N.store(s, acc ? cand : pv);
     if (acc) {
       ++accepted;

@@ -545,6 +545,29 @@ std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers,
     for (int64_t c = 0; c < nchunks; ++c)
       out.max_chunk_work = std::max<int64_t>(out.max_chunk_work, cnt[out.chunk_lvl[c + 1]] - cnt[out.chunk_lvl[c]]);
   }
+  {
+    // Dataflow order: by level, slot-ascending inside a level (counting sort).
+    std::vector<int64_t> cnt(nlev + 1, 0);
+    for (int64_t s = 0; s < nv; ++s) {
+      const int32_t L = level[hm.order[s]];
+      if (L >= 0) ++cnt[L + 1];
+    }
+    for (int32_t L = 0; L < nlev; ++L) cnt[L + 1] += cnt[L];
+    out.flow_rec.assign(static_cast<size_t>(cnt[nlev]) * kChunkRecWords, 0);
+    for (int64_t s = 0; s < nv; ++s) {
+      const int32_t L = level[hm.order[s]];
+      if (L < 0) continue;
+      uint32_t* r = out.flow_rec.data() + static_cast<size_t>(cnt[L]++) * kChunkRecWords;
+      const uint32_t o0 = hm.off[s], n = hm.off[s + 1] - o0;
+      r[0] = static_cast<uint32_t>(s);
+      r[1] = n;
+      if (n <= static_cast<uint32_t>(kChunkRecMaxDeg))
+        for (uint32_t j = 0; j < n; ++j) {
+          r[2 + j] = out.nbr_fresh[o0 + j];
+          r[2 + kChunkRecMaxDeg + j] = hm.fan[o0 + j];
+        }
+    }
+  }
   out.levels.resize(nlev);
   for (int32_t L = 0; L < nlev; ++L) {
     Phase& ph = out.levels[L];

@@ -91,6 +91,9 @@ struct FormBSchedule {
   // Per entry of cb_order a kChunkRecWords-word record: slot, valence, then (valence <=
   // kChunkRecMaxDeg) the row's neighbour slots (with kFreshBit) and its fan records.
   std::vector<uint32_t> cb_rec;
+  // Dataflow schedule (tsg_flow.cuh): the movable slots sorted by (level, slot), one
+  // kChunkRecWords record each (same format as cb_rec).
+  std::vector<uint32_t> flow_rec;
 };
 constexpr int kChunkRecWords = 32;
 constexpr int kChunkRecMaxDeg = 15;

@@ -41,6 +41,22 @@ def owners_by_order(order: np.ndarray, world: int) -> np.ndarray:
     return owner
 
 
+def owners_by_weight(order: np.ndarray, weight: np.ndarray, world: int) -> np.ndarray:
+    """owner[v] for contiguous ranges of the locality order holding equal total `weight`
+    (e.g. 1 + valence: a rank's pass time grows with its rows' lengths, so graded meshes with
+    hubs are cut by work, not by vertex count)."""
+    nv = len(order)
+    w = np.asarray(weight, dtype=np.float64)[order]
+    cum = np.cumsum(w)
+    total = cum[-1] if nv else 0.0
+    # vertex at position i goes to rank floor(world * (cum[i] - w[i] / 2) / total)
+    mid = cum - 0.5 * w
+    rank_of_pos = np.minimum((mid * world / max(total, 1e-300)).astype(np.int64), world - 1)
+    owner = np.empty(nv, dtype=np.int32)
+    owner[order] = rank_of_pos.astype(np.int32)
+    return owner
+
+
 def _gather_rows(off: np.ndarray, vals: np.ndarray, rows: np.ndarray):
     """CSR rows `rows` of (off, vals) -> (new_off int64, new_vals)."""
     lens = off[rows + 1] - off[rows]
@@ -136,6 +152,50 @@ def build_partition(rank: int, world: int, owner: np.ndarray, xy: np.ndarray, tr
                      np.concatenate(recv_ids).astype(np.int64), recv_counts)
 
 
+# ---- per-rank partition files: the mesh is prepared once, every rank loads only its part ----
+
+_PART_FIELDS = ("gids", "owned", "xy", "tri", "send_ids", "recv_ids")
+_TOPO_FIELDS = ("nbr_off", "nbr", "inc_off", "inc", "boundary")
+
+
+def write_partitions(out_dir: str, world: int, owner: np.ndarray, xy: np.ndarray, tri: np.ndarray, topo: dict,
+                     bbox_diag: float) -> list:
+    """Builds every rank's Partition from the global mesh (once, on one host process) and
+    writes `part_<r>.npz` per rank plus `meta.npz` (nv, nt, world, bbox diagonal) into
+    `out_dir`.  A rank then needs only its own file (`load_partition`): no rank holds the
+    global mesh or builds the global topology.  Returns the file paths."""
+    import os
+
+    os.makedirs(out_dir, exist_ok=True)
+    paths = []
+    for r in range(world):
+        p = build_partition(r, world, owner, xy, tri, topo)
+        arrays = {k: getattr(p, k) for k in _PART_FIELDS}
+        arrays.update({"topo_" + k: np.asarray(p.topo[k]) for k in _TOPO_FIELDS})
+        arrays["send_counts"] = np.asarray(p.send_counts, dtype=np.int64)
+        arrays["recv_counts"] = np.asarray(p.recv_counts, dtype=np.int64)
+        path = os.path.join(out_dir, f"part_{r}.npz")
+        np.savez(path, **arrays)
+        paths.append(path)
+    np.savez(os.path.join(out_dir, "meta.npz"), nv=len(xy), nt=len(tri), world=world, bbox_diag=bbox_diag)
+    return paths
+
+
+def load_partition(out_dir: str, rank: int):
+    """(Partition, meta dict) of `rank` from write_partitions' files."""
+    import os
+
+    meta = dict(np.load(os.path.join(out_dir, "meta.npz")))
+    world = int(meta["world"])
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside the partition set of {world}")
+    z = np.load(os.path.join(out_dir, f"part_{rank}.npz"))
+    topo = {k: z["topo_" + k] for k in _TOPO_FIELDS}
+    part = Partition(rank, world, z["gids"], z["owned"], z["xy"], z["tri"], topo, z["send_ids"],
+                     [int(c) for c in z["send_counts"]], z["recv_ids"], [int(c) for c in z["recv_counts"]])
+    return part, {k: (float(v) if k == "bbox_diag" else int(v)) for k, v in meta.items()}
+
+
 class DeviceEngine:
     """A partition on one GPU through the C ABI (paper_1502_00355_b200.capi)."""
 
@@ -204,7 +264,7 @@ class Exchanger:
 def _require_form_a(cfg):
     """Partitions are exact for Form A only: a Form B vertex reads in-chunk values written
     earlier in the same pass, so a partition boundary inside a chunk would change results."""
-    if cfg.form != 0:
+    if cfg is not None and cfg.form != 0:
         raise ValueError("partitioned smoothing supports Form A only (Form B reads live in-chunk "
                          "values; see DESIGN.md §6)")
 

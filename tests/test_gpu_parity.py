@@ -161,12 +161,13 @@ def test_single_fan_hub_beyond_shared_memory(capi, gpu_ctx, ts, port, n):
         dm.free()
 
 
-@pytest.mark.parametrize("mode", ["levels", "chunks"])
+@pytest.mark.parametrize("mode", ["levels", "chunks", "flow"])
 @pytest.mark.parametrize("case", [("grid", (30, 40, 0.3, 2), 1), ("delaunay", (12000, 9), 7),
                                   ("delaunay", (12000, 9), 300)])
 def test_form_b_schedules_vs_oracle(capi, gpu_ctx, ts, port, mode, case):
-    """Both Form B schedules (a launch per dependency level / one CTA per chunk walking its
-    levels) reproduce the reference bit for bit, both strategies."""
+    """The Form B schedules (a launch per dependency level / one CTA per chunk walking its
+    levels / the (vertex, pass) dataflow kernel) reproduce the reference bit for bit, both
+    strategies."""
     kind, args, chunks = case
     xy, tri = ts.grid_arrays(*args) if kind == "grid" else ts.delaunay_arrays(*args)
     want = port.smooth(xy, tri, form="b", chunks=chunks, max_iters=25, move_tol=0.0)
@@ -178,6 +179,38 @@ def test_form_b_schedules_vs_oracle(capi, gpu_ctx, ts, port, mode, case):
         assert np.array_equal(got["accepted"], want.accepted)
         assert np.array_equal(dm.get_coords().view(np.uint64), want.xy.view(np.uint64))
         dm.free()
+
+
+@pytest.mark.parametrize("case", [((30, 40, 0.3, 2), 1e-5, 1), ((30, 40, 0.3, 2), 1e-5, 7),
+                                  ((60, 60, 0.3, 3), 1e-5, 1), ((30, 40, 0.3, 2), 1e-6, 1)])
+@pytest.mark.parametrize("layout", ["aos", "soa"])
+def test_form_b_dataflow_rounds_and_replay_vs_oracle(capi, gpu_ctx, ts, port, case, layout):
+    """The dataflow schedule runs rounds of 64 passes while the displacement stop is live and
+    replays the round that stops (tsg_smooth, smooth_flow): stops at passes 71..245, in both
+    swap modes, equal the reference's (proj/src/smoothing.cpp:132-141) bit for bit."""
+    args, tol, chunks = case
+    xy, tri = ts.grid_arrays(*args)
+    want = port.smooth(xy, tri, form="b", chunks=chunks, max_iters=1000, move_tol=tol)
+    assert 64 < want.iterations < 1000 and want.stop == "displacement"
+    topo = ts.topology(len(xy), tri)
+    dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, layout=layout)
+    dm.formb_schedule("flow")
+    for swap in ("pingpong", "copy"):
+        dm.set_coords(xy)
+        got = dm.smooth(capi.make_cfg(form="b", chunks=chunks, swap=swap, max_iters=1000, move_tol=tol,
+                                      bbox_diag=ts.bbox_diagonal(xy)))
+        assert got["iterations"] == want.iterations and got["stop"] == want.stop
+        assert np.array_equal(got["accepted"], want.accepted)
+        assert np.array_equal(got["max_disp"].view(np.uint64), want.max_disp.view(np.uint64))
+        assert np.array_equal(dm.get_coords().view(np.uint64), want.xy.view(np.uint64))
+    # round boundaries without a live displacement stop: one launch for all passes
+    for n in (63, 64, 65, 129):
+        dm.set_coords(xy)
+        got = dm.smooth(capi.make_cfg(form="b", chunks=chunks, max_iters=n, move_tol=0.0))
+        w = port.smooth(xy, tri, form="b", chunks=chunks, max_iters=n, move_tol=0.0)
+        assert got["iterations"] == w.iterations and np.array_equal(got["accepted"], w.accepted)
+        assert np.array_equal(dm.get_coords().view(np.uint64), w.xy.view(np.uint64))
+    dm.free()
 
 
 @pytest.mark.parametrize("seed", [0, 1])
