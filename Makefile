@@ -29,7 +29,7 @@ tsg: $(TSG_SO)
 host: $(TS_SO)
 module: $(MOD_SO)
 
-build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_flow.cuh $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp $(CSRC)/tsg_internal.hpp include/tsg.h
+build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_flow.cuh $(CSRC)/tsg_peer.cuh $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp $(CSRC)/tsg_internal.hpp include/tsg.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas.log || (cat build/ptxas.log; false)
 

@@ -307,41 +307,83 @@ def run_reference_arm(args, cfg):
     print(json.dumps(out))
 
 
-def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
-    """N GPUs, one process each: the mesh is partitioned (Hilbert ranges + one-ring halos) and
-    every pass exchanges halos (NCCL all-to-all on device buffers) and all-reduces the stop
-    statistics, all enqueued on the engine stream (DeviceLoop: no host round trip per pass) —
-    strong scaling of one mesh (paper_1502_00355_b200/distributed.py)."""
+def prepare_partitions(args, cfg, rank, world, dist):
+    """Per-rank prep: rank 0 generates the mesh, builds the topology and the work-weighted
+    Hilbert ranges and writes one partition file per rank (distributed.write_partitions); every
+    rank then loads only its own (no rank holds the global mesh afterwards)."""
     import paper_1502_00355_b200 as ts
+    from paper_1502_00355_b200 import capi, distributed as D
+
+    part_dir = os.path.join("/tmp", f"tsg_parts_{args.config}_{args.nodes or 0}_{world}")
+    info = [None]
+    if rank == 0:
+        xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
+        topo = ts.topology(len(xy), tri)
+        deg = np.diff(topo["nbr_off"])
+        owner = D.owners_by_weight(capi.hilbert_order(xy), 1 + deg, world)
+        D.write_partitions(part_dir, world, owner, xy, tri, topo, ts.bbox_diagonal(xy))
+        b_pass = algorithmic_bytes_per_pass(len(xy), len(tri), int(topo["nbr_off"][-1]), cfg["precision"])
+        info = [{"config": workload_config(args, cfg, len(xy), len(tri), gargs, deg.max(), b_pass), "b_pass": b_pass}]
+        del xy, tri, topo
+    dist.broadcast_object_list(info, src=0)
+    part, meta = D.load_partition(part_dir, rank)
+    return part, meta, info[0]
+
+
+def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
+    """N GPUs, one process each, strong scaling of one mesh: the mesh is partitioned (work-
+    weighted Hilbert ranges + one-ring halos, per-rank partition files) and every pass exchanges
+    the halo.  Default transport "p2p": the peers' buffers are mapped over CUDA IPC and each
+    rank's smooth() is ONE conditional-WHILE graph whose passes store the halo straight into the
+    peers' memory and meet at a flag barrier carrying the stop statistics (tsg_peer.cuh).
+    "nccl": the DeviceLoop (NCCL all-to-all + all-gather per pass on the engine stream);
+    "gloo": host buffers (N ranks may share one GPU, tests)."""
     from paper_1502_00355_b200 import capi, distributed as D
 
     if cfg["form"] != "a":
         raise SystemExit("partitioned multi-GPU runs support Form A (see DESIGN.md)")
-    xy, tri, gargs = make_mesh(ts, cfg, args.nodes)
-    nv, nt = len(xy), len(tri)
     t0 = time.time()
-    topo = ts.topology(nv, tri)
-    owner = D.owners_by_order(capi.hilbert_order(xy), world)
-    part = D.build_partition(rank, world, owner, xy, tri, topo)
+    part, meta, info = prepare_partitions(args, cfg, rank, world, dist)
+    nv, nt = meta["nv"], meta["nt"]
     ctx = capi.Context(dev_index)
     eng = D.DeviceEngine(ctx, part, layout=cfg["layout"], precision=cfg["precision"])
-    device_buffers = args.transport == "nccl"
-    loop = D.DeviceLoop(eng, part, device=device_buffers, torch_device=torch.device("cuda", dev_index),
-                        stream_ptr=ctx.stream)
+    transport = args.transport
+    opened = []
+    if transport == "p2p":
+        try:
+            opened = D.connect_peers_ipc(ctx, eng.mesh, part, dist)
+        except Exception as exc:  # e.g. no IPC between these devices: the host-buffer loop instead
+            transport = f"gloo (p2p setup failed: {exc})"
+    loop = None
+    if not transport.startswith("p2p"):
+        device_buffers = not transport.startswith("gloo")
+        loop = D.DeviceLoop(eng, part, device=device_buffers, torch_device=torch.device("cuda", dev_index),
+                            stream_ptr=ctx.stream)
     prep_s = time.time() - t0
-    diag = ts.bbox_diagonal(xy)
     passes = cfg["passes"]
     scfg = capi.make_cfg(form="a", strategy=cfg["strategy"], swap=args.swap, max_iters=passes,
-                         move_tol=cfg["move_tol"], bbox_diag=diag)
+                         move_tol=cfg["move_tol"], bbox_diag=meta["bbox_diag"])
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", dev_index))
+    # control-plane tensors (timing, counts) live where the process group's backend wants them:
+    # p2p and gloo runs use a gloo group (the data plane of p2p is the peers' memory)
+    on_dev = dist.get_backend() == "nccl"
 
-    def step():  # device-resident pass loop: pass, halo all-to-all, stats all-reduce, stop rule
+    def run():
+        if loop is None:
+            r = eng.mesh.smooth(scfg)
+            return r["iterations"], r["launches"]
+        it, _, _, _ = loop.smooth(scfg)
+        return it, eng.mesh.dist_launches
+
+    def step():
         eng.mesh.restore_coords()
-        return loop.smooth(scfg)
+        return run()
 
+    if loop is None:
+        eng.mesh.peer_prepare(scfg)
+        dist.barrier()
     for _ in range(args.warmup):
-        it, _, _, _ = step()
-    launches_per_step = eng.mesh.dist_launches  # this rank's kernels in one step (tsg_dist_end)
+        it, launches_per_step = step()
     sampler = ClockSampler(dev_index)
     sampler.start()
     dist.barrier()
@@ -350,20 +392,22 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     e0.record(stream)
     updates = 0
     passes_run = 0
+    launches = 0
     for _ in range(args.steps):
-        it, _, _, _ = step()
+        it, k = step()
         updates += nv * it
         passes_run += it
+        launches += k
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
     clocks = sampler.stop()
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if device_buffers else "cpu")
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda" if on_dev else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_ms = float(t.item())
     value = updates / (elapsed_ms / 1000.0)  # whole-mesh node updates (every rank's share)
-    halo = torch.tensor([len(part.send_ids)], dtype=torch.int64, device="cuda" if device_buffers else "cpu")
+    halo = torch.tensor([len(part.send_ids)], dtype=torch.int64, device="cuda" if on_dev else "cpu")
     dist.all_reduce(halo, op=dist.ReduceOp.MAX)
 
     # End to end through the public API with host buffers: each rank uploads its partition's
@@ -374,18 +418,16 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
     e2e_updates = 0
     for _ in range(args.steps):
         eng.mesh.set_coords(part_xy)
-        it_e, _, _, _ = loop.smooth(scfg)
+        it_e, _ = run()
         _ = eng.owned_coords()
         e2e_updates += nv * it_e
     dist.barrier()
-    e2e_s = torch.tensor([time.perf_counter() - t_e], dtype=torch.float64,
-                         device="cuda" if device_buffers else "cpu")
+    e2e_s = torch.tensor([time.perf_counter() - t_e], dtype=torch.float64, device="cuda" if on_dev else "cpu")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     io = torch.tensor([16 * len(part_xy), 16 * int(part.owned.sum())], dtype=torch.int64,
-                      device="cuda" if device_buffers else "cpu")
+                      device="cuda" if on_dev else "cpu")
     dist.all_reduce(io, op=dist.ReduceOp.SUM)
-    sum_deg = int(topo["nbr_off"][-1])
-    b_pass = algorithmic_bytes_per_pass(nv, nt, sum_deg, cfg["precision"])
+    b_pass = info["b_pass"]
     pass_ms = elapsed_ms / max(1, passes_run)
     peak, peak_src = measured_peak()
     achieved = b_pass / world / (pass_ms / 1000.0) / 1e9  # per GPU, pass time incl. the exchange
@@ -395,24 +437,27 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg["precision"], "data": "synthetic",
-            "config": workload_config(args, cfg, nv, nt, gargs, np.diff(topo["nbr_off"]).max(), b_pass),
-            "impl_config": {"parallelism": f"partitioned x{world} (Hilbert ranges, one-ring halo, "
-                                           f"{args.transport} all-to-all per pass)",
-                            "max_halo_vertices_per_rank": int(halo.item()), "passes_run": passes_run},
+            "config": info["config"],
+            "impl_config": {"parallelism": f"partitioned x{world} (work-weighted Hilbert ranges, one-ring halo, "
+                                           f"{transport} halo exchange per pass)",
+                            "max_halo_vertices_per_rank": int(halo.item()), "passes_run": passes_run,
+                            "prep": "rank 0 writes per-rank partition files; each rank loads its own"},
             "ms_per_pass": pass_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                          "kernel": "per-GPU share of B_pass over the whole pass (node kernels + halo "
-                                   "exchange + stats all-reduce)",
+                                   "exchange + barrier / stop statistics)",
                          "bytes_per_launch": b_pass / world},
             "e2e": {"value": e2e_updates / float(e2e_s.item()), "unit": "node-updates/s",
                     "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item()),
                     "path": "per rank: set_coords (host) -> device pass loop -> owned coords (host)"},
             "cpu_baseline": None, "clocks": clocks,
-            "gpu_launches": launches_per_step * args.steps, "launches_per_step_rank0": launches_per_step,
+            "gpu_launches": launches, "launches_per_step_rank0": launches_per_step,
             "prep_s": prep_s,
         }
         print(json.dumps(out))
+    for ptr in opened:
+        ctx.ipc_close(ptr)
     eng.mesh.free()
     ctx.close()
 
@@ -439,9 +484,10 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=2.0, help="reference arm: target seconds of passes per step")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: 1 step, no e2e / baseline")
     ap.add_argument("--emit-mesh", default=None, help=argparse.SUPPRESS)  # reference arm's mesh child
-    ap.add_argument("--transport", choices=["nccl", "gloo"], default="nccl",
-                    help="N>1 halo exchange: NCCL device buffers (default) or gloo host buffers "
-                         "(lets N ranks share one GPU for testing)")
+    ap.add_argument("--transport", choices=["p2p", "nccl", "gloo"], default="p2p",
+                    help="N>1 halo exchange: p2p = direct stores into the peers' memory inside the graph "
+                         "(default), nccl = all-to-all on device buffers, gloo = host buffers "
+                         "(N ranks may share one GPU for testing)")
     args = ap.parse_args()
 
     cfg = dict(CONFIGS[args.config])

@@ -271,6 +271,36 @@ tsg_status tsg_quality_vertex_minima(tsg_context* ctx, int64_t nv, const int64_t
                                      const int32_t* inc, int64_t nt, const double* alpha,
                                      double* vmin_out);
 
+/* ---- partitioned Form A over peer memory (one process per GPU, NVLink / NVSwitch) ----
+ * Each rank uploads its partition (owned vertices + one-ring halo, halo pinned) as usual, then:
+ *   tsg_peer_local   its own coordinate buffers and sync block (allocated on first use), to be
+ *                    shared with the peers: raw pointers in one process, or CUDA IPC handles
+ *                    (tsg_ipc_handle / tsg_ipc_open) across processes;
+ *   tsg_mesh_slots   device slot of local vertex ids (the peers' push destinations);
+ *   tsg_peer_setup   the world's mapped pointers (entry `rank` = its own tsg_peer_local values)
+ *                    and this rank's push plan: for each owned vertex in peer q's halo, the
+ *                    local id and q's slot for it.
+ * From then on tsg_smooth on the mesh (Form A) runs the partitioned loop: per pass the node
+ * kernels, direct stores of the send vertices into the peers' buffers and a flag barrier with
+ * the global stop statistics, all inside one conditional-WHILE graph per rank (tsg_peer.cuh).
+ * Every rank must run the same sequence of tsg_smooth calls with the same configuration;
+ * results are bit-identical to one GPU.  tsg_peer_clear returns to single-mesh runs. */
+#define TSG_IPC_HANDLE_BYTES 64
+tsg_status tsg_peer_local(tsg_mesh* mesh, void** buf0, void** buf1, void** sync, int64_t* nv);
+tsg_status tsg_mesh_slots(tsg_mesh* mesh, const int64_t* ids, int64_t n, int64_t* slots_out);
+tsg_status tsg_peer_setup(tsg_mesh* mesh, int32_t rank, int32_t world, void* const* peer_buf0,
+                          void* const* peer_buf1, void* const* peer_sync, const int64_t* peer_nv,
+                          int64_t n_push, const int32_t* push_peer, const int64_t* push_src_ids,
+                          const int64_t* push_dst_slots);
+/* Allocations, capture and instantiation of the peer graph for `cfg` (they may synchronise the
+ * device): call on every rank before the first tsg_smooth with that configuration whenever
+ * several ranks share a device or a process. */
+tsg_status tsg_peer_prepare(tsg_mesh* mesh, const tsg_smooth_cfg* cfg);
+tsg_status tsg_peer_clear(tsg_mesh* mesh);
+tsg_status tsg_ipc_handle(const void* dev_ptr, void* handle_out);
+tsg_status tsg_ipc_open(tsg_context* ctx, const void* handle, void** dev_ptr_out);
+tsg_status tsg_ipc_close(tsg_context* ctx, void* dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

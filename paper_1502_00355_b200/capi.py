@@ -35,7 +35,10 @@ EXPORTS = (
     "tsg_halo_pack", "tsg_halo_unpack", "tsg_dist_begin", "tsg_dist_pass", "tsg_dist_halo_pack",
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
     "tsg_debug_trace", "tsg_mesh_side_schedule", "tsg_quality_tri_alpha", "tsg_quality_vertex_minima",
+    "tsg_peer_local", "tsg_mesh_slots", "tsg_peer_setup", "tsg_peer_prepare", "tsg_peer_clear", "tsg_ipc_handle", "tsg_ipc_open",
+    "tsg_ipc_close",
 )
+IPC_HANDLE_BYTES = 64
 
 
 class MeshDesc(C.Structure):
@@ -113,6 +116,14 @@ def lib() -> C.CDLL:
             "tsg_dist_end": (i32, [P, C.POINTER(SmoothCfg), P, P, i32, P, P, P]),
             "tsg_quality_tri_alpha": (i32, [P, i64, P, i64, P, P, C.POINTER(QualityReport)]),
             "tsg_quality_vertex_minima": (i32, [P, i64, P, P, i64, P, P]),
+            "tsg_peer_local": (i32, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(i64)]),
+            "tsg_mesh_slots": (i32, [P, P, i64, P]),
+            "tsg_peer_setup": (i32, [P, i32, i32, P, P, P, P, i64, P, P, P]),
+            "tsg_peer_prepare": (i32, [P, C.POINTER(SmoothCfg)]),
+            "tsg_peer_clear": (i32, [P]),
+            "tsg_ipc_handle": (i32, [P, P]),
+            "tsg_ipc_open": (i32, [P, P, C.POINTER(P)]),
+            "tsg_ipc_close": (i32, [P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -136,6 +147,13 @@ def hilbert_order(xy: np.ndarray) -> np.ndarray:
     out = np.empty(len(xy), dtype=np.int64)
     check(lib().tsg_hilbert_order(len(xy), _ptr(xy), _ptr(out)), "tsg_hilbert_order")
     return out
+
+
+def ipc_handle(dev_ptr: int) -> bytes:
+    """CUDA IPC handle (64 bytes) of a device allocation's base pointer (tsg_ipc_handle)."""
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    check(lib().tsg_ipc_handle(C.c_void_p(dev_ptr), buf), "tsg_ipc_handle")
+    return buf.raw
 
 
 class Context:
@@ -178,6 +196,16 @@ class Context:
         check(lib().tsg_quality_vertex_minima(self.h, len(out), _ptr(inc_off), _ptr(inc), len(alpha), _ptr(alpha),
                                               _ptr(out)), "tsg_quality_vertex_minima")
         return out
+
+    def ipc_open(self, handle: bytes) -> int:
+        """Maps a peer process's allocation (tsg_ipc_open); returns the device pointer."""
+        out = C.c_void_p()
+        buf = C.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+        check(lib().tsg_ipc_open(self.h, buf, C.byref(out)), "tsg_ipc_open")
+        return out.value
+
+    def ipc_close(self, dev_ptr: int):
+        check(lib().tsg_ipc_close(self.h, C.c_void_p(dev_ptr)), "tsg_ipc_close")
 
     def close(self):
         if self.h:
@@ -337,6 +365,34 @@ class DeviceMesh:
         grid) or "persist" (a persistent kernel beside it).  Results are identical."""
         check(lib().tsg_mesh_side_schedule(self.h, {"auto": 0, "kernels": 1, "persist": 2}[mode]),
               "tsg_mesh_side_schedule")
+
+    # ---- peer-memory partitioned driver (include/tsg.h, tsg_peer_*) ----
+    def peer_local(self):
+        """(buf0, buf1, sync, nv): this mesh's coordinate buffers and sync block (device ptrs)."""
+        b0, b1, sy, nv = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(lib().tsg_peer_local(self.h, C.byref(b0), C.byref(b1), C.byref(sy), C.byref(nv)), "tsg_peer_local")
+        return b0.value, b1.value, sy.value, nv.value
+
+    def slots(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.empty(len(ids), dtype=np.int64)
+        check(lib().tsg_mesh_slots(self.h, _ptr(ids), len(ids), _ptr(out)), "tsg_mesh_slots")
+        return out
+
+    def peer_setup(self, rank, world, buf0s, buf1s, syncs, nvs, push_peer, push_src, push_dst):
+        arr = lambda xs: (C.c_void_p * len(xs))(*xs)
+        nvs = np.ascontiguousarray(nvs, dtype=np.int64)
+        self._push = (np.ascontiguousarray(push_peer, dtype=np.int32), np.ascontiguousarray(push_src, dtype=np.int64),
+                      np.ascontiguousarray(push_dst, dtype=np.int64))
+        check(lib().tsg_peer_setup(self.h, rank, world, arr(buf0s), arr(buf1s), arr(syncs), _ptr(nvs),
+                                   len(self._push[0]), _ptr(self._push[0]), _ptr(self._push[1]), _ptr(self._push[2])),
+              "tsg_peer_setup")
+
+    def peer_prepare(self, cfg: SmoothCfg):
+        check(lib().tsg_peer_prepare(self.h, C.byref(cfg)), "tsg_peer_prepare")
+
+    def peer_clear(self):
+        check(lib().tsg_peer_clear(self.h), "tsg_peer_clear")
 
     # Device-resident partitioned loop (include/tsg.h, tsg_dist_*): enqueue-only calls taking
     # device pointers (e.g. torch CUDA tensors' data_ptr()).

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -19,6 +20,7 @@
 
 #include "tsg.h"
 #include "tsg_flow.cuh"
+#include "tsg_peer.cuh"
 #include "tsg_kernels.cuh"
 #include "tsg_internal.hpp"
 #include "tsg_prep.hpp"
@@ -355,9 +357,28 @@ __global__ void dist_halo_unpack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b
   commit_maxabs(m, maxabs);
 }
 
+// The dynamic shared-memory limit of a kernel is a per-function, per-device setting shared by
+// every mesh: only ever raise it (a later mesh needing less must not lower the limit an earlier
+// mesh's launches rely on).
+template <class K>
+cudaError_t raise_smem_limit(K* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> limit;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = limit[{dev, reinterpret_cast<const void*>(fn)}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
 struct GraphCache {
   bool valid = false;
   int32_t form = -1, strategy = -1, chunks = -1, swap = -1, max_iters = -1;
+  bool peer = false;
   double tol_abs = 0.0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -440,6 +461,16 @@ struct tsg_mesh {
   int32_t* d_recv_slots = nullptr;
   int64_t n_send = 0, n_recv = 0;
   double* d_halo_stage = nullptr;  // 2 * max(n_send, n_recv) doubles (host-pointer transfers)
+  // Peer-memory partitioned driver (tsg_peer.cuh): this rank, the peers' mapped buffers and
+  // sync blocks, and the push plan (own slot -> peer, peer slot).
+  int32_t peer_rank = 0, peer_world = 0;
+  tsg::PeerSync* d_peer_sync = nullptr;
+  tsg::PeerEntry* d_peer_tab = nullptr;
+  int32_t* d_push_peer = nullptr;
+  uint32_t *d_push_src = nullptr, *d_push_dst = nullptr;
+  int64_t n_push = 0;
+  uint32_t peer_tick = 0;  // last tick of the previous peer run (identical on every rank)
+  uint32_t h_peer_tick0 = 0;  // host copy of this run's start tick (source of an async copy)
 };
 
 #define TSG_LOCK_MESH(m) tsg_abi::CtxLock tsg_ctx_lock_((m) ? (m)->ctx : nullptr)
@@ -604,7 +635,7 @@ struct Engine {
       a.count = nh;
       const size_t smem = static_cast<size_t>(hub_cap) * sizeof(R2) * (kFormB ? 2 : 1);
       tsg::hub_update<R, kSoA, kFormB, kTwoPhase><<<static_cast<unsigned>(nh), tsg::kHubBlock, smem, t>>>(a, hub_cap);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     if (nmed > 0) {
@@ -614,7 +645,7 @@ struct Engine {
       a.count = nmed;
       tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxMedDeg, kMedBlock>
           <<<static_cast<unsigned>((nmed + kMedBlock - 1) / kMedBlock), kMedBlock, 0, t>>>(a);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     if (ns > 0) {
@@ -623,7 +654,7 @@ struct Engine {
       a.count = ns;
       tsg::node_update<R, kSoA, kFormB, kTwoPhase, kMaxSmallDeg, tsg::kNodeBlock>
           <<<static_cast<unsigned>((ns + tsg::kNodeBlock - 1) / tsg::kNodeBlock), tsg::kNodeBlock, 0, s>>>(a);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     if (fork) {
@@ -672,7 +703,7 @@ struct Engine {
         tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true><<<ntiles, kTileThreads, smem, s>>>(a, ta);
       else
         tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     // The persistent side kernel is enqueued AFTER the tile grid: in the captured graph the two
@@ -690,7 +721,7 @@ struct Engine {
       if (a.count > 0) {
         tsg::side_rows<R, kSoA, kSideWarps, kWarpTierCap, kSideRegs>
             <<<static_cast<unsigned>(m->num_sms), kSideWarps * 32, 0, tw>>>(a, m->d_side_ctr);
-        TSG_CUDA(cudaGetLastError());
+        TSG_LAUNCHED();
         ++*kernels;
       }
     }
@@ -702,7 +733,7 @@ struct Engine {
       a.count = n_cta;
       const int32_t cap = hub_fast_cap(m);
       tsg::hub_fast_update<R, kSoA><<<static_cast<unsigned>(n_cta), tsg::kHubFastBlock, cap * sizeof(R2), th>>>(a, cap);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     if (!persist && nwarp > 0) {
@@ -711,7 +742,7 @@ struct Engine {
       a.count = nwarp;
       tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>
           <<<static_cast<unsigned>((nwarp + kWarpTierWarps - 1) / kWarpTierWarps), kWarpTierWarps * 32, 0, tw>>>(a);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     for (int i = 0; i < nf; ++i) {  // join
@@ -738,7 +769,7 @@ struct Engine {
       tsg::tri_alpha<R, kSoA><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
           coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1), c.swap, m->d_state, m->d_tri,
           m->hm.nt, static_cast<R*>(m->d_alpha));
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     }
     Args base = base_args(m, c);
@@ -758,7 +789,7 @@ struct Engine {
       // Form B, both strategies (equal thresholds): one CTA per chunk.
       tsg::formb_chunk_update<R, kSoA><<<static_cast<unsigned>(m->fb_nchunks), 256, kChunkRecSmem, s>>>(
           base, m->d_cb_order, m->d_cb_lvl, m->d_cb_chunk, m->d_cb_rec);
-      TSG_CUDA(cudaGetLastError());
+      TSG_LAUNCHED();
       ++*kernels;
     } else {
       for (const tsg::Phase& L : m->fb_levels) {
@@ -773,7 +804,7 @@ struct Engine {
     if (!with_finalize) return TSG_OK;  // partitioned driver: the stop rule runs on global totals
     tsg::finalize_pass<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, m->d_acc, m->d_md, tol_abs,
                                         c.max_iters, h, use_handle);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     ++*kernels;
     return TSG_OK;
   }
@@ -807,20 +838,16 @@ struct Engine {
 
   // Opt-in shared memory for the hub kernels (done outside any stream capture).
   static tsg_status prepare(tsg_mesh* m) {
-    TSG_CUDA(cudaFuncSetAttribute(tsg::formb_chunk_update<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kChunkRecSmem));
-    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_fast_update<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(hub_fast_cap(m) * sizeof(R2))));
+    TSG_CUDA(raise_smem_limit(tsg::formb_chunk_update<R, kSoA>, kChunkRecSmem));
+    TSG_CUDA(raise_smem_limit(tsg::hub_fast_update<R, kSoA>, static_cast<int>(hub_fast_cap(m) * sizeof(R2))));
     {
       const tsg::TileArgs ta = tile_args(m);
       const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap));
       if (std::getenv("TSG_DIAG"))
         std::fprintf(stderr, "[tsg] tile smem %d B (ext_cap %d, rec_cap %d words), large rows %zu (hub CTAs %lld)\n",
                      smem, ta.ext_cap, ta.rec_cap, m->hm.large.size(), static_cast<long long>(m->n_hub_fast));
-      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      TSG_CUDA(raise_smem_limit(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>, smem));
+      TSG_CUDA(raise_smem_limit(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>, smem));
     }
     // Kernels that run concurrently on one SM must agree on its L1 / shared-memory split: the
     // tile and side-tier kernels all ask for the maximum shared-memory carveout, so that a
@@ -839,10 +866,10 @@ struct Engine {
     }
     const int32_t hub_cap = std::max(1, std::min(m->hub_max_deg, kHubCap));
     const int smem1 = static_cast<int>(hub_cap * sizeof(R2)), smem2 = 2 * smem1;
-    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
-    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
-    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
-    TSG_CUDA(cudaFuncSetAttribute(tsg::hub_update<R, kSoA, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    TSG_CUDA(raise_smem_limit(tsg::hub_update<R, kSoA, false, false>, smem1));
+    TSG_CUDA(raise_smem_limit(tsg::hub_update<R, kSoA, false, true>, smem1));
+    TSG_CUDA(raise_smem_limit(tsg::hub_update<R, kSoA, true, false>, smem2));
+    TSG_CUDA(raise_smem_limit(tsg::hub_update<R, kSoA, true, true>, smem2));
     return TSG_OK;
   }
 
@@ -872,7 +899,7 @@ struct Engine {
     coords_from_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(m->d_xy_stage, m->d_order, nv,
                                                                 coords_of<R, kSoA>(m, 0),
                                                                 coords_of<R, kSoA>(m, 1), m->d_maxabs);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpyAsync(m->init, m->buf[0], 2 * nv * sizeof(R), cudaMemcpyDeviceToDevice, s));
     m->cur = 0;
     return TSG_OK;
@@ -883,7 +910,7 @@ struct Engine {
     const int64_t nv = m->hm.nv;
     coords_to_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, m->cur), m->d_order,
                                                               nv, m->d_xy_stage);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpyAsync(xy_host, m->d_xy_stage, 2 * nv * sizeof(double), cudaMemcpyDeviceToHost, s));
     TSG_CUDA(cudaStreamSynchronize(s));
     return TSG_OK;
@@ -897,7 +924,7 @@ struct Engine {
     zero_u64<<<1, 1, 0, s>>>(m->d_maxabs);  // (a kernel: see smooth_enqueue_graph)
     coords_from_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(stage, m->d_order, nv, coords_of<R, kSoA>(m, 0),
                                                                 coords_of<R, kSoA>(m, 1), m->d_maxabs);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     m->cur = 0;
     return TSG_OK;
   }
@@ -906,7 +933,7 @@ struct Engine {
     const int64_t nv = m->hm.nv;
     coords_to_orig_parity<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1),
                                                                      swap, m->d_state, m->d_order, nv, stage);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     return TSG_OK;
   }
 
@@ -926,11 +953,10 @@ struct Engine {
     const int64_t n = m->flow_n;
     if (n == 0 || np <= 0) return TSG_OK;
     tsg::flow_reset<<<grid_for(n, 256), 256, 0, s>>>(m->d_flow_rec, n, m->d_flow_done);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     int per_sm = 0, sms = 0;
     constexpr size_t smem = tsg::flow_smem_bytes<R>();
-    TSG_CUDA(cudaFuncSetAttribute(tsg::formb_flow<R, kSoA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    TSG_CUDA(raise_smem_limit(tsg::formb_flow<R, kSoA>, static_cast<int>(smem)));
     TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsg::formb_flow<R, kSoA>, tsg::kFlowBlock, smem));
     TSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->ctx->device));
     const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * sms;
@@ -958,12 +984,22 @@ struct Engine {
     return TSG_OK;
   }
 
+  static tsg_status peer_push(tsg_mesh* m, cudaStream_t s, int64_t* kernels) {
+    if (m->n_push == 0) return TSG_OK;
+    tsg::peer_push<R, kSoA><<<grid_for(m->n_push, 256), 256, 0, s>>>(
+        m->d_state, coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1), m->d_push_peer, m->d_push_src,
+        m->d_push_dst, m->n_push, m->d_peer_tab);
+    TSG_LAUNCHED();
+    ++*kernels;
+    return TSG_OK;
+  }
+
   static tsg_status refresh_alpha(tsg_mesh* m) {
     cudaStream_t s = m->ctx->stream;
     tsg::tri_alpha<R, kSoA><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
         coords_of<R, kSoA>(m, m->cur), coords_of<R, kSoA>(m, m->cur), 0, nullptr, m->d_tri, m->hm.nt,
         static_cast<R*>(m->d_alpha));
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     return TSG_OK;
   }
 };
@@ -1089,7 +1125,7 @@ tsg_status tsg_selftest_alpha(tsg_context* ctx, int64_t n, uint64_t seed, int32_
   TSG_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
   TSG_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
   selftest_alpha<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, seed, newton_steps, d, d + 1);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   unsigned long long h[2];
   TSG_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   TSG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1108,7 +1144,7 @@ tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, 
   TSG_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
   TSG_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
   selftest_alpha_cycle<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, seed, d, d + 1);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   unsigned long long h[2];
   TSG_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   TSG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1227,7 +1263,8 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
   void* ptrs[] = {m->buf[0], m->buf[1], m->init, m->d_off, m->d_nbr, m->d_fan, m->d_fan16, m->d_tmeta, m->d_tile_rec, m->d_ext_off, m->d_tile_ext, m->d_trec, m->d_vinc_off, m->d_vinc,
                   m->d_tri, m->d_hubs, m->d_medium, m->d_large, m->d_maxabs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
-                  m->d_ext, m->d_side_ctr, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage};
+                  m->d_ext, m->d_side_ctr, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage,
+                  m->d_peer_sync, m->d_peer_tab, m->d_push_peer, m->d_push_src, m->d_push_dst};
   for (void* p : ptrs) cudaFree(p);
   for (int b = 0; b < 2; ++b) {
     cudaFree(m->d_batch_in[b]);
@@ -1292,7 +1329,7 @@ tsg_status tsg_tri_alpha(tsg_mesh* m, double* alpha_out) {
     else
       to_double_scatter<float><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
           static_cast<const float*>(m->d_alpha), m->d_tri_order, m->hm.nt, dst);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpyAsync(alpha_out, dst, m->hm.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
     TSG_CUDA(cudaStreamSynchronize(s));
     if (own) cudaFree(dst);
@@ -1315,9 +1352,9 @@ tsg_status tsg_vertex_minima(tsg_mesh* m, double* vmin_out) {
   else
     tsg::vertex_min<float><<<grid_for(nv, 256), 256, 0, s>>>(m->d_vinc_off, m->d_vinc,
                                                              static_cast<const float*>(m->d_alpha), nv, m->d_vmin);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   to_double_scatter<double><<<grid_for(nv, 256), 256, 0, s>>>(m->d_vmin, m->d_order, nv, m->d_xy_stage);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   TSG_CUDA(cudaMemcpyAsync(vmin_out, m->d_xy_stage, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
   return TSG_OK;
@@ -1337,7 +1374,7 @@ tsg_status tsg_alpha_extrema(tsg_mesh* m, double* min_out, double* max_out, int6
   else
     tsg::alpha_extrema<float><<<grid_for(m->hm.nt, 256), 256, 0, s>>>(
         static_cast<const float*>(m->d_alpha), m->hm.nt, m->d_ext, m->d_ext + 1, m->d_ext + 2);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   unsigned long long h[3];
   TSG_CUDA(cudaMemcpyAsync(h, m->d_ext, sizeof(h), cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
@@ -1370,9 +1407,9 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
   // the host<->device copies tsg_smooth_host_batch overlaps with this stream)
   reset_pass_state<<<grid_for(int64_t{tsg::kStatSlots} * c->max_iters, 256), 256, 0, s>>>(
       m->d_state, m->d_sacc, m->d_smd, int64_t{tsg::kStatSlots} * c->max_iters, m->d_side_ctr);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   GraphCache& g = m->gc;
-  if (!(g.valid && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
+  if (!(g.valid && !g.peer && g.form == c->form && g.strategy == c->strategy && g.chunks == c->chunks &&
         g.swap == c->swap && g.max_iters == c->max_iters && g.tol_abs == tol_abs)) {
     g.reset();
     TSG_CUDA(cudaGraphCreate(&g.graph, 0));
@@ -1397,6 +1434,7 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
     if (e != cudaSuccess) return fail(TSG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
     TSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
     g.valid = true;
+    g.peer = false;
     g.form = c->form;
     g.strategy = c->strategy;
     g.chunks = c->chunks;
@@ -1407,6 +1445,84 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
   }
   *kernels_per_pass = g.kernels_per_pass;
   TSG_CUDA(cudaGraphLaunch(g.exec, s));
+  return TSG_OK;
+}
+
+// Partitioned Form A over peer memory: the conditional-WHILE graph whose body is the pass's node
+// kernels, peer_push and peer_sync (tsg_peer.cuh).  Built (stats capacity, capture,
+// instantiation) before any rank's start barrier spins: those calls may synchronise the device,
+// which must not happen while a peer on the same device waits for this rank
+// (tsg_peer_prepare does it ahead of the first run).
+tsg_status peer_graph(tsg_mesh* m, const tsg_smooth_cfg* c) {
+  cudaStream_t s = m->ctx->stream;
+  tsg_status st;
+  if ((st = ensure_stats_capacity(m, c->max_iters))) return st;
+  const double tol_abs = c->move_tol * c->bbox_diag;
+  tsg_smooth_cfg cc = *c;
+  cc.swap = TSG_SWAP_PINGPONG;  // see tsg_peer.cuh: copy mode maps to ping-pong (same results)
+  GraphCache& g = m->gc;
+  if (g.valid && g.peer && g.form == cc.form && g.strategy == cc.strategy && g.max_iters == cc.max_iters &&
+      g.tol_abs == tol_abs)
+    return TSG_OK;
+  g.reset();
+  TSG_CUDA(cudaGraphCreate(&g.graph, 0));
+  cudaGraphConditionalHandle h;
+  TSG_CUDA(cudaGraphConditionalHandleCreate(&h, g.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  TSG_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  TSG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int64_t k = 0;
+  st = dispatch(m, [&](auto E) {
+    tsg_status r = decltype(E)::enqueue_pass(m, cc, s, tol_abs, h, 1, nullptr, nullptr, nullptr, &k, false);
+    if (r) return r;
+    return decltype(E)::peer_push(m, s, &k);
+  });
+  if (!st) {
+    tsg::peer_sync<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, m->d_peer_sync, m->d_peer_tab, m->peer_rank,
+                                    m->peer_world, m->d_acc, m->d_md, tol_abs, c->max_iters, h, 0);
+    ++k;
+  }
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &captured);
+  if (st) return st;
+  if (e != cudaSuccess) return fail(TSG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+  TSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+  g.valid = true;
+  g.peer = true;
+  g.form = cc.form;
+  g.strategy = cc.strategy;
+  g.chunks = cc.chunks;
+  g.swap = cc.swap;
+  g.max_iters = cc.max_iters;
+  g.tol_abs = tol_abs;
+  g.kernels_per_pass = k;
+  return TSG_OK;
+}
+
+// Start barrier, then one launch of the peer graph (no synchronising call in between).
+tsg_status smooth_enqueue_peer(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* kernels_per_pass) {
+  cudaStream_t s = m->ctx->stream;
+  tsg_status st;
+  if ((st = peer_graph(m, c))) return st;
+  const double tol_abs = c->move_tol * c->bbox_diag;
+  reset_pass_state<<<grid_for(int64_t{tsg::kStatSlots} * c->max_iters, 256), 256, 0, s>>>(
+      m->d_state, m->d_sacc, m->d_smd, int64_t{tsg::kStatSlots} * c->max_iters, m->d_side_ctr);
+  TSG_LAUNCHED();
+  m->h_peer_tick0 = m->peer_tick + 1;
+  TSG_CUDA(cudaMemcpyAsync(&m->d_peer_sync->tick0, &m->h_peer_tick0, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  TSG_CUDA(cudaMemsetAsync(&m->d_peer_sync->error, 0, sizeof(int32_t), s));
+  tsg::peer_sync<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, m->d_peer_sync, m->d_peer_tab, m->peer_rank,
+                                  m->peer_world, m->d_acc, m->d_md, tol_abs, c->max_iters,
+                                  cudaGraphConditionalHandle{}, 1);
+  TSG_LAUNCHED();
+  *kernels_per_pass = m->gc.kernels_per_pass;
+  TSG_CUDA(cudaGraphLaunch(m->gc.exec, s));
   return TSG_OK;
 }
 
@@ -1553,7 +1669,14 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   int64_t kernels_per_pass = 0;
   double node_ms = -1.0;
   int64_t launches = 0;
-  if (c->driver == TSG_DRIVER_GRAPH) {
+  const bool peer = m->peer_world > 1;
+  if (peer) {
+    if (c->form != TSG_FORM_A) return fail(TSG_ERR_INVALID, "the peer-memory partitioned driver runs Form A");
+    TSG_CUDA(cudaEventRecord(ctx->ev0, s));
+    if ((st = smooth_enqueue_peer(m, c, &kernels_per_pass))) return st;
+    TSG_CUDA(cudaEventRecord(ctx->ev1, s));
+    launches = 2;  // the start barrier and the graph
+  } else if (c->driver == TSG_DRIVER_GRAPH) {
     TSG_CUDA(cudaEventRecord(ctx->ev0, s));
     if ((st = smooth_enqueue_graph(m, c, &kernels_per_pass))) return st;
     TSG_CUDA(cudaEventRecord(ctx->ev1, s));
@@ -1618,8 +1741,17 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
       for (int b = 0; b < 16; ++b) std::fprintf(stderr, "[tsg diag] |hyp-thr| 2^%d: %llu\n", b - 60, hist[b]);
     }
   }
-  if (c->swap == TSG_SWAP_PINGPONG) m->cur = it & 1;
-  else m->cur = 0;
+  if (peer) {
+    int32_t err = 0;
+    TSG_CUDA(cudaMemcpy(&err, &m->d_peer_sync->error, sizeof err, cudaMemcpyDeviceToHost));
+    m->peer_tick += 1 + static_cast<uint32_t>(it);
+    if (err) return fail(TSG_ERR_CUDA, "peer barrier timed out (a rank did not reach the same pass)");
+    m->cur = it & 1;
+  } else if (c->swap == TSG_SWAP_PINGPONG) {
+    m->cur = it & 1;
+  } else {
+    m->cur = 0;
+  }
   const int32_t n = std::min(capacity, it);
   if (accepted_per_pass && n > 0)
     TSG_CUDA(cudaMemcpy(accepted_per_pass, m->d_acc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
@@ -1634,7 +1766,8 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
     stats->node_updates = m->hm.nv * static_cast<int64_t>(it);
     stats->device_ms = total_ms;
     stats->node_kernel_ms = node_ms;
-    stats->launches = c->driver == TSG_DRIVER_GRAPH ? kernels_per_pass * it : launches;
+    stats->launches = peer ? 2 + kernels_per_pass * it
+                      : c->driver == TSG_DRIVER_GRAPH ? kernels_per_pass * it : launches;
   }
   return TSG_OK;
 }
@@ -1691,7 +1824,7 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
     st = dispatch(m, [&](auto E) { return decltype(E)::batch_store(m, c->swap, m->d_batch_out[b]); });
     if (st) return st;
     save_state<<<1, 1, 0, s>>>(m->d_state, m->d_batch_state + k);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     TSG_CUDA(cudaEventRecord(ctx->ev_out_ready[b], s));
     TSG_CUDA(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_ready[b], 0));
     TSG_CUDA(cudaMemcpyAsync(xy_out[k], m->d_batch_out[b], bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
@@ -1754,7 +1887,7 @@ tsg_status tsg_pass_lockstep(tsg_mesh* m, int32_t form, int32_t chunks, int8_t* 
   if (decision_out) {
     scatter_i8<<<grid_for(m->hm.nv, 256), 256, 0, s>>>(m->d_decision, m->d_order, m->hm.nv,
                                                        m->d_decision_orig);
-    TSG_CUDA(cudaGetLastError());
+    TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpyAsync(decision_out, m->d_decision_orig, m->hm.nv, cudaMemcpyDeviceToHost, s));
   }
   int32_t acc = 0;
@@ -1891,7 +2024,7 @@ tsg_status tsg_dist_pass(tsg_mesh* m, const tsg_smooth_cfg* c, double* stats_dev
   });
   if (st) return st;
   dist_fold<<<1, 32, 0, s>>>(m->d_state, m->d_sacc, m->d_smd, stats_dev);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   m->dist_launches += k + 1;
   return TSG_OK;
 }
@@ -1914,7 +2047,7 @@ tsg_status tsg_dist_halo_pack(tsg_mesh* m, const tsg_smooth_cfg* c, double* out_
     else
       dist_halo_pack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), c->swap, m->d_state, m->d_send_slots, m->n_send, out_dev);
   }
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   ++m->dist_launches;
   return TSG_OK;
 }
@@ -1937,7 +2070,7 @@ tsg_status tsg_dist_halo_unpack(tsg_mesh* m, const double* in_dev) {
     else
       dist_halo_unpack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), m->d_state, m->d_recv_slots, m->n_recv, in_dev, m->d_maxabs);
   }
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   ++m->dist_launches;
   return TSG_OK;
 }
@@ -1949,7 +2082,7 @@ tsg_status tsg_dist_finalize(tsg_mesh* m, const tsg_smooth_cfg* c, const double*
   const double tol_abs = c->move_tol * c->bbox_diag;  // smoothing.cpp:136, same rounding
   dist_finalize<<<1, 1, 0, m->ctx->stream>>>(m->d_state, gathered_dev, n_parts, m->d_acc, m->d_md, tol_abs,
                                             c->max_iters);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   ++m->dist_launches;
   return TSG_OK;
 }
@@ -2008,7 +2141,7 @@ tsg_status tsg_halo_pack(tsg_mesh* m, double* out, int32_t out_is_host) {
     else
       halo_pack<float, false><<<grid_for(m->n_send, 256), 256, 0, s>>>(coords_of<float, false>(m, m->cur), m->d_send_slots, m->n_send, dst);
   }
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   if (out_is_host)
     TSG_CUDA(cudaMemcpyAsync(out, dst, 2 * m->n_send * sizeof(double), cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
@@ -2038,8 +2171,135 @@ tsg_status tsg_halo_unpack(tsg_mesh* m, const double* in, int32_t in_is_host) {
     else
       halo_unpack<float, false><<<g, 256, 0, s>>>(coords_of<float, false>(m, 0), coords_of<float, false>(m, 1), m->d_recv_slots, m->n_recv, src, m->d_maxabs);
   }
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   TSG_CUDA(cudaStreamSynchronize(s));
+  return TSG_OK;
+}
+
+// ---- peer-memory partitioned driver (tsg_peer.cuh) ----
+
+tsg_status tsg_peer_local(tsg_mesh* m, void** buf0, void** buf1, void** sync, int64_t* nv) {
+  TSG_LOCK_MESH(m);
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  if (!m->d_peer_sync) {
+    TSG_CUDA(cudaMalloc(&m->d_peer_sync, sizeof(tsg::PeerSync)));
+    TSG_CUDA(cudaMemset(m->d_peer_sync, 0, sizeof(tsg::PeerSync)));
+    m->bytes += sizeof(tsg::PeerSync);
+  }
+  if (buf0) *buf0 = m->buf[0];
+  if (buf1) *buf1 = m->buf[1];
+  if (sync) *sync = m->d_peer_sync;
+  if (nv) *nv = m->hm.nv;
+  return TSG_OK;
+}
+
+tsg_status tsg_mesh_slots(tsg_mesh* m, const int64_t* ids, int64_t n, int64_t* slots_out) {
+  TSG_LOCK_MESH(m);
+  if (!m || n < 0 || (n > 0 && (!ids || !slots_out))) return fail(TSG_ERR_INVALID, "bad arguments");
+  for (int64_t i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "vertex id out of range");
+    slots_out[i] = m->hm.rank[ids[i]];
+  }
+  return TSG_OK;
+}
+
+tsg_status tsg_peer_setup(tsg_mesh* m, int32_t rank, int32_t world, void* const* peer_buf0, void* const* peer_buf1,
+                          void* const* peer_sync, const int64_t* peer_nv, int64_t n_push, const int32_t* push_peer,
+                          const int64_t* push_src_ids, const int64_t* push_dst_slots) {
+  TSG_LOCK_MESH(m);
+  if (!m || world < 2 || world > tsg::kMaxPeers || rank < 0 || rank >= world || !peer_buf0 || !peer_buf1 ||
+      !peer_sync || !peer_nv || n_push < 0 || (n_push > 0 && (!push_peer || !push_src_ids || !push_dst_slots)))
+    return fail(TSG_ERR_INVALID, "bad peer setup arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  tsg_status st = tsg_peer_local(m, nullptr, nullptr, nullptr, nullptr);
+  if (st) return st;
+  if (peer_sync[rank] != m->d_peer_sync || peer_buf0[rank] != m->buf[0] || peer_buf1[rank] != m->buf[1])
+    return fail(TSG_ERR_INVALID, "the rank's own entry must be its tsg_peer_local pointers");
+  std::vector<tsg::PeerEntry> tab(world);
+  for (int r = 0; r < world; ++r) {
+    if (!peer_buf0[r] || !peer_buf1[r] || !peer_sync[r] || peer_nv[r] < 0)
+      return fail(TSG_ERR_INVALID, "missing peer mapping");
+    tab[r] = tsg::PeerEntry{static_cast<tsg::PeerSync*>(peer_sync[r]), peer_buf0[r], peer_buf1[r], peer_nv[r]};
+  }
+  std::vector<int32_t> pp(n_push);
+  std::vector<uint32_t> src(n_push), dst(n_push);
+  for (int64_t i = 0; i < n_push; ++i) {
+    const int32_t q = push_peer[i];
+    if (q < 0 || q >= world || q == rank) return fail(TSG_ERR_INVALID, "push peer out of range");
+    if (push_src_ids[i] < 0 || push_src_ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "push source out of range");
+    if (push_dst_slots[i] < 0 || push_dst_slots[i] >= peer_nv[q]) return fail(TSG_ERR_INVALID, "push slot out of range");
+    pp[i] = q;
+    src[i] = static_cast<uint32_t>(m->hm.rank[push_src_ids[i]]);
+    dst[i] = static_cast<uint32_t>(push_dst_slots[i]);
+  }
+  cudaFree(m->d_peer_tab);
+  cudaFree(m->d_push_peer);
+  cudaFree(m->d_push_src);
+  cudaFree(m->d_push_dst);
+  m->d_peer_tab = nullptr;
+  m->d_push_peer = nullptr;
+  m->d_push_src = m->d_push_dst = nullptr;
+  int64_t b = 0;
+  cudaStream_t s = m->ctx->stream;
+  if ((st = upload(&m->d_peer_tab, tab, &b, s))) return st;
+  if ((st = upload(&m->d_push_peer, pp, &b, s))) return st;
+  if ((st = upload(&m->d_push_src, src, &b, s))) return st;
+  if ((st = upload(&m->d_push_dst, dst, &b, s))) return st;
+  TSG_CUDA(cudaStreamSynchronize(s));
+  m->n_push = n_push;
+  m->peer_rank = rank;
+  m->peer_world = world;
+  m->gc.reset();
+  return TSG_OK;
+}
+
+tsg_status tsg_peer_prepare(tsg_mesh* m, const tsg_smooth_cfg* c) {
+  TSG_LOCK_MESH(m);
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  tsg_status st = validate_cfg(c);
+  if (st) return st;
+  if (m->peer_world < 2) return fail(TSG_ERR_INVALID, "tsg_peer_setup first");
+  if (c->form != TSG_FORM_A) return fail(TSG_ERR_INVALID, "the peer-memory partitioned driver runs Form A");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  if ((st = peer_graph(m, c))) return st;
+  TSG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  return TSG_OK;
+}
+
+tsg_status tsg_peer_clear(tsg_mesh* m) {
+  TSG_LOCK_MESH(m);
+  if (!m) return fail(TSG_ERR_INVALID, "null mesh");
+  m->peer_world = 0;
+  m->n_push = 0;
+  m->gc.reset();
+  return TSG_OK;
+}
+
+tsg_status tsg_ipc_handle(const void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return fail(TSG_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  TSG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof h == TSG_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  std::memcpy(handle_out, &h, sizeof h);
+  return TSG_OK;
+}
+
+tsg_status tsg_ipc_open(tsg_context* ctx, const void* handle, void** dev_ptr_out) {
+  TSG_LOCK_CTX(ctx);
+  if (!ctx || !handle || !dev_ptr_out) return fail(TSG_ERR_INVALID, "null argument");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  TSG_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return TSG_OK;
+}
+
+tsg_status tsg_ipc_close(tsg_context* ctx, void* dev_ptr) {
+  TSG_LOCK_CTX(ctx);
+  if (!ctx || !dev_ptr) return fail(TSG_ERR_INVALID, "null argument");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  TSG_CUDA(cudaIpcCloseMemHandle(dev_ptr));
   return TSG_OK;
 }
 

@@ -30,6 +30,15 @@ inline tsg_status fail(tsg_status code, const std::string& msg) {
                            std::string(#call) + ": " + cudaGetErrorString(e_));               \
   } while (0)
 
+// After a kernel launch: the launch error with the source line that made it.
+#define TSG_LAUNCHED()                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess)                                                                     \
+      return tsg_abi::fail(TSG_ERR_CUDA, std::string("kernel launch at " __FILE__ ":") +       \
+                                             std::to_string(__LINE__) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
 struct tsg_context {
   int device = 0;
   cudaStream_t stream = nullptr;

@@ -189,9 +189,9 @@ tsg_status tsg_quality_tri_alpha(tsg_context* ctx, int64_t nv, const double* xy,
   if (nv) TSG_CUDA(cudaMemcpyAsync(dxy, xy, sizeof(double2) * nv, cudaMemcpyHostToDevice, s));
   if (nt) TSG_CUDA(cudaMemcpyAsync(dtri, tri, sizeof(int32_t) * 3 * nt, cudaMemcpyHostToDevice, s));
   audit_alpha<<<grid_of(nt), kThreads, 0, s>>>(dxy, dtri, nt, dalpha, dacc);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   audit_first<<<grid_of(nt), kThreads, 0, s>>>(dalpha, nt, dacc);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   if (nt) TSG_CUDA(cudaMemcpyAsync(alpha_out, dalpha, sizeof(double) * nt, cudaMemcpyDeviceToHost, s));
   AuditScratch h{};
   TSG_CUDA(cudaMemcpyAsync(&h, dacc, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -236,7 +236,7 @@ tsg_status tsg_quality_vertex_minima(tsg_context* ctx, int64_t nv, const int64_t
   if (m) TSG_CUDA(cudaMemcpyAsync(dinc, inc, sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
   if (nt && alpha) TSG_CUDA(cudaMemcpyAsync(dalpha, alpha, sizeof(double) * nt, cudaMemcpyHostToDevice, s));
   audit_vertex_minima<<<grid_of(nv), kThreads, 0, s>>>(doff, dinc, dalpha, nv, dout);
-  TSG_CUDA(cudaGetLastError());
+  TSG_LAUNCHED();
   TSG_CUDA(cudaMemcpyAsync(vmin_out, dout, sizeof(double) * nv, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
   return TSG_OK;

@@ -352,6 +352,74 @@ class DeviceLoop:
         return mesh.dist_end(cfg)
 
 
+# ---- peer-memory partitioned loop (tsg_peer_*: halo stores and barrier inside the graph) ----
+
+def _groups(ids: np.ndarray, counts) -> list:
+    out, o = [], 0
+    for c in counts:
+        out.append(ids[o:o + c])
+        o += c
+    return out
+
+
+def peer_info(mesh, part: Partition) -> dict:
+    """What the other ranks need from this rank: its buffers / sync block, its vertex count, and
+    for every sender q the device slots of the halo vertices q sends (in q's send order:
+    ascending global id on both sides)."""
+    b0, b1, sync, nv = mesh.peer_local()
+    recv = _groups(part.recv_ids, part.recv_counts)
+    return {"rank": part.rank, "ptrs": (b0, b1, sync), "nv": nv, "recv_slots": [mesh.slots(g) for g in recv]}
+
+
+def connect_peers(mesh, part: Partition, infos: list, mapped: list):
+    """tsg_peer_setup from every rank's peer_info and the peers' pointers as mapped in this
+    process (`mapped[r] = (buf0, buf1, sync)`; entry `part.rank` = this mesh's own)."""
+    send = _groups(part.send_ids, part.send_counts)
+    peer, src, dst = [], [], []
+    for r in range(part.world):
+        if r == part.rank or len(send[r]) == 0:
+            continue
+        d = infos[r]["recv_slots"][part.rank]
+        if len(d) != len(send[r]):
+            raise RuntimeError(f"rank {part.rank} sends {len(send[r])} vertices to {r}, which expects {len(d)}")
+        peer.append(np.full(len(d), r, dtype=np.int32))
+        src.append(send[r])
+        dst.append(d)
+    cat = lambda xs, t: np.concatenate(xs).astype(t) if xs else np.zeros(0, dtype=t)
+    mesh.peer_setup(part.rank, part.world, [m[0] for m in mapped], [m[1] for m in mapped], [m[2] for m in mapped],
+                    [i["nv"] for i in infos], cat(peer, np.int32), cat(src, np.int64), cat(dst, np.int64))
+
+
+def connect_peers_local(meshes: list, parts: list):
+    """All partitions in this process (one device or several): raw device pointers."""
+    infos = [peer_info(m, p) for m, p in zip(meshes, parts)]
+    for m, p in zip(meshes, parts):
+        connect_peers(m, p, infos, [i["ptrs"] for i in infos])
+
+
+def connect_peers_ipc(ctx, mesh, part: Partition, dist) -> list:
+    """One process per GPU: the buffers are shared as CUDA IPC handles through
+    torch.distributed (all_gather_object) and mapped with tsg_ipc_open.  Returns the mapped
+    pointers to release with ctx.ipc_close after the last smooth."""
+    from . import capi
+
+    info = peer_info(mesh, part)
+    own = info.pop("ptrs")
+    info["handles"] = tuple(capi.ipc_handle(p) for p in own)
+    infos = [None] * part.world
+    dist.all_gather_object(infos, info)
+    mapped, opened = [], []
+    for r, inf in enumerate(infos):
+        if r == part.rank:
+            mapped.append(own)
+        else:
+            ptrs = tuple(ctx.ipc_open(h) for h in inf["handles"])
+            mapped.append(ptrs)
+            opened.extend(ptrs)
+    connect_peers(mesh, part, infos, mapped)
+    return opened
+
+
 def gather_coords(part: Partition, owned_xy: np.ndarray, nv: int):
     """All owned coordinates to every rank (gloo / nccl object gather), in global order."""
     import torch.distributed as dist

@@ -160,27 +160,24 @@ def test_upload_rejects_malformed_descriptions(capi, gpu_ctx, ts):
     upload().free()  # the untouched description still uploads
 
 
-def test_concurrent_smooth_calls_share_the_default_context(ts):
-    """The drop-in smooth() shares one process-wide device context; concurrent calls on
-    distinct meshes from several host threads (the GIL is released) give the sequential
-    results (tsg_context::mu serialises the C-ABI calls)."""
-    import threading
-
-    seeds = [3, 4, 5, 6]
-    want = []
-    for s in seeds:
-        m = ts.generate_delaunay(8000, seed=s)
-        ts.smooth(m, form="a", max_iters=20, move_tol=0.0)
-        want.append(m.points())
+_CONCURRENT_SCRIPT = r"""
+import sys, threading
+sys.path.insert(0, sys.argv[1])
+import paper_1502_00355_b200 as ts
+seeds = [3, 4, 5, 6]
+want = []
+for s in seeds:
+    m = ts.generate_delaunay(8000, seed=s)
+    ts.smooth(m, form="a", max_iters=20, move_tol=0.0)
+    want.append(m.points())
+for rep in range(3):
     meshes = [ts.generate_delaunay(8000, seed=s) for s in seeds]
     errors = []
-
     def work(m):
         try:
             ts.smooth(m, form="a", max_iters=20, move_tol=0.0)
-        except Exception as exc:  # pragma: no cover - reported below
+        except Exception as exc:
             errors.append(exc)
-
     threads = [threading.Thread(target=work, args=(m,)) for m in meshes]
     for t in threads:
         t.start()
@@ -189,3 +186,22 @@ def test_concurrent_smooth_calls_share_the_default_context(ts):
     assert not errors, errors
     for m, w in zip(meshes, want):
         assert m.points() == w
+print("ok")
+"""
+
+
+def test_concurrent_smooth_calls_share_the_default_context():
+    """The drop-in smooth() shares one process-wide device context; concurrent calls on
+    distinct meshes from several host threads (the GIL is released) give the sequential
+    results (tsg_context::mu serialises the C-ABI calls).  Runs in a child process with
+    TSG_SEGV_TRACE=1 so that a crash is reported with its native stack instead of ending the
+    test session."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSG_SEGV_TRACE="1")
+    r = subprocess.run([sys.executable, "-c", _CONCURRENT_SCRIPT, root], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.returncode, r.stdout[-2000:], r.stderr[-6000:])
