@@ -75,3 +75,63 @@ def test_peer_partitions_equal_one_mesh(capi, ts, world, kind, tol):
     meshes[0].smooth(capi.make_cfg(form="a", max_iters=3))
     for m in meshes:
         m.free()
+
+
+def _ipc_worker(rank, world, port_num, part_dir, passes, out_path):
+    import os
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    from paper_1502_00355_b200 import capi, distributed as D
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_num}", rank=rank, world_size=world)
+    part, meta = D.load_partition(part_dir, rank)
+    ctx = capi.Context(0)
+    mesh = capi.DeviceMesh(ctx, part.xy, part.tri, part.topo, order=capi.hilbert_order(part.xy))
+    opened = D.connect_peers_ipc(ctx, mesh, part, dist)
+    cfg = capi.make_cfg(form="a", max_iters=passes, move_tol=0.0, bbox_diag=meta["bbox_diag"])
+    mesh.peer_prepare(cfg)
+    dist.barrier()
+    r = mesh.smooth(cfg)
+    full = D.gather_coords(part, mesh.get_coords()[part.owned], meta["nv"])
+    if rank == 0:
+        np.savez(out_path, xy=full, acc=r["accepted"], it=r["iterations"])
+    dist.barrier()
+    for p in opened:
+        ctx.ipc_close(p)
+    mesh.free()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_peer_partitions_over_cuda_ipc_processes(capi, ts, tmp_path):
+    """One process per partition (two processes sharing cuda:0), buffers shared as CUDA IPC
+    handles (distributed.connect_peers_ipc, the bench's --transport p2p): the gathered result
+    equals one mesh's run bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_1502_00355_b200 import distributed as D
+
+    xy, tri = ts.delaunay_arrays(20000, 12)
+    topo = ts.topology(len(xy), tri)
+    world, passes = 2, 8
+    owner = D.owners_by_order(capi.hilbert_order(xy), world)
+    part_dir = str(tmp_path / "parts")
+    D.write_partitions(part_dir, world, owner, xy, tri, topo, ts.bbox_diagonal(xy))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port_num = s.getsockname()[1]
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_ipc_worker, args=(world, port_num, part_dir, passes, out), nprocs=world, join=True)
+    r = np.load(out)
+    ctx = capi.Context(0)
+    ref = capi.DeviceMesh(ctx, xy, tri, topo)
+    want = ref.smooth(capi.make_cfg(form="a", max_iters=passes, move_tol=0.0))
+    assert int(r["it"]) == want["iterations"] and np.array_equal(r["acc"], want["accepted"])
+    assert np.array_equal(r["xy"].view(np.uint64), ref.get_coords().view(np.uint64))
+    ref.free()
