@@ -35,6 +35,7 @@ using tsg_abi::g_err;
 constexpr int kMaxSmallDeg = 10;
 constexpr int kMaxMedDeg = 31;
 constexpr tsg::Tiers kTiers{kMaxSmallDeg, kMaxMedDeg};
+constexpr int kGraphUnroll = 4;  // passes per WHILE-body iteration (graph_unroll)
 constexpr int kHubCap = 4096;     // hub entries staged in shared memory
 constexpr int kTileThreads = 256;  // tile_update: threads per 1024-slot tile
 constexpr int kTileExtCap = 2048;  // ... external coordinates staged in shared memory
@@ -1394,6 +1395,19 @@ tsg_status tsg_alpha_extrema(tsg_mesh* m, double* min_out, double* max_out, int6
 
 namespace {
 
+// Passes per WHILE-body iteration (TSG_GRAPH_UNROLL overrides, 1..16).  Measured on B200:
+// Form A without side rows (cfg2, 1M Delaunay) 45.8 -> 43.7 us per pass at 4; with the
+// persistent side kernel (cfg3) unrolling loses its dispatch order (0.459 -> 0.573 ms), so 1.
+int graph_unroll(const tsg_mesh* m, const tsg_smooth_cfg* c) {
+  static const int env = [] {
+    const char* e = std::getenv("TSG_GRAPH_UNROLL");
+    return e ? std::max(1, std::min(16, std::atoi(e))) : 0;
+  }();
+  if (env) return env;
+  const bool side_rows = c->form == TSG_FORM_A && !m->hm.large.empty();
+  return c->max_iters >= 8 && !side_rows ? kGraphUnroll : 1;
+}
+
 // Resets the pass state and enqueues a whole smooth() as one launch of the cached
 // conditional-WHILE graph on the context stream (no synchronisation).
 tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* kernels_per_pass) {
@@ -1424,10 +1438,16 @@ tsg_status smooth_enqueue_graph(tsg_mesh* m, const tsg_smooth_cfg* c, int64_t* k
     TSG_CUDA(cudaGraphAddNode(&node, g.graph, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     TSG_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    // The WHILE body holds `unroll` passes: the conditional re-launch of the body is paid once
+    // per `unroll` passes.  After the stop rule fires inside the body, the remaining passes of the
+    // body are empty (every node kernel and finalize_pass return on `done`).
+    const int unroll = graph_unroll(m, c);
     int64_t k = 0;
-    st = dispatch(m, [&](auto E) {
-      return decltype(E)::enqueue_pass(m, *c, s, tol_abs, h, 1, nullptr, nullptr, nullptr, &k);
-    });
+    for (int u = 0; u < unroll && !st; ++u)
+      st = dispatch(m, [&](auto E) {
+        return decltype(E)::enqueue_pass(m, *c, s, tol_abs, h, 1, nullptr, nullptr, nullptr, &k);
+      });
+    k /= unroll;
     cudaGraph_t captured = nullptr;
     cudaError_t e = cudaStreamEndCapture(s, &captured);
     if (st) return st;
