@@ -41,7 +41,11 @@ build/tsg_prep.o: $(CSRC)/tsg_prep.cpp $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.h
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(TSG_SO): build/tsg_engine.o build/tsg_quality.o build/tsg_prep.o
+build/tsg_topo.o: $(CSRC)/tsg_topo.cu $(CSRC)/tsg_internal.hpp include/tsg.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_topo.log || (cat build/ptxas_topo.log; false)
+
+$(TSG_SO): build/tsg_engine.o build/tsg_quality.o build/tsg_topo.o build/tsg_prep.o
 	$(NVCC) -shared $(ARCH) -Xcompiler -fPIC -o $@ $^ -lpthread
 
 build/host/%.o: $(CSRC)/host/%.cpp $(wildcard include/trismooth/*.hpp) include/tsg.h

@@ -31,6 +31,9 @@ struct Topology64 {
 
 Topology64 build_topology(int64_t nv, const int32_t* tri, int64_t nt);
 
+/// The same topology built on the device (tsg_topology: radix sorts, no int32 raw list).
+Topology64 device_topology(int64_t nv, const int32_t* tri, int64_t nt, tsg_context* ctx = nullptr);
+
 /// The process-wide device context (device = $TSG_DEVICE, else $LOCAL_RANK, else 0).
 /// Throws Error when no CUDA device is usable: there is no CPU fallback.
 tsg_context* default_context();

@@ -301,6 +301,15 @@ tsg_status tsg_ipc_handle(const void* dev_ptr, void* handle_out);
 tsg_status tsg_ipc_open(tsg_context* ctx, const void* handle, void** dev_ptr_out);
 tsg_status tsg_ipc_close(tsg_context* ctx, void* dev_ptr);
 
+/* ---- mesh topology on the device (find_neighbors + determine_constraints,
+ * proj/src/topology.cpp:12-95, without the int32 raw list) ----
+ * nbr_off / inc_off: nv+1 int64; nbr: unique neighbours, each row ascending (capacity nbr_cap,
+ * 6*nt always suffices; the count is returned in n_nbr_out); inc: 3*nt incident triangles,
+ * each row ascending; boundary: 1 = isolated or some neighbour multiplicity != 2. */
+tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, const int32_t* tri, int64_t* nbr_off,
+                        int32_t* nbr, int64_t nbr_cap, int64_t* inc_off, int32_t* inc, uint8_t* boundary,
+                        int64_t* n_nbr_out);
+
 #ifdef __cplusplus
 }
 #endif

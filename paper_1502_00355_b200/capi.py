@@ -36,7 +36,7 @@ EXPORTS = (
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
     "tsg_debug_trace", "tsg_mesh_side_schedule", "tsg_quality_tri_alpha", "tsg_quality_vertex_minima",
     "tsg_peer_local", "tsg_mesh_slots", "tsg_peer_setup", "tsg_peer_prepare", "tsg_peer_clear", "tsg_ipc_handle", "tsg_ipc_open",
-    "tsg_ipc_close",
+    "tsg_ipc_close", "tsg_topology",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -124,6 +124,7 @@ def lib() -> C.CDLL:
             "tsg_ipc_handle": (i32, [P, P]),
             "tsg_ipc_open": (i32, [P, P, C.POINTER(P)]),
             "tsg_ipc_close": (i32, [P, P]),
+            "tsg_topology": (i32, [P, i64, i64, P, P, P, i64, P, P, P, C.POINTER(i64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -206,6 +207,22 @@ class Context:
 
     def ipc_close(self, dev_ptr: int):
         check(lib().tsg_ipc_close(self.h, C.c_void_p(dev_ptr)), "tsg_ipc_close")
+
+    def topology(self, nv: int, tri) -> dict:
+        """Adjacency + constraints on the device (tsg_topology): same dict as
+        paper_1502_00355_b200.topology (find_neighbors / determine_constraints)."""
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        nt = len(tri)
+        nbr_off = np.empty(nv + 1, dtype=np.int64)
+        inc_off = np.empty(nv + 1, dtype=np.int64)
+        nbr = np.empty(max(1, 6 * nt), dtype=np.int32)
+        inc = np.empty(max(1, 3 * nt), dtype=np.int32)
+        bnd = np.empty(nv, dtype=np.uint8)
+        n = C.c_int64()
+        check(lib().tsg_topology(self.h, nv, nt, _ptr(tri), _ptr(nbr_off), _ptr(nbr), len(nbr), _ptr(inc_off),
+                                 _ptr(inc), _ptr(bnd), C.byref(n)), "tsg_topology")
+        return dict(nbr_off=nbr_off, nbr=nbr[: n.value].copy(), inc_off=inc_off, inc=inc[: 3 * nt],
+                    boundary=bnd)
 
     def close(self):
         if self.h:

@@ -1,9 +1,10 @@
 // smooth() on the B200 (include/trismooth/smoothing.hpp) and the device-mesh plumbing of
 // include/trismooth/gpu.hpp.
 //
-// Pipeline and statistics follow proj/src/smoothing.cpp:146-182; the pass loop
-// (:76-142) runs in libtsg.so as one CUDA-graph launch.  Host prep (adjacency,
-// constraints, locality order) stays in C++ on the host, as in the reference.
+// Pipeline and statistics follow proj/src/smoothing.cpp:146-182; the pass loop (:76-142) runs
+// in libtsg.so as one CUDA-graph launch, the adjacency and constraints (find_neighbors /
+// determine_constraints) are built on the device (tsg_topology) and installed into the mesh;
+// the device layout (locality order, tiles) is prepared on the host (tsg_prep.cpp).
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -56,6 +57,24 @@ tsg_context* default_context() {
     check(tsg_context_create(dev % n, &ctx), "tsg_context_create");
   }
   return ctx;
+}
+
+Topology64 device_topology(int64_t nv, const int32_t* tri, int64_t nt, tsg_context* ctx) {
+  if (!ctx) ctx = default_context();
+  Topology64 T;
+  T.nbr_off.resize(nv + 1);
+  T.inc_off.resize(nv + 1);
+  T.nbr.resize(static_cast<size_t>(std::max<int64_t>(1, 6 * nt)));
+  T.inc.resize(static_cast<size_t>(std::max<int64_t>(1, 3 * nt)));
+  T.boundary.resize(nv);
+  int64_t n = 0;
+  check(tsg_topology(ctx, nv, nt, tri, T.nbr_off.data(), T.nbr.data(), static_cast<int64_t>(T.nbr.size()),
+                     T.inc_off.data(), T.inc.data(), T.boundary.data(), &n),
+        "tsg_topology");
+  T.nbr.resize(n);
+  T.nbr.shrink_to_fit();
+  T.inc.resize(3 * nt);
+  return T;
 }
 
 double bbox_diagonal(const double* xy, int64_t nv) {
@@ -165,35 +184,45 @@ RunStats smooth(Mesh& mesh, const SmoothConfig& config) {
   init_flags(mesh);
   const double init_flags_ms = ms_since(t0);
 
-  t0 = Clock::now();
-  const Adjacency adj = find_neighbors(mesh);
-  const double topo_ms = ms_since(t0);
-
-  t0 = Clock::now();
-  determine_constraints(mesh, adj);
-  const double constr_host_ms = ms_since(t0);
-
+  // Host arrays the device path reads: coordinates and corners in original numbering.
   const int64_t nv = mesh.vertex_count(), nt = mesh.triangle_count();
   std::vector<double> xy(2 * nv);
   std::vector<int32_t> tri(3 * nt);
-  gpu::Topology64 topo;
-  topo.boundary.resize(nv);
   mesh.visit([&](const auto& m) {
     for (int64_t v = 0; v < nv; ++v) {
       const Point p = m.position(static_cast<int>(v));
       xy[2 * v] = p.x;
       xy[2 * v + 1] = p.y;
-      topo.boundary[v] = m.is_boundary(static_cast<int>(v)) ? 1 : 0;
     }
     for (int64_t t = 0; t < nt; ++t) {
       const auto c = m.tri(static_cast<int>(t));
       tri[3 * t] = c[0], tri[3 * t + 1] = c[1], tri[3 * t + 2] = c[2];
     }
   });
-  topo.nbr_off.assign(adj.unique.offsets.begin(), adj.unique.offsets.end());
-  topo.inc_off.assign(adj.incident.offsets.begin(), adj.incident.offsets.end());
-  topo.nbr.assign(adj.unique.values.begin(), adj.unique.values.end());
-  topo.inc.assign(adj.incident.values.begin(), adj.incident.values.end());
+
+  // find_neighbors + determine_constraints (proj/src/topology.cpp:12-95) on the device: the
+  // same unique / incident rows and flags, with int64 offsets (no int32 raw list).
+  t0 = Clock::now();
+  gpu::Topology64 topo = gpu::device_topology(nv, tri.data(), nt, ctx);
+  const double topo_ms = ms_since(t0);
+
+  // Install the adjacency and the constraint flags into the mesh as the reference does
+  // (tests read them after smooth()).  The reference's Csr is int-indexed: beyond 2^31 entries
+  // the rows stay device-side only.
+  t0 = Clock::now();
+  const bool fits = topo.nbr_off[nv] < (int64_t{1} << 31) && topo.inc_off[nv] < (int64_t{1} << 31);
+  mesh.visit([&](auto& m) {
+    if (fits) {
+      Csr unique, incident;
+      unique.offsets.assign(topo.nbr_off.begin(), topo.nbr_off.end());
+      unique.values.assign(topo.nbr.begin(), topo.nbr.end());
+      incident.offsets.assign(topo.inc_off.begin(), topo.inc_off.end());
+      incident.values.assign(topo.inc.begin(), topo.inc.end());
+      m.assign_adjacency(unique, incident);
+    }
+    for (int64_t v = 0; v < nv; ++v) m.set_boundary(static_cast<int>(v), topo.boundary[v] != 0);
+  });
+  const double constr_host_ms = ms_since(t0);
 
   // Locality order only where it cannot change results: Form A reads every neighbour from the
   // previous pass and the device keeps each neighbour row in original-id order (K10).

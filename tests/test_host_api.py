@@ -177,3 +177,60 @@ def test_bbox_diagonal_matches_reference_formula():
     xy, _ = ts.delaunay_arrays(1000, 3)
     d = ts.bbox_diagonal(xy)
     assert d == math.hypot(xy[:, 0].max() - xy[:, 0].min(), xy[:, 1].max() - xy[:, 1].min())
+
+
+def _local_delaunay_violations(xy, tri, sample, rng):
+    """Edges (of `sample` random triangles) whose opposite vertex across the edge lies strictly
+    inside the triangle's circumcircle beyond rounding: local Delaunay on every edge is
+    equivalent to the global empty-circumcircle property."""
+    nt = len(tri)
+    idx = rng.choice(nt, size=min(sample, nt), replace=False)
+    # edge -> triangles map via sorted edge keys (all triangles: the neighbour may be anywhere)
+    e = np.concatenate([tri[:, [0, 1]], tri[:, [1, 2]], tri[:, [2, 0]]])
+    opp = np.concatenate([tri[:, 2], tri[:, 0], tri[:, 1]])
+    owner = np.tile(np.arange(nt), 3)
+    key = np.minimum(e[:, 0], e[:, 1]).astype(np.int64) * len(xy) + np.maximum(e[:, 0], e[:, 1])
+    order = np.argsort(key, kind="stable")
+    ks, os_, ow = key[order], opp[order], owner[order]
+    pair = np.flatnonzero(ks[1:] == ks[:-1])  # interior edges: two consecutive entries
+    sel = np.isin(ow[pair], idx)
+    pair = pair[sel]
+    a, b = ow[pair], os_[pair + 1]  # triangle a, the vertex opposite across the shared edge
+    p = xy[tri[a]]
+    d = xy[b]
+    ax, ay = p[:, 0, 0] - d[:, 0], p[:, 0, 1] - d[:, 1]
+    bx, by = p[:, 1, 0] - d[:, 0], p[:, 1, 1] - d[:, 1]
+    cx, cy = p[:, 2, 0] - d[:, 0], p[:, 2, 1] - d[:, 1]
+    det = ((ax * ax + ay * ay) * (bx * cy - cx * by) - (bx * bx + by * by) * (ax * cy - cx * ay)
+           + (cx * cx + cy * cy) * (ax * by - bx * ay))
+    scale = ((ax * ax + ay * ay) * (np.abs(bx * cy) + np.abs(cx * by))
+             + (bx * bx + by * by) * (np.abs(ax * cy) + np.abs(cx * ay))
+             + (cx * cx + cy * cy) * (np.abs(ax * by) + np.abs(bx * ay)))
+    return int((det > 1e-12 * scale).sum()), len(pair)
+
+
+def test_spatial_insertion_equals_generation_order_at_1m(golden_big):
+    """Beyond 2M points the generator inserts along a Hilbert curve; the triangulation must be
+    the same canonical output as the reference's generation-order insertion: forced on the 1M
+    golden point set it reproduces the reference's triangles exactly."""
+    case = golden_big["d1m_formA_10"]
+    xy, tri = ts.delaunay_arrays(1_000_000, 42)
+    assert sha(tri) == case["tri"]
+    spatial = ts.triangulate(xy, True)
+    assert sha(spatial) == case["tri"]
+
+
+def test_spatial_generator_is_delaunay_at_4m():
+    """A 4M-point mesh (spatial insertion path): CCW, canonical (smallest corner first, sorted),
+    Euler count nt = 2n - 2 - h, and no local Delaunay violation on 200K sampled triangles."""
+    xy, tri = ts.delaunay_arrays(4_000_000, 7)
+    n = len(xy)
+    assert tri.shape[0] > 2 * n - 2 - 4 * int(np.sqrt(n))  # h (hull size) is O(sqrt n)
+    assert (tri[:, 0] < tri[:, 1]).all() and (tri[:, 0] < tri[:, 2]).all()
+    first = tri[:, 0].astype(np.int64) * n * n + tri[:, 1].astype(np.int64) * n + tri[:, 2]
+    assert (np.diff(first) > 0).all()
+    p = xy[tri]
+    area = (p[:, 1, 0] - p[:, 0, 0]) * (p[:, 2, 1] - p[:, 0, 1]) - (p[:, 1, 1] - p[:, 0, 1]) * (p[:, 2, 0] - p[:, 0, 0])
+    assert (area > 0).all()
+    bad, checked = _local_delaunay_violations(xy, tri, 200_000, np.random.default_rng(1))
+    assert checked > 250_000 and bad == 0
