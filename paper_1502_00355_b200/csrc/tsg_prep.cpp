@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <thread>
 
@@ -82,6 +84,18 @@ uint32_t hilbert_d(uint32_t x, uint32_t y) {
   }
   return d;
 }
+
+// TSG_PREP_TIMING=1: per-phase wall times of build_host_mesh on stderr (profiling aid).
+struct PhaseTimer {
+  bool on = std::getenv("TSG_PREP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tsg prep] %-24s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 }  // namespace
 
@@ -248,18 +262,28 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   const int64_t nv = d.nv, nt = d.nt;
   if (nv <= 0 || nt <= 0) return "mesh must have vertices and triangles";
   if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
+  PhaseTimer pt;
   if (std::string e = validate_desc(d); !e.empty()) return e;
+  pt.mark("validate");
   hm.nv = nv;
   hm.nt = nt;
   hm.order.resize(nv);
   hm.rank.resize(nv);
   if (d.order) {
-    std::vector<uint8_t> seen(nv, 0);
-    for (int64_t s = 0; s < nv; ++s) {
-      const int64_t v = d.order[s];
-      if (v < 0 || v >= nv || seen[v]) return "order is not a permutation of 0..nv-1";
-      seen[v] = 1;
-      hm.order[s] = v;
+    {
+      std::vector<std::atomic<uint8_t>> seen(nv);
+      std::atomic<bool> ok{true};
+      parallel_ranges(nv, [&](int64_t b, int64_t e) {
+        for (int64_t s = b; s < e; ++s) {
+          const int64_t v = d.order[s];
+          if (v < 0 || v >= nv || seen[v].exchange(1, std::memory_order_relaxed)) {
+            ok = false;
+            return;
+          }
+          hm.order[s] = v;
+        }
+      });
+      if (!ok) return "order is not a permutation of 0..nv-1";
     }
     // Degree sort inside windows of kSigma consecutive slots of the locality order (SELL-C-σ
     // style): warps then see near-uniform valences (no divergent loop tails) while every
@@ -278,11 +302,14 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
         std::stable_sort(first, last, [&](int64_t x, int64_t y) { return degree_key(x) > degree_key(y); });
       }
     });
-    for (int64_t s = 0; s < nv; ++s) hm.rank[hm.order[s]] = s;
+    parallel_ranges(nv, [&](int64_t b, int64_t e) {
+      for (int64_t s = b; s < e; ++s) hm.rank[hm.order[s]] = s;
+    });
   } else {
     for (int64_t s = 0; s < nv; ++s) hm.order[s] = hm.rank[s] = s;
   }
 
+  pt.mark("slot order");
   // Row lengths: movable vertices only; interior (all multiplicities 2) implies
   // #incident == #unique neighbours, which the fan encoding relies on.
   std::vector<uint32_t> deg(nv, 0);
@@ -322,6 +349,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   hm.cycrot.assign(total, 0);
   hm.has_cycle.assign(nv, 0);
 
+  pt.mark("row lengths + alloc");
   // Device triangle order: identity, or by the smallest slot among the corners (stable) so
   // that the triangle kernels stream coordinates in the same locality order as the vertices.
   hm.tri_order.resize(nt);
@@ -352,6 +380,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     }
   });
 
+  pt.mark("triangle order");
   std::atomic<int64_t> broken{-1};
   parallel_ranges(nv, [&](int64_t b, int64_t e) {
     for (int64_t s = b; s < e; ++s) {
@@ -415,6 +444,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
   });
   if (broken >= 0) return "incident / neighbour lists disagree at vertex " + std::to_string(broken.load());
 
+  pt.mark("rows, fans, cycles");
   // Full incident CSR (all vertices) for TwoPhase thresholds and vertex minima.
   hm.vinc_off.assign(nv + 1, 0);
   uint64_t it = 0;
@@ -437,6 +467,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     }
   });
 
+  pt.mark("incident CSR");
   hm.hubs.clear();
   hm.medium.clear();
   hm.large.clear();
@@ -447,12 +478,14 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     if (tier == 2) hm.hubs.push_back(static_cast<int32_t>(s));
     if (deg[s] > static_cast<uint32_t>(kMaxCycleDeg)) hm.large.push_back(static_cast<int32_t>(s));
   }
+  pt.mark("tier lists");
   {
     const std::string terr = build_tiles(hm, deg, kMaxCycleDeg);
     if (!terr.empty()) return terr;
     std::vector<uint8_t>().swap(hm.cycpos);  // only build_tiles reads the cycles
     std::vector<uint8_t>().swap(hm.cycrot);
   }
+  pt.mark("tiles");
   // Longest rows first: the warp tier's tail is its largest hubs.
   std::stable_sort(hm.large.begin(), hm.large.end(), [&](int32_t x, int32_t y) { return deg[x] > deg[y]; });
   return "";
