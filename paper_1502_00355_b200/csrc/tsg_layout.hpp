@@ -9,7 +9,10 @@ constexpr int kMaxCycleDeg = 31;  // tile (thread-per-vertex) rows: valence <= 3
 // Tiles of tile_update: kTile consecutive slots (the degree-sort windows of the locality
 // order).  A tile's small rows address their neighbours by LOCAL index: slot - tile base for
 // in-tile slots, kTile + position in the tile's sorted external-slot list otherwise.
-constexpr int kTile = 1024;
+#ifndef TSG_TILE
+#define TSG_TILE 1024
+#endif
+constexpr int kTile = TSG_TILE;
 constexpr uint32_t kNoLocal = 0x3fffu;  // cycle entry of a row without a single link cycle
 // Tile row word: row[j] (bits 0-13) | cycle[j] (bits 16-29) | k[j] (bits 30-31).
 constexpr uint32_t kLocalMask = 0x3fffu;
