@@ -29,7 +29,7 @@ tsg: $(TSG_SO)
 host: $(TS_SO)
 module: $(MOD_SO)
 
-build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_flow.cuh $(CSRC)/tsg_peer.cuh $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp $(CSRC)/tsg_internal.hpp include/tsg.h
+build/tsg_engine.o: $(CSRC)/tsg_engine.cu $(CSRC)/tsg_layout_dev.hpp $(CSRC)/tsg_flow.cuh $(CSRC)/tsg_peer.cuh $(CSRC)/tsg_kernels.cuh $(CSRC)/tsg_device.cuh $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp $(CSRC)/tsg_internal.hpp include/tsg.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas.log || (cat build/ptxas.log; false)
 
@@ -45,7 +45,11 @@ build/tsg_topo.o: $(CSRC)/tsg_topo.cu $(CSRC)/tsg_internal.hpp include/tsg.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_topo.log || (cat build/ptxas_topo.log; false)
 
-$(TSG_SO): build/tsg_engine.o build/tsg_quality.o build/tsg_topo.o build/tsg_prep.o
+build/tsg_layout_dev.o: $(CSRC)/tsg_layout_dev.cu $(CSRC)/tsg_layout_dev.hpp $(CSRC)/tsg_prep.hpp $(CSRC)/tsg_layout.hpp include/tsg.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_layout.log || (cat build/ptxas_layout.log; false)
+
+$(TSG_SO): build/tsg_engine.o build/tsg_quality.o build/tsg_topo.o build/tsg_layout_dev.o build/tsg_prep.o
 	$(NVCC) -shared $(ARCH) -Xcompiler -fPIC -o $@ $^ -lpthread
 
 build/host/%.o: $(CSRC)/host/%.cpp $(wildcard include/trismooth/*.hpp) include/tsg.h

@@ -310,6 +310,11 @@ tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, const int32_t*
                         int32_t* nbr, int64_t nbr_cap, int64_t* inc_off, int32_t* inc, uint8_t* boundary,
                         int64_t* n_nbr_out);
 
+/* Test hook: builds the device layout of `desc` on the GPU (tsg_layout_dev.cu) and on the host
+ * (build_host_mesh) and writes the name of the first array that differs into `mismatch`
+ * ("" when identical). */
+tsg_status tsg_debug_layout_check(tsg_context* ctx, const tsg_mesh_desc* desc, char* mismatch, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

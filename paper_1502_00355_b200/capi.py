@@ -36,7 +36,7 @@ EXPORTS = (
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
     "tsg_debug_trace", "tsg_mesh_side_schedule", "tsg_quality_tri_alpha", "tsg_quality_vertex_minima",
     "tsg_peer_local", "tsg_mesh_slots", "tsg_peer_setup", "tsg_peer_prepare", "tsg_peer_clear", "tsg_ipc_handle", "tsg_ipc_open",
-    "tsg_ipc_close", "tsg_topology",
+    "tsg_ipc_close", "tsg_topology", "tsg_debug_layout_check",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -125,6 +125,7 @@ def lib() -> C.CDLL:
             "tsg_ipc_open": (i32, [P, P, C.POINTER(P)]),
             "tsg_ipc_close": (i32, [P, P]),
             "tsg_topology": (i32, [P, i64, i64, P, P, P, i64, P, P, P, C.POINTER(i64)]),
+            "tsg_debug_layout_check": (i32, [P, C.POINTER(MeshDesc), C.c_char_p, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -207,6 +208,23 @@ class Context:
 
     def ipc_close(self, dev_ptr: int):
         check(lib().tsg_ipc_close(self.h, C.c_void_p(dev_ptr)), "tsg_ipc_close")
+
+    def layout_check(self, xy, tri, topo: dict, order=None) -> str:
+        """Builds the device layout on the GPU and on the host; returns the name of the first
+        array that differs ("" when identical) — tsg_debug_layout_check."""
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        keep = dict(nbr_off=np.ascontiguousarray(topo["nbr_off"], dtype=np.int64),
+                    nbr=np.ascontiguousarray(topo["nbr"], dtype=np.int32),
+                    inc_off=np.ascontiguousarray(topo["inc_off"], dtype=np.int64),
+                    inc=np.ascontiguousarray(topo["inc"], dtype=np.int32),
+                    boundary=np.ascontiguousarray(topo["boundary"], dtype=np.uint8))
+        order = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+        d = MeshDesc(len(xy), len(tri), _ptr(xy), _ptr(tri), _ptr(keep["nbr_off"]), _ptr(keep["nbr"]),
+                     _ptr(keep["inc_off"]), _ptr(keep["inc"]), _ptr(keep["boundary"]), _ptr(order), 0, 0)
+        buf = C.create_string_buffer(64)
+        check(lib().tsg_debug_layout_check(self.h, C.byref(d), buf, 64), "tsg_debug_layout_check")
+        return buf.value.decode()
 
     def topology(self, nv: int, tri) -> dict:
         """Adjacency + constraints on the device (tsg_topology): same dict as

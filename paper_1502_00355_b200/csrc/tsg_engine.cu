@@ -23,6 +23,7 @@
 #include "tsg_peer.cuh"
 #include "tsg_kernels.cuh"
 #include "tsg_internal.hpp"
+#include "tsg_layout_dev.hpp"
 #include "tsg_prep.hpp"
 
 namespace {
@@ -1170,35 +1171,72 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   m->layout = d->layout;
   m->prec = d->precision;
   m->rsize = d->precision == TSG_F64 ? 8 : 4;
-  const std::string err = tsg::build_host_mesh(*d, kTiers, m->hm);
-  if (!err.empty()) return fail(TSG_ERR_INVALID, err);
-  const auto& hm = m->hm;
-  const int64_t nv = hm.nv, nt = hm.nt;
   cudaStream_t s = ctx->stream;
   int64_t* b = &m->bytes;
   tsg_status st;
+  // Device layout: built on the GPU (tsg_layout_dev.cu, default) or on the host
+  // (build_host_mesh, TSG_HOST_PREP=1); identical arrays either way.
+  static const bool host_prep = std::getenv("TSG_HOST_PREP") != nullptr;
+  if (!host_prep) {
+    std::string err = tsg::validate_desc(*d);
+    if (!err.empty()) return fail(TSG_ERR_INVALID, err);
+    tsg::DeviceLayout L;
+    err = tsg::build_device_layout(s, *d, kTiers, m->hm, L);
+    if (!err.empty()) {
+      tsg::free_layout(L);
+      return fail(err.find("cuda") != std::string::npos ? TSG_ERR_CUDA : TSG_ERR_INVALID, err);
+    }
+    const auto& h = m->hm;
+    const int64_t ntiles = (h.nv + tsg::kTile - 1) / tsg::kTile;
+    m->d_off = L.off;
+    m->d_nbr = L.nbr;
+    m->d_fan = L.fan;
+    m->d_fan16 = L.fan16;
+    m->d_tmeta = L.tmeta;
+    m->d_tile_rec = L.tile_rec;
+    m->d_ext_off = L.ext_off;
+    m->d_tile_ext = L.ext;
+    m->d_trec = L.trec;
+    m->d_vinc_off = L.vinc_off;
+    m->d_vinc = L.vinc;
+    m->d_tri = L.tri;
+    m->d_order = L.order;
+    m->d_tri_order = L.tri_order;
+    const int64_t nrow = static_cast<int64_t>(h.nbr.size());
+    *b += 4 * (h.nv + 1) + 10 * nrow + 4 * h.nv + 8 * (ntiles + 1) + 12 * h.nt + 4 * (h.nv + 1) + 12 * h.nt +
+          (L.order ? 8 * (h.nv + h.nt) : 0);
+    if ((st = upload(&m->d_hubs, h.hubs, b, s))) return st;
+    if ((st = upload(&m->d_medium, h.medium, b, s))) return st;
+    if ((st = upload(&m->d_large, h.large, b, s))) return st;
+  } else {
+    const std::string err = tsg::build_host_mesh(*d, kTiers, m->hm);
+    if (!err.empty()) return fail(TSG_ERR_INVALID, err);
+    const auto& h = m->hm;
+    if ((st = upload(&m->d_off, h.off, b, s))) return st;
+    if ((st = upload(&m->d_nbr, h.nbr, b, s))) return st;
+    if ((st = upload(&m->d_fan, h.fan, b, s))) return st;
+    if ((st = upload(&m->d_fan16, h.fan16, b, s))) return st;
+    if ((st = upload(&m->d_tmeta, h.tmeta, b, s))) return st;
+    if ((st = upload(&m->d_tile_rec, h.tile_rec, b, s))) return st;
+    if ((st = upload(&m->d_ext_off, h.ext_off, b, s))) return st;
+    if ((st = upload(&m->d_tile_ext, h.ext, b, s))) return st;
+    if ((st = upload(&m->d_trec, h.trec, b, s))) return st;
+    if ((st = upload(&m->d_vinc_off, h.vinc_off, b, s))) return st;
+    if ((st = upload(&m->d_vinc, h.vinc, b, s))) return st;
+    if ((st = upload(&m->d_tri, h.tri, b, s))) return st;
+    if ((st = upload(&m->d_hubs, h.hubs, b, s))) return st;
+    if ((st = upload(&m->d_medium, h.medium, b, s))) return st;
+    if ((st = upload(&m->d_large, h.large, b, s))) return st;
+    if (d->order) {
+      if ((st = upload(&m->d_order, h.order, b, s))) return st;
+      if ((st = upload(&m->d_tri_order, h.tri_order, b, s))) return st;
+    }
+  }
+  const auto& hm = m->hm;
+  const int64_t nv = hm.nv, nt = hm.nt;
   for (void** p : {&m->buf[0], &m->buf[1], &m->init}) {
     TSG_CUDA(cudaMalloc(p, 2 * nv * m->rsize));
     *b += 2 * nv * m->rsize;
-  }
-  if ((st = upload(&m->d_off, hm.off, b, s))) return st;
-  if ((st = upload(&m->d_nbr, hm.nbr, b, s))) return st;
-  if ((st = upload(&m->d_fan, hm.fan, b, s))) return st;
-  if ((st = upload(&m->d_fan16, hm.fan16, b, s))) return st;
-  if ((st = upload(&m->d_tmeta, hm.tmeta, b, s))) return st;
-  if ((st = upload(&m->d_tile_rec, hm.tile_rec, b, s))) return st;
-  if ((st = upload(&m->d_ext_off, hm.ext_off, b, s))) return st;
-  if ((st = upload(&m->d_tile_ext, hm.ext, b, s))) return st;
-  if ((st = upload(&m->d_trec, hm.trec, b, s))) return st;
-  if ((st = upload(&m->d_vinc_off, hm.vinc_off, b, s))) return st;
-  if ((st = upload(&m->d_vinc, hm.vinc, b, s))) return st;
-  if ((st = upload(&m->d_tri, hm.tri, b, s))) return st;
-  if ((st = upload(&m->d_hubs, hm.hubs, b, s))) return st;
-  if ((st = upload(&m->d_medium, hm.medium, b, s))) return st;
-  if ((st = upload(&m->d_large, hm.large, b, s))) return st;
-  if (d->order) {
-    if ((st = upload(&m->d_order, hm.order, b, s))) return st;
-    if ((st = upload(&m->d_tri_order, hm.tri_order, b, s))) return st;
   }
   TSG_CUDA(cudaMalloc(&m->d_alpha, nt * m->rsize));
   *b += nt * m->rsize;
@@ -2320,6 +2358,47 @@ tsg_status tsg_ipc_close(tsg_context* ctx, void* dev_ptr) {
   if (!ctx || !dev_ptr) return fail(TSG_ERR_INVALID, "null argument");
   TSG_CUDA(cudaSetDevice(ctx->device));
   TSG_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return TSG_OK;
+}
+
+// Test hook: builds the layout both ways and names the first HostMesh array that differs.
+tsg_status tsg_debug_layout_check(tsg_context* ctx, const tsg_mesh_desc* d, char* mismatch, int32_t cap) {
+  TSG_LOCK_CTX(ctx);
+  if (!ctx || !d || !mismatch || cap < 1) return fail(TSG_ERR_INVALID, "null argument");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  tsg::HostMesh H, D;
+  std::string err = tsg::build_host_mesh(*d, kTiers, H);
+  if (!err.empty()) return fail(TSG_ERR_INVALID, "host: " + err);
+  tsg::DeviceLayout L;
+  err = tsg::build_device_layout(ctx->stream, *d, kTiers, D, L);
+  if (err.empty()) err = tsg::download_layout(ctx->stream, L, D);
+  tsg::free_layout(L);
+  if (!err.empty()) return fail(TSG_ERR_CUDA, "device: " + err);
+  std::string bad;
+  auto cmp = [&](const char* name, const auto& a, const auto& b2) {
+    if (bad.empty() && a != b2) bad = name;
+  };
+  cmp("order", H.order, D.order);
+  cmp("rank", H.rank, D.rank);
+  cmp("tri_order", H.tri_order, D.tri_order);
+  cmp("off", H.off, D.off);
+  cmp("nbr", H.nbr, D.nbr);
+  cmp("fan", H.fan, D.fan);
+  cmp("fan16", H.fan16, D.fan16);
+  cmp("vinc_off", H.vinc_off, D.vinc_off);
+  cmp("vinc", H.vinc, D.vinc);
+  cmp("tri", H.tri, D.tri);
+  cmp("medium", H.medium, D.medium);
+  cmp("hubs", H.hubs, D.hubs);
+  cmp("large", H.large, D.large);
+  cmp("tmeta", H.tmeta, D.tmeta);
+  cmp("tile_rec", H.tile_rec, D.tile_rec);
+  cmp("ext_off", H.ext_off, D.ext_off);
+  cmp("ext", H.ext, D.ext);
+  cmp("trec", H.trec, D.trec);
+  if (bad.empty() && (H.max_ext != D.max_ext || H.max_rec_words != D.max_rec_words || H.max_deg != D.max_deg))
+    bad = "scalars";
+  std::snprintf(mismatch, static_cast<size_t>(cap), "%s", bad.c_str());
   return TSG_OK;
 }
 

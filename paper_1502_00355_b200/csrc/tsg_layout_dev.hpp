@@ -1,0 +1,34 @@
+// Device-side layout preparation (tsg_layout_dev.cu): the device arrays of a tsg_mesh built on
+// the GPU, identical to what build_host_mesh (tsg_prep.cpp) computes on the host.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "tsg_prep.hpp"
+
+namespace tsg {
+
+// Device arrays owned by the caller after a successful build (free_layout releases them).
+// order / tri_order stay null for the identity order (no locality order given).
+struct DeviceLayout {
+  uint32_t *off = nullptr, *nbr = nullptr, *fan = nullptr, *tmeta = nullptr, *tile_rec = nullptr;
+  uint32_t *ext_off = nullptr, *ext = nullptr, *trec = nullptr, *vinc_off = nullptr, *vinc = nullptr;
+  uint16_t* fan16 = nullptr;
+  int32_t* tri = nullptr;
+  int64_t *order = nullptr, *tri_order = nullptr;
+};
+
+// Builds the layout on `s` from the host description (validated by the caller).  Fills the
+// host mirror's nv, nt, order, rank, off, nbr, fan, tri_order, medium, hubs, large, max_deg,
+// max_ext, max_rec_words.  Returns "" or an error (arrays allocated so far stay in `L`).
+std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
+                                DeviceLayout& L);
+// The remaining HostMesh arrays from the device (fan16, tri, vinc_off, vinc, tmeta, tile_rec,
+// ext_off, ext, trec): for tests that compare with build_host_mesh.
+std::string download_layout(cudaStream_t s, const DeviceLayout& L, HostMesh& hm);
+void free_layout(DeviceLayout& L);
+
+}  // namespace tsg

@@ -216,7 +216,7 @@ void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
 // proj/src/mesh.cpp:69-81): corner ids in range, CSR offsets starting at 0 and
 // non-decreasing, entries in range, neighbour rows strictly ascending.  Runs in parallel
 // chunks; returns the first problem found.
-static std::string validate_desc(const tsg_mesh_desc& d) {
+std::string validate_desc(const tsg_mesh_desc& d) {
   const int64_t nv = d.nv, nt = d.nt;
   std::atomic<int> bad{0};  // bit 0 tri, 1 nbr, 2 inc
   parallel_ranges(nt, [&](int64_t b, int64_t e) {
@@ -255,6 +255,20 @@ static std::string validate_desc(const tsg_mesh_desc& d) {
   const int f = bad.load();
   if (f & 2) return "neighbour CSR malformed (offsets decreasing, id out of range or row not strictly ascending)";
   if (f & 4) return "incident CSR malformed (offsets decreasing or triangle id out of range)";
+  if (d.order) {
+    std::vector<std::atomic<uint8_t>> seen(nv);
+    std::atomic<bool> ok{true};
+    parallel_ranges(nv, [&](int64_t b, int64_t e) {
+      for (int64_t s = b; s < e; ++s) {
+        const int64_t v = d.order[s];
+        if (v < 0 || v >= nv || seen[v].exchange(1, std::memory_order_relaxed)) {
+          ok = false;
+          return;
+        }
+      }
+    });
+    if (!ok) return "order is not a permutation of 0..nv-1";
+  }
   return {};
 }
 

@@ -24,10 +24,16 @@ namespace tsg {
 // medium (<= medium_max, a separate list) rows, CTA-per-vertex for hubs.  A small / medium fan
 // record stores ring positions with v itself at position small_max / medium_max, which must
 // fit 5 bits.
+#ifdef __CUDACC__
+#define TSG_HD __host__ __device__
+#else
+#define TSG_HD
+#endif
+
 struct Tiers {
   int32_t small_max = 12;
   int32_t medium_max = 31;
-  int tier(uint32_t deg) const {
+  TSG_HD int tier(uint32_t deg) const {
     return deg <= static_cast<uint32_t>(small_max) ? 0 : deg <= static_cast<uint32_t>(medium_max) ? 1 : 2;
   }
 };
@@ -98,6 +104,9 @@ struct FormBSchedule {
 constexpr int kChunkRecWords = 32;
 constexpr int kChunkRecMaxDeg = 15;
 
+// Structural checks of a caller's description (corner ids, CSR offsets / entries, the order
+// permutation); "" when valid.  build_host_mesh runs them first.
+std::string validate_desc(const tsg_mesh_desc& d);
 // Returns "" on success, else an error message.
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
 std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);

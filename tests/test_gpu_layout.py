@@ -1,0 +1,38 @@
+"""Device layout prep (csrc/tsg_layout_dev.cu, the default of tsg_mesh_upload) against the host
+build (tsg_prep.cpp build_host_mesh, TSG_HOST_PREP=1): every array of the device mesh — slot
+order, ranks, compact CSR, fan records, fan16, device triangle order and corners, incident CSR,
+tier lists, tile meta / records / externals — identical (tsg_debug_layout_check), so the two
+preps give bit-identical smoothing; the parity suites run on the device prep."""
+import numpy as np
+import pytest
+
+from helpers import fan
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(ts):
+    xy, tri = ts.delaunay_arrays(6000, 70)
+    flip = np.random.default_rng(1).random(len(tri)) < 0.05
+    tri_f = tri.copy()
+    tri_f[flip] = tri_f[flip][:, [0, 2, 1]]
+    yield "grid", ts.grid_arrays(61, 47, 0.3, 2)
+    yield "delaunay", ts.delaunay_arrays(40000, 3)
+    yield "graded", ts.graded_arrays(60000, 3, 2e-3, 2048)
+    yield "flipped", (xy, tri_f)
+    yield "fan5000", fan(5000, (0.01, -0.02))
+    yield "tiny", (np.array([[0, 0], [1, 0], [0, 1], [1, 1]], float), np.array([[0, 1, 2], [1, 3, 2]], np.int32))
+
+
+@pytest.mark.parametrize("with_order", [True, False])
+def test_device_layout_equals_host(capi, gpu_ctx, ts, with_order):
+    for name, (xy, tri) in _cases(ts):
+        topo = ts.topology(len(xy), tri)
+        order = capi.hilbert_order(xy) if with_order else None
+        assert gpu_ctx.layout_check(xy, tri, topo, order) == "", name
+
+
+def test_device_layout_equals_host_at_cfg3_scale(capi, gpu_ctx, ts):
+    xy, tri = ts.graded_arrays(16_000_000, 1, 1e-3, 1024)
+    topo = gpu_ctx.topology(len(xy), tri)
+    assert gpu_ctx.layout_check(xy, tri, topo, capi.hilbert_order(xy)) == ""
