@@ -533,12 +533,14 @@ def main():
     t0 = time.time()
     topo = ctx.topology(nv, tri)  # adjacency + constraints on the device (tsg_topology)
     t_topo = time.time() - t0
-    order = capi.hilbert_order(xy) if cfg["reorder"] else None
+    order = ctx.hilbert_order(xy) if cfg["reorder"] else None  # on the device
     t_order = time.time() - t0 - t_topo
     dm = capi.DeviceMesh(ctx, xy, tri, topo, layout=cfg["layout"], precision=cfg["precision"], order=order)
     prep_s = time.time() - t0
     prep_split = {"topology_device_s": round(t_topo, 3), "locality_order_s": round(t_order, 3),
-                  "device_layout_upload_s": round(prep_s - t_topo - t_order, 3)}
+                  "device_layout_s": round(prep_s - t_topo - t_order, 3),
+                  "where": "all three on the device (tsg_topology, tsg_hilbert_order_device, tsg_mesh_upload "
+                           "with the device layout prep); host arrays in, host mesh generation excluded"}
     if cfg["form"] == "b":
         dm.formb_schedule(args.formb_schedule)
     deg = np.diff(topo["nbr_off"])

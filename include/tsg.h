@@ -259,6 +259,8 @@ tsg_status tsg_debug_trace(void* out, int64_t bytes);
 /* order_out[s] = original id for slot s: vertices sorted along a Hilbert curve over the
  * bounding box (ties by original id).  Pure host code, deterministic. */
 tsg_status tsg_hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
+/* The same order computed on the device (radix sort of the same keys). */
+tsg_status tsg_hilbert_order_device(tsg_context* ctx, int64_t nv, const double* xy, int64_t* order_out);
 
 /* ---- quality audit on the device (no tsg_mesh needed) ----
  * tsg_quality_tri_alpha: alpha_out[t] = triangle_alpha of triangle t (bit-exact), plus the

@@ -36,7 +36,7 @@ EXPORTS = (
     "tsg_dist_halo_unpack", "tsg_dist_finalize", "tsg_dist_status", "tsg_dist_end", "tsg_mesh_formb_schedule",
     "tsg_debug_trace", "tsg_mesh_side_schedule", "tsg_quality_tri_alpha", "tsg_quality_vertex_minima",
     "tsg_peer_local", "tsg_mesh_slots", "tsg_peer_setup", "tsg_peer_prepare", "tsg_peer_clear", "tsg_ipc_handle", "tsg_ipc_open",
-    "tsg_ipc_close", "tsg_topology", "tsg_debug_layout_check",
+    "tsg_ipc_close", "tsg_topology", "tsg_debug_layout_check", "tsg_hilbert_order_device",
 )
 IPC_HANDLE_BYTES = 64
 
@@ -126,6 +126,7 @@ def lib() -> C.CDLL:
             "tsg_ipc_close": (i32, [P, P]),
             "tsg_topology": (i32, [P, i64, i64, P, P, P, i64, P, P, P, C.POINTER(i64)]),
             "tsg_debug_layout_check": (i32, [P, C.POINTER(MeshDesc), C.c_char_p, i32]),
+            "tsg_hilbert_order_device": (i32, [P, i64, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -225,6 +226,13 @@ class Context:
         buf = C.create_string_buffer(64)
         check(lib().tsg_debug_layout_check(self.h, C.byref(d), buf, 64), "tsg_debug_layout_check")
         return buf.value.decode()
+
+    def hilbert_order(self, xy) -> np.ndarray:
+        """capi.hilbert_order computed on the device (tsg_hilbert_order_device): same order."""
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        out = np.empty(len(xy), dtype=np.int64)
+        check(lib().tsg_hilbert_order_device(self.h, len(xy), _ptr(xy), _ptr(out)), "tsg_hilbert_order_device")
+        return out
 
     def topology(self, nv: int, tri) -> dict:
         """Adjacency + constraints on the device (tsg_topology): same dict as

@@ -18,6 +18,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -71,6 +73,44 @@ __global__ void mark_isolated(const int64_t* __restrict__ cnt, int64_t nv, uint8
   for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nv;
        v += static_cast<int64_t>(gridDim.x) * blockDim.x)
     if (cnt[v] == 0) boundary[v] = 1;
+}
+
+// Hilbert index of (x, y) on a 2^16 x 2^16 lattice (the host hilbert_d, tsg_prep.cpp).
+__device__ uint32_t hilbert_d_dev(uint32_t x, uint32_t y) {
+  uint32_t d = 0;
+  for (uint32_t s = 1u << 15; s > 0; s >>= 1) {
+    const uint32_t rx = (x & s) ? 1u : 0u, ry = (y & s) ? 1u : 0u;
+    d += s * s * ((3u * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = 0xffffu - x;
+        y = 0xffffu - y;
+      }
+      const uint32_t t = x;
+      x = y;
+      y = t;
+    }
+  }
+  return d;
+}
+
+__global__ void hilbert_keys(const double2* __restrict__ xy, int64_t nv, double xmin, double ymin, double sx, double sy,
+                             unsigned long long* __restrict__ keys) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 p = xy[v];
+    const double fx = isfinite(p.x) ? __dmul_rn(__dsub_rn(p.x, xmin), sx) : 0.0;
+    const double fy = isfinite(p.y) ? __dmul_rn(__dsub_rn(p.y, ymin), sy) : 0.0;
+    const uint32_t qx = static_cast<uint32_t>(fx < 0.0 ? 0.0 : (fx > 65535.0 ? 65535.0 : fx));
+    const uint32_t qy = static_cast<uint32_t>(fy < 0.0 ? 0.0 : (fy > 65535.0 ? 65535.0 : fy));
+    keys[v] = (static_cast<unsigned long long>(hilbert_d_dev(qx, qy)) << 32) | static_cast<unsigned long long>(v);
+  }
+}
+
+__global__ void keys_to_order(const unsigned long long* __restrict__ keys, int64_t nv, int64_t* __restrict__ order) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    order[i] = static_cast<int64_t>(keys[i] & 0xffffffffULL);
 }
 
 int end_bit_for(int64_t nv) {
@@ -175,5 +215,56 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   TSG_CUDA(cudaMemcpyAsync(boundary, d_bnd, nv, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
   *n_nbr_out = h_runs;
+  return TSG_OK;
+}
+
+// tsg_hilbert_order on the device: same keys (bounding box and quantisation on the host, exact
+// fp64 without contraction), radix-sorted; identical order.
+extern "C" tsg_status tsg_hilbert_order_device(tsg_context* ctx, int64_t nv, const double* xy, int64_t* order_out) {
+  TSG_LOCK_CTX(ctx);
+  if (!ctx || nv <= 0 || nv >= (int64_t{1} << 32) || !xy || !order_out)
+    return tsg_abi::fail(TSG_ERR_INVALID, "tsg_hilbert_order_device: bad arguments");
+  double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+  for (int64_t v = 0; v < nv; ++v) {
+    xmin = std::min(xmin, xy[2 * v]);
+    xmax = std::max(xmax, xy[2 * v]);
+    ymin = std::min(ymin, xy[2 * v + 1]);
+    ymax = std::max(ymax, xy[2 * v + 1]);
+  }
+  const double sx = xmax > xmin ? 65535.0 / (xmax - xmin) : 0.0;
+  const double sy = ymax > ymin ? 65535.0 / (ymax - ymin) : 0.0;
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  struct Bufs {
+    cudaStream_t s;
+    std::vector<void*> p;
+    ~Bufs() {
+      for (void* q : p) cudaFreeAsync(q, s);
+    }
+    cudaError_t get(void** out, size_t bytes) {
+      cudaError_t e = cudaMallocAsync(out, bytes ? bytes : 8, s);
+      if (e == cudaSuccess) p.push_back(*out);
+      return e;
+    }
+  } B{s, {}};
+  double2* d_xy = nullptr;
+  unsigned long long *k1 = nullptr, *k2 = nullptr;
+  int64_t* d_order = nullptr;
+  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_xy), sizeof(double2) * nv));
+  TSG_CUDA(B.get(reinterpret_cast<void**>(&k1), 8 * nv));
+  TSG_CUDA(B.get(reinterpret_cast<void**>(&k2), 8 * nv));
+  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_order), 8 * nv));
+  TSG_CUDA(cudaMemcpyAsync(d_xy, xy, sizeof(double2) * nv, cudaMemcpyHostToDevice, s));
+  hilbert_keys<<<grid_of(nv), kThreads, 0, s>>>(d_xy, nv, xmin, ymin, sx, sy, k1);
+  TSG_LAUNCHED();
+  size_t bytes = 0;
+  TSG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, k1, k2, nv, 0, 64, s));
+  void* tmp = nullptr;
+  TSG_CUDA(B.get(&tmp, bytes));
+  TSG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, k1, k2, nv, 0, 64, s));
+  keys_to_order<<<grid_of(nv), kThreads, 0, s>>>(k2, nv, d_order);
+  TSG_LAUNCHED();
+  TSG_CUDA(cudaMemcpyAsync(order_out, d_order, 8 * nv, cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
   return TSG_OK;
 }

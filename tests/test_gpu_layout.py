@@ -36,3 +36,9 @@ def test_device_layout_equals_host_at_cfg3_scale(capi, gpu_ctx, ts):
     xy, tri = ts.graded_arrays(16_000_000, 1, 1e-3, 1024)
     topo = gpu_ctx.topology(len(xy), tri)
     assert gpu_ctx.layout_check(xy, tri, topo, capi.hilbert_order(xy)) == ""
+
+
+def test_device_hilbert_order_equals_host(capi, gpu_ctx, ts):
+    for xy in (ts.delaunay_arrays(100000, 4)[0], ts.grid_arrays(300, 200, 0.3, 1)[0],
+               np.vstack([ts.delaunay_arrays(5000, 1)[0], [[np.nan, 0.5]], [[2.0, 2.0]]])):
+        assert np.array_equal(gpu_ctx.hilbert_order(xy), capi.hilbert_order(xy))
