@@ -44,6 +44,8 @@ quality_report = _core.quality_report
 compute_all_qualities = _core.compute_all_qualities
 reduce_vertex_minima = _core.reduce_vertex_minima
 update_two_phase = _core.update_two_phase
+write_binary = _core.write_binary
+read_binary = _core.read_binary
 
 LIB_DIR = _HERE
 

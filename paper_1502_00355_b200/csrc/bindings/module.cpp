@@ -358,6 +358,27 @@ PYBIND11_MODULE(_trismooth, m) {
       py::arg("node"), py::arg("ele"), py::arg("layout") = "aos");
 
   m.def(
+      "write_binary",
+      [](const std::string& path, F64Array xy, I32Array tri) {
+        write_mesh_binary(path, xy.data(), xy.size() / 2, tri.data(), tri.size() / 3);
+      },
+      py::arg("path"), py::arg("xy"), py::arg("tri"),
+      "Binary mesh file (TSGMESH1: sizes, float64 xy, int32 corners) — the fast path beside .node/.ele.");
+  m.def(
+      "read_binary",
+      [](const std::string& path) {
+        BinaryMesh b;
+        {
+          py::gil_scoped_release nogil;
+          b = read_mesh_binary(path);
+        }
+        const int64_t nv = b.nv, nt = b.nt;
+        return py::make_tuple(to_numpy(std::move(b.xy), {static_cast<py::ssize_t>(nv), 2}),
+                              to_numpy(std::move(b.tri), {static_cast<py::ssize_t>(nt), 3}));
+      },
+      py::arg("path"));
+
+  m.def(
       "write_mesh", [](const Mesh& mesh, const std::string& prefix) { write_mesh_files(mesh, prefix); },
       py::arg("mesh"), py::arg("prefix"), "Writes <prefix>.node and <prefix>.ele.");
 

@@ -234,3 +234,25 @@ def test_spatial_generator_is_delaunay_at_4m():
     assert (area > 0).all()
     bad, checked = _local_delaunay_violations(xy, tri, 200_000, np.random.default_rng(1))
     assert checked > 250_000 and bad == 0
+
+
+def test_binary_mesh_round_trip_and_validation(tmp_path):
+    import paper_1502_00355_b200 as core
+
+    xy, tri = ts.delaunay_arrays(20000, 6)
+    p = str(tmp_path / "m.tsgmesh")
+    core.write_binary(p, xy, tri)
+    xy2, tri2 = core.read_binary(p)
+    assert np.array_equal(xy.view(np.uint64), xy2.view(np.uint64)) and np.array_equal(tri, tri2)
+    raw = bytearray(open(p, "rb").read())
+    open(str(tmp_path / "short"), "wb").write(raw[:-4])
+    with pytest.raises(RuntimeError, match="do not match"):
+        core.read_binary(str(tmp_path / "short"))
+    bad = tri.copy()
+    bad[5, 1] = len(xy)
+    core.write_binary(str(tmp_path / "bad"), xy, bad)
+    with pytest.raises(RuntimeError, match="out of range"):
+        core.read_binary(str(tmp_path / "bad"))
+    open(str(tmp_path / "junk"), "wb").write(b"NOTAMESH" + bytes(40))
+    with pytest.raises(RuntimeError, match="not a TSGMESH1"):
+        core.read_binary(str(tmp_path / "junk"))
