@@ -6,8 +6,8 @@ set -e
 name=$1; shift
 mkdir -p build/var_$name
 NV="nvcc -O3 -std=c++20 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false -Xcompiler -fPIC,-O3 -Iinclude -Ipaper_1502_00355_b200/csrc --expt-relaxed-constexpr $*"
-$NV -c paper_1502_00355_b200/csrc/tsg_engine.cu -o build/var_$name/tsg_engine.o
-$NV -c paper_1502_00355_b200/csrc/tsg_quality.cu -o build/var_$name/tsg_quality.o
-$NV -x cu -c paper_1502_00355_b200/csrc/tsg_topo.cu -o build/var_$name/tsg_topo.o
+for f in paper_1502_00355_b200/csrc/*.cu; do
+  $NV -c $f -o build/var_$name/$(basename $f .cu).o
+done
 g++ -O3 -std=c++20 -fPIC -Iinclude -Ipaper_1502_00355_b200/csrc $* -c paper_1502_00355_b200/csrc/tsg_prep.cpp -o build/var_$name/tsg_prep.o
-nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -o paper_1502_00355_b200/libtsg_$name.so build/var_$name/*.o -lpthread
+nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -Xlinker --no-undefined -o paper_1502_00355_b200/libtsg_$name.so build/var_$name/*.o -lpthread
