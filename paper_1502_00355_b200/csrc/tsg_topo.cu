@@ -7,16 +7,20 @@
 // outputs come from radix sorts on the device:
 //   * incident rows: the 3 nt (corner vertex, triangle) pairs sorted by vertex — a stable sort,
 //     and the pairs are generated in triangle order, so every row is ascending (Adjacency::incident);
-//   * unique neighbour rows: the 6 nt directed corner pairs (v, u) as 64-bit keys v << 32 | u,
-//     sorted, run-length encoded: the runs are the rows' entries in ascending u, the run lengths
-//     their multiplicities (Adjacency::unique + multiplicity);
-//   * boundary: isolated (no run) or some multiplicity != 2.
-// Offsets are int64 and no raw list is materialised, so cfg5-sized meshes (nt = 512M) build.
+//   * unique neighbour rows, per vertex from its incident rows: the two other corners of every
+//     incident triangle (the reference's raw row, in some order), sorted and run-length counted —
+//     in registers / local memory for rows of up to kLocalCand candidates (thread per vertex),
+//     through a segmented sort for the few longer rows (hubs) — giving the rows in ascending id
+//     and the multiplicities (Adjacency::unique + multiplicity);
+//   * boundary: isolated or some multiplicity != 2.
+// Offsets are int64, no raw list is materialised and no device-wide sort exceeds 3 nt items,
+// so cfg5-sized meshes (nt = 512M: 1.5e9 corners) build.
 // Results equal gpu::build_topology / find_neighbors bit for bit (tests/test_gpu_topology.py).
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <cub/device/device_scan.cuh>
 #include <algorithm>
 #include <cmath>
@@ -35,44 +39,129 @@ unsigned grid_of(int64_t n) {
   return static_cast<unsigned>(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
 }
 
-__global__ void corner_pairs(const int32_t* __restrict__ tri, int64_t nt, uint32_t* __restrict__ cv,
-                             int32_t* __restrict__ ct, unsigned long long* __restrict__ pairs,
-                             int64_t* __restrict__ inc_cnt) {
+__global__ void corner_keys(const int32_t* __restrict__ tri, int64_t nt, uint32_t* __restrict__ cv,
+                            int32_t* __restrict__ ct, unsigned long long* __restrict__ inc_cnt) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t a = static_cast<uint32_t>(tri[3 * t]), b = static_cast<uint32_t>(tri[3 * t + 1]),
-                   c = static_cast<uint32_t>(tri[3 * t + 2]);
-    const uint32_t v[3] = {a, b, c};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      cv[3 * t + k] = v[k];
+      const uint32_t v = static_cast<uint32_t>(tri[3 * t + k]);
+      cv[3 * t + k] = v;
       ct[3 * t + k] = static_cast<int32_t>(t);
-      atomicAdd(reinterpret_cast<unsigned long long*>(inc_cnt + v[k]), 1ULL);
-      const unsigned long long hi = static_cast<unsigned long long>(v[k]) << 32;
-      pairs[6 * t + 2 * k] = hi | v[(k + 1) % 3];
-      pairs[6 * t + 2 * k + 1] = hi | v[(k + 2) % 3];
+      atomicAdd(inc_cnt + v, 1ULL);
     }
   }
 }
 
-__global__ void row_counts(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ mult,
-                           const int64_t* __restrict__ nruns, int32_t* __restrict__ nbr, int64_t* __restrict__ cnt,
-                           uint8_t* __restrict__ boundary) {
-  const int64_t n = *nruns;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long k = keys[i];
-    const uint32_t v = static_cast<uint32_t>(k >> 32);
-    nbr[i] = static_cast<int32_t>(k & 0xffffffffULL);
-    atomicAdd(reinterpret_cast<unsigned long long*>(cnt + v), 1ULL);
-    if (mult[i] != 2) boundary[v] = 1;
+constexpr int kLocalCand = 64;  // candidates sorted in a thread's local array (valence <= 32)
+
+// The two other corners of each incident triangle of v.
+__device__ __forceinline__ int gather_candidates(const int32_t* __restrict__ tri, const int32_t* __restrict__ inc,
+                                                 int64_t b, int64_t e, int32_t v, int32_t* c) {
+  int n = 0;
+  for (int64_t i = b; i < e; ++i) {
+    const int32_t* tv = tri + 3 * static_cast<int64_t>(inc[i]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (tv[k] != v) c[n++] = tv[k];
+  }
+  return n;
+}
+
+// Sorted candidates -> unique values (optional output), count, and "some multiplicity != 2".
+__device__ __forceinline__ int unique_runs(const int32_t* c, int n, int32_t* out, bool& odd) {
+  int u = 0;
+  for (int i = 0; i < n;) {
+    int j = i + 1;
+    while (j < n && c[j] == c[i]) ++j;
+    if (out) out[u] = c[i];
+    odd = odd || (j - i) != 2;
+    ++u;
+    i = j;
+  }
+  return u;
+}
+
+// Thread per vertex: rows of up to kLocalCand candidates; longer rows are flagged for the
+// segmented path.  Pass 0 counts (and classifies), pass 1 writes the values.
+__global__ void local_rows(const int32_t* __restrict__ tri, const unsigned long long* __restrict__ inc_off,
+                           const int32_t* __restrict__ inc, int64_t nv, int pass, unsigned long long* __restrict__ cnt,
+                           uint8_t* __restrict__ boundary, uint8_t* __restrict__ big,
+                           const unsigned long long* __restrict__ off, int32_t* __restrict__ nbr) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = static_cast<int64_t>(inc_off[v]), e = static_cast<int64_t>(inc_off[v + 1]);
+    if (2 * (e - b) > kLocalCand) {
+      if (pass == 0) big[v] = 1;
+      continue;
+    }
+    int32_t c[kLocalCand];
+    const int n = gather_candidates(tri, inc, b, e, static_cast<int32_t>(v), c);
+    for (int i = 1; i < n; ++i) {  // insertion sort (about a dozen entries)
+      const int32_t x = c[i];
+      int j = i - 1;
+      while (j >= 0 && c[j] > x) {
+        c[j + 1] = c[j];
+        --j;
+      }
+      c[j + 1] = x;
+    }
+    bool odd = false;
+    if (pass == 0) {
+      big[v] = 0;
+      cnt[v] = static_cast<unsigned long long>(unique_runs(c, n, nullptr, odd));
+      boundary[v] = (n == 0 || odd) ? 1 : 0;
+    } else {
+      unique_runs(c, n, nbr + off[v], odd);
+    }
   }
 }
 
-__global__ void mark_isolated(const int64_t* __restrict__ cnt, int64_t nv, uint8_t* __restrict__ boundary) {
-  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nv;
-       v += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    if (cnt[v] == 0) boundary[v] = 1;
+// Long rows (hubs): candidates into a buffer segmented by big vertex, sorted by CUB, then counted
+// / written by a thread per big vertex.
+__global__ void big_candidates(const int32_t* __restrict__ tri, const unsigned long long* __restrict__ inc_off,
+                               const int32_t* __restrict__ inc, const int32_t* __restrict__ bigv, int64_t nbig,
+                               const unsigned long long* __restrict__ cand_off, int32_t* __restrict__ cand) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nbig;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = bigv[i];
+    gather_candidates(tri, inc, static_cast<int64_t>(inc_off[v]), static_cast<int64_t>(inc_off[v + 1]), v,
+                      cand + cand_off[i]);
+  }
+}
+
+__global__ void big_rows(const int32_t* __restrict__ cand, const unsigned long long* __restrict__ cand_off,
+                         const int32_t* __restrict__ bigv, int64_t nbig, int pass, unsigned long long* __restrict__ cnt,
+                         uint8_t* __restrict__ boundary, const unsigned long long* __restrict__ off,
+                         int32_t* __restrict__ nbr) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nbig;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = bigv[i];
+    const int32_t* c = cand + cand_off[i];
+    const int n = static_cast<int>(cand_off[i + 1] - cand_off[i]);
+    bool odd = false;
+    if (pass == 0) {
+      cnt[v] = static_cast<unsigned long long>(unique_runs(c, n, nullptr, odd));
+      boundary[v] = (n == 0 || odd) ? 1 : 0;
+    } else {
+      unique_runs(c, n, nbr + off[v], odd);
+    }
+  }
+}
+
+__global__ void big_cand_counts(const unsigned long long* __restrict__ inc_off, const int32_t* __restrict__ bigv,
+                                int64_t nbig, unsigned long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nbig;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = bigv[i];
+    out[i] = 2 * (inc_off[v + 1] - inc_off[v]);
+  }
+}
+
+__global__ void iota32(int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(i);
 }
 
 // Hilbert index of (x, y) on a 2^16 x 2^16 lattice (the host hilbert_d, tsg_prep.cpp).
@@ -113,6 +202,25 @@ __global__ void keys_to_order(const unsigned long long* __restrict__ keys, int64
     order[i] = static_cast<int64_t>(keys[i] & 0xffffffffULL);
 }
 
+// Stream-ordered device allocations released on every return path.
+struct DevBufs {
+  cudaStream_t s;
+  std::vector<void*> p;
+  ~DevBufs() {
+    for (void* q : p) cudaFreeAsync(q, s);
+  }
+  template <class T>
+  cudaError_t get(T** out, int64_t n) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, static_cast<size_t>(n > 0 ? n : 1) * sizeof(T), s);
+    if (e == cudaSuccess) {
+      p.push_back(q);
+      *out = static_cast<T*>(q);
+    }
+    return e;
+  }
+};
+
 int end_bit_for(int64_t nv) {
   int b = 1;
   while (b < 32 && (int64_t{1} << b) < nv) ++b;
@@ -125,96 +233,112 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
                                    int32_t* nbr, int64_t nbr_cap, int64_t* inc_off, int32_t* inc, uint8_t* boundary,
                                    int64_t* n_nbr_out) {
   TSG_LOCK_CTX(ctx);
-  if (!ctx || nv <= 0 || nt < 0 || nv >= (int64_t{1} << 31) || (nt > 0 && !tri) || !nbr_off || !inc_off ||
-      !boundary || !n_nbr_out || (nt > 0 && (!inc || !nbr)))
+  if (!ctx || nv <= 0 || nt < 0 || nv >= (int64_t{1} << 31) || 3 * nt >= (int64_t{1} << 31) || (nt > 0 && !tri) ||
+      !nbr_off || !inc_off || !boundary || !n_nbr_out || (nt > 0 && (!inc || !nbr)))
     return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: bad arguments");
   for (int64_t i = 0; i < 3 * nt; ++i)
     if (tri[i] < 0 || tri[i] >= nv) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: corner index out of range");
   TSG_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
-  const int64_t m3 = 3 * nt, m6 = 6 * nt;
+  const int64_t m3 = 3 * nt;
   const int vbits = end_bit_for(nv);
-  // device buffers (stream-ordered; freed on every path by the guard)
-  struct Bufs {
-    cudaStream_t s;
-    std::vector<void*> p;
-    ~Bufs() {
-      for (void* q : p) cudaFreeAsync(q, s);
-    }
-    cudaError_t get(void** out, size_t bytes) {
-      cudaError_t e = cudaMallocAsync(out, bytes ? bytes : 8, s);
-      if (e == cudaSuccess) p.push_back(*out);
-      return e;
-    }
-  } B{s, {}};
-  int32_t *d_tri = nullptr, *d_ct = nullptr, *d_ct2 = nullptr, *d_mult = nullptr, *d_nbr = nullptr;
-  uint32_t *d_cv = nullptr, *d_cv2 = nullptr;
-  unsigned long long *d_pairs = nullptr, *d_pairs2 = nullptr, *d_ukeys = nullptr;
-  int64_t *d_inc_cnt = nullptr, *d_inc_off = nullptr, *d_cnt = nullptr, *d_off = nullptr, *d_nruns = nullptr;
-  uint8_t* d_bnd = nullptr;
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_tri), sizeof(int32_t) * m3));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_cv), sizeof(uint32_t) * m3));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_cv2), sizeof(uint32_t) * m3));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_ct), sizeof(int32_t) * m3));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_ct2), sizeof(int32_t) * m3));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_pairs), sizeof(unsigned long long) * m6));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_pairs2), sizeof(unsigned long long) * m6));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_inc_cnt), sizeof(int64_t) * (nv + 1)));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_inc_off), sizeof(int64_t) * (nv + 1)));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_cnt), sizeof(int64_t) * (nv + 1)));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_off), sizeof(int64_t) * (nv + 1)));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_nruns), sizeof(int64_t)));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_bnd), nv));
-  TSG_CUDA(cudaMemsetAsync(d_inc_cnt, 0, sizeof(int64_t) * (nv + 1), s));
-  TSG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (nv + 1), s));
-  TSG_CUDA(cudaMemsetAsync(d_bnd, 0, nv, s));
-  if (nt) TSG_CUDA(cudaMemcpyAsync(d_tri, tri, sizeof(int32_t) * m3, cudaMemcpyHostToDevice, s));
-  corner_pairs<<<grid_of(nt), kThreads, 0, s>>>(d_tri, nt, d_cv, d_ct, d_pairs, d_inc_cnt);
+  DevBufs B{s, {}};
+  auto cub_call = [&](auto&& f) -> cudaError_t {
+    size_t bytes = 0;
+    cudaError_t e = f(nullptr, bytes);
+    if (e != cudaSuccess) return e;
+    char* t = nullptr;
+    if ((e = B.get(&t, static_cast<int64_t>(bytes))) != cudaSuccess) return e;
+    return f(t, bytes);
+  };
+  int32_t *d_tri, *d_ct, *d_inc;
+  uint32_t *d_cv, *d_cv2;
+  unsigned long long *d_inc_cnt, *d_inc_off, *d_cnt, *d_off;
+  uint8_t *d_bnd, *d_big;
+  TSG_CUDA(B.get(&d_tri, m3));
+  TSG_CUDA(B.get(&d_cv, m3));
+  TSG_CUDA(B.get(&d_cv2, m3));
+  TSG_CUDA(B.get(&d_ct, m3));
+  TSG_CUDA(B.get(&d_inc, m3));
+  TSG_CUDA(B.get(&d_inc_cnt, nv + 1));
+  TSG_CUDA(B.get(&d_inc_off, nv + 1));
+  TSG_CUDA(B.get(&d_cnt, nv + 1));
+  TSG_CUDA(B.get(&d_off, nv + 1));
+  TSG_CUDA(B.get(&d_bnd, nv));
+  TSG_CUDA(B.get(&d_big, nv));
+  TSG_CUDA(cudaMemsetAsync(d_inc_cnt, 0, 8 * (nv + 1), s));
+  TSG_CUDA(cudaMemsetAsync(d_cnt, 0, 8 * (nv + 1), s));
+  if (nt) TSG_CUDA(cudaMemcpyAsync(d_tri, tri, 4 * m3, cudaMemcpyHostToDevice, s));
+  corner_keys<<<grid_of(nt), kThreads, 0, s>>>(d_tri, nt, d_cv, d_ct, d_inc_cnt);
   TSG_LAUNCHED();
-
-  // incident rows: stable sort of (vertex, triangle) by vertex
-  size_t tmp_bytes = 0, need = 0;
-  TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, d_cv, d_cv2, d_ct, d_ct2, m3, 0, vbits, s));
-  tmp_bytes = need;
-  TSG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, d_pairs, d_pairs2, m6, 0, 32 + vbits, s));
-  tmp_bytes = std::max(tmp_bytes, need);
-  TSG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, need, d_pairs2, d_pairs, d_ct, d_nruns, m6, s));
-  tmp_bytes = std::max(tmp_bytes, need);
-  TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, d_inc_cnt, d_inc_off, nv + 1, s));
-  tmp_bytes = std::max(tmp_bytes, need);
-  void* d_tmp = nullptr;
-  TSG_CUDA(B.get(&d_tmp, tmp_bytes));
-  need = tmp_bytes;
-  TSG_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, need, d_cv, d_cv2, d_ct, d_ct2, m3, 0, vbits, s));
-  need = tmp_bytes;
-  TSG_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, need, d_inc_cnt, d_inc_off, nv + 1, s));
-
-  // unique neighbour rows with multiplicities: sort the directed pairs, run-length encode
-  need = tmp_bytes;
-  TSG_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, need, d_pairs, d_pairs2, m6, 0, 32 + vbits, s));
-  d_ukeys = d_pairs;  // the runs overwrite the (consumed) unsorted keys
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_mult), sizeof(int32_t) * m6));
-  need = tmp_bytes;
-  TSG_CUDA(cub::DeviceRunLengthEncode::Encode(d_tmp, need, d_pairs2, d_ukeys, d_mult, d_nruns, m6, s));
-  int64_t h_runs = 0;
-  TSG_CUDA(cudaMemcpyAsync(&h_runs, d_nruns, sizeof h_runs, cudaMemcpyDeviceToHost, s));
+  // incident rows: stable sort of (vertex, triangle) by vertex (pairs generated in triangle order)
+  TSG_CUDA(cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, d_cv, d_cv2, d_ct, d_inc, static_cast<int>(m3), 0, vbits, s);
+  }));
+  TSG_CUDA(cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, d_inc_cnt, d_inc_off, nv + 1, s);
+  }));
+  // unique rows: pass 0 counts and classifies
+  local_rows<<<grid_of(nv), kThreads, 0, s>>>(d_tri, d_inc_off, d_inc, nv, 0, d_cnt, d_bnd, d_big, nullptr, nullptr);
+  TSG_LAUNCHED();
+  int32_t *d_iota, *d_bigv;
+  int64_t* d_nbig;
+  TSG_CUDA(B.get(&d_iota, nv));
+  TSG_CUDA(B.get(&d_bigv, nv));
+  TSG_CUDA(B.get(&d_nbig, 1));
+  iota32<<<grid_of(nv), kThreads, 0, s>>>(nv, d_iota);
+  TSG_LAUNCHED();
+  TSG_CUDA(cub_call([&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, d_iota, d_big, d_bigv, d_nbig, nv, s);
+  }));
+  int64_t nbig = 0;
+  TSG_CUDA(cudaMemcpyAsync(&nbig, d_nbig, 8, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
-  if (h_runs > nbr_cap) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: nbr capacity too small");
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_nbr), sizeof(int32_t) * h_runs));
-  row_counts<<<grid_of(h_runs), kThreads, 0, s>>>(d_ukeys, d_mult, d_nruns, d_nbr, d_cnt, d_bnd);
+  unsigned long long *d_coff = nullptr, *d_ccnt = nullptr;
+  int32_t *d_cand = nullptr, *d_cand2 = nullptr;
+  if (nbig > 0) {
+    TSG_CUDA(B.get(&d_ccnt, nbig + 1));
+    TSG_CUDA(B.get(&d_coff, nbig + 1));
+    TSG_CUDA(cudaMemsetAsync(d_ccnt + nbig, 0, 8, s));
+    big_cand_counts<<<grid_of(nbig), kThreads, 0, s>>>(d_inc_off, d_bigv, nbig, d_ccnt);
+    TSG_LAUNCHED();
+    TSG_CUDA(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, d_ccnt, d_coff, nbig + 1, s); }));
+    unsigned long long ncand = 0;
+    TSG_CUDA(cudaMemcpyAsync(&ncand, d_coff + nbig, 8, cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    if (ncand >= (1ULL << 31)) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: hub rows exceed 2^31 entries");
+    TSG_CUDA(B.get(&d_cand, static_cast<int64_t>(ncand)));
+    TSG_CUDA(B.get(&d_cand2, static_cast<int64_t>(ncand)));
+    big_candidates<<<grid_of(nbig), kThreads, 0, s>>>(d_tri, d_inc_off, d_inc, d_bigv, nbig, d_coff, d_cand);
+    TSG_LAUNCHED();
+    TSG_CUDA(cub_call([&](void* t, size_t& b) {
+      return cub::DeviceSegmentedSort::SortKeys(t, b, d_cand, d_cand2, static_cast<int>(ncand), static_cast<int>(nbig),
+                                                d_coff, d_coff + 1, s);
+    }));
+    big_rows<<<grid_of(nbig), kThreads, 0, s>>>(d_cand2, d_coff, d_bigv, nbig, 0, d_cnt, d_bnd, nullptr, nullptr);
+    TSG_LAUNCHED();
+  }
+  TSG_CUDA(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, d_cnt, d_off, nv + 1, s); }));
+  unsigned long long h_total = 0;
+  TSG_CUDA(cudaMemcpyAsync(&h_total, d_off + nv, 8, cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaStreamSynchronize(s));
+  if (static_cast<int64_t>(h_total) > nbr_cap) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: nbr capacity too small");
+  int32_t* d_nbr;
+  TSG_CUDA(B.get(&d_nbr, static_cast<int64_t>(h_total)));
+  local_rows<<<grid_of(nv), kThreads, 0, s>>>(d_tri, d_inc_off, d_inc, nv, 1, d_cnt, d_bnd, d_big, d_off, d_nbr);
   TSG_LAUNCHED();
-  mark_isolated<<<grid_of(nv), kThreads, 0, s>>>(d_cnt, nv, d_bnd);
-  TSG_LAUNCHED();
-  need = tmp_bytes;
-  TSG_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, need, d_cnt, d_off, nv + 1, s));
-
-  TSG_CUDA(cudaMemcpyAsync(nbr_off, d_off, sizeof(int64_t) * (nv + 1), cudaMemcpyDeviceToHost, s));
-  TSG_CUDA(cudaMemcpyAsync(inc_off, d_inc_off, sizeof(int64_t) * (nv + 1), cudaMemcpyDeviceToHost, s));
-  if (h_runs) TSG_CUDA(cudaMemcpyAsync(nbr, d_nbr, sizeof(int32_t) * h_runs, cudaMemcpyDeviceToHost, s));
-  if (m3) TSG_CUDA(cudaMemcpyAsync(inc, d_ct2, sizeof(int32_t) * m3, cudaMemcpyDeviceToHost, s));
+  if (nbig > 0) {
+    big_rows<<<grid_of(nbig), kThreads, 0, s>>>(d_cand2, d_coff, d_bigv, nbig, 1, d_cnt, d_bnd, d_off, d_nbr);
+    TSG_LAUNCHED();
+  }
+  static_assert(sizeof(unsigned long long) == sizeof(int64_t), "offset width");
+  TSG_CUDA(cudaMemcpyAsync(nbr_off, d_off, 8 * (nv + 1), cudaMemcpyDeviceToHost, s));
+  TSG_CUDA(cudaMemcpyAsync(inc_off, d_inc_off, 8 * (nv + 1), cudaMemcpyDeviceToHost, s));
+  if (h_total) TSG_CUDA(cudaMemcpyAsync(nbr, d_nbr, 4 * h_total, cudaMemcpyDeviceToHost, s));
+  if (m3) TSG_CUDA(cudaMemcpyAsync(inc, d_inc, 4 * m3, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaMemcpyAsync(boundary, d_bnd, nv, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
-  *n_nbr_out = h_runs;
+  *n_nbr_out = static_cast<int64_t>(h_total);
   return TSG_OK;
 }
 
@@ -235,32 +359,21 @@ extern "C" tsg_status tsg_hilbert_order_device(tsg_context* ctx, int64_t nv, con
   const double sy = ymax > ymin ? 65535.0 / (ymax - ymin) : 0.0;
   TSG_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
-  struct Bufs {
-    cudaStream_t s;
-    std::vector<void*> p;
-    ~Bufs() {
-      for (void* q : p) cudaFreeAsync(q, s);
-    }
-    cudaError_t get(void** out, size_t bytes) {
-      cudaError_t e = cudaMallocAsync(out, bytes ? bytes : 8, s);
-      if (e == cudaSuccess) p.push_back(*out);
-      return e;
-    }
-  } B{s, {}};
+  DevBufs B{s, {}};
   double2* d_xy = nullptr;
   unsigned long long *k1 = nullptr, *k2 = nullptr;
   int64_t* d_order = nullptr;
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_xy), sizeof(double2) * nv));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&k1), 8 * nv));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&k2), 8 * nv));
-  TSG_CUDA(B.get(reinterpret_cast<void**>(&d_order), 8 * nv));
+  TSG_CUDA(B.get(&d_xy, nv));
+  TSG_CUDA(B.get(&k1, nv));
+  TSG_CUDA(B.get(&k2, nv));
+  TSG_CUDA(B.get(&d_order, nv));
   TSG_CUDA(cudaMemcpyAsync(d_xy, xy, sizeof(double2) * nv, cudaMemcpyHostToDevice, s));
   hilbert_keys<<<grid_of(nv), kThreads, 0, s>>>(d_xy, nv, xmin, ymin, sx, sy, k1);
   TSG_LAUNCHED();
   size_t bytes = 0;
   TSG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, k1, k2, nv, 0, 64, s));
-  void* tmp = nullptr;
-  TSG_CUDA(B.get(&tmp, bytes));
+  char* tmp = nullptr;
+  TSG_CUDA(B.get(&tmp, static_cast<int64_t>(bytes)));
   TSG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, k1, k2, nv, 0, 64, s));
   keys_to_order<<<grid_of(nv), kThreads, 0, s>>>(k2, nv, d_order);
   TSG_LAUNCHED();
