@@ -957,21 +957,12 @@ struct Engine {
     tsg::flow_reset<<<grid_for(n, 256), 256, 0, s>>>(m->d_flow_rec, n, m->d_flow_done);
     TSG_LAUNCHED();
     int per_sm = 0, sms = 0;
-    // TSG_FLOW_WARP=0 selects the thread-per-vertex variant (A/B)
-    static const bool warp = [] {
-      const char* e = std::getenv("TSG_FLOW_WARP");
-      return !e || std::atoi(e) != 0;
-    }();
     constexpr size_t smem = tsg::flow_smem_bytes<R>();
-    auto kern = warp ? tsg::formb_flow_warp<R, kSoA> : tsg::formb_flow<R, kSoA>;
-    const int block = warp ? tsg::kFlowWarpBlock : tsg::kFlowBlock;
-    const size_t dyn = warp ? 0 : smem;
-    if (!warp) TSG_CUDA(raise_smem_limit(tsg::formb_flow<R, kSoA>, static_cast<int>(smem)));
-    TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, dyn));
+    TSG_CUDA(raise_smem_limit(tsg::formb_flow<R, kSoA>, static_cast<int>(smem)));
+    TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsg::formb_flow<R, kSoA>, tsg::kFlowBlock, smem));
     TSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->ctx->device));
     const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * sms;
-    const int64_t per_block = warp ? block / 32 : block;  // entries a block works on at a time
-    const int64_t want = (n + per_block - 1) / per_block;
+    const int64_t want = (n + tsg::kFlowBlock - 1) / tsg::kFlowBlock;
     const unsigned grid = static_cast<unsigned>(std::min(cap, want));
     tsg::FlowArgs<R> f{};
     f.buf0 = static_cast<R*>(m->buf[0]);
@@ -989,7 +980,8 @@ struct Engine {
     f.slot_md = m->d_smd;
     f.maxabs = m->d_maxabs;
     void* args[] = {&f};
-    TSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(block), args, dyn, s));
+    TSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tsg::formb_flow<R, kSoA>), dim3(grid),
+                                         dim3(tsg::kFlowBlock), args, smem, s));
     *kernels += 2;
     return TSG_OK;
   }

@@ -274,159 +274,6 @@ __global__ void __launch_bounds__(kFlowBlock) formb_flow(FlowArgs<R> f) {
   }
 }
 
-// Warp-cooperative variant (one vertex per warp at a time; lane j = row entry / fan triangle j):
-// the ring's counters are polled in parallel, the gather is one batch across the lanes, the
-// two minima are shuffle reductions — a dependent step of the dataflow costs about one L2 round
-// trip for the counters, one for the coordinates and the release, instead of a lane's serial
-// chain.  Rows beyond a record (valence > kChunkRecMaxDeg) go through flow_decide_global on
-// lane 0.  Same schedule (entries dealt to warps in level order), same arithmetic.
-constexpr int kFlowWarpBlock = 128;
-
-template <typename R, bool kSoA>
-__global__ void __launch_bounds__(kFlowWarpBlock) formb_flow_warp(FlowArgs<R> f) {
-  using O = Arith<R>;
-  using R2 = typename O::R2;
-  constexpr bool kExact = sizeof(R) == 8;
-  __shared__ R2 ring_s[kFlowWarpBlock / 32][2][32];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  R2* sp = ring_s[wl][0];
-  R2* sv = ring_s[wl][1];
-  const int64_t W = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const int64_t first = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wl;
-  const bool xonly = exact_only(f.maxabs);
-  const unsigned stat_slot = static_cast<unsigned>(first) & (kStatSlots - 1);
-  int64_t e = first;
-  int q = e < f.n ? 0 : f.np;
-  int accepted = 0;
-  double disp = 0.0;
-  while (q < f.np) {
-    const uint32_t* r = f.rec + e * kChunkRecWords;
-    const int64_t s = __ldg(r);
-    const int deg = static_cast<int>(__ldg(r + 1));
-    const bool small = deg <= kChunkRecMaxDeg;
-    uint32_t u = 0, fr = 0;
-    if (small && lane < deg) {
-      u = __ldg(r + 2 + lane);
-      fr = __ldg(r + 2 + kChunkRecMaxDeg + lane);
-    }
-    // dependencies (small rows: one counter per lane; larger rows: lanes stride the row)
-    bool ok = true;
-    if (small) {
-      if (lane < deg) {
-        const uint32_t need = (u & kFreshBit) ? static_cast<uint32_t>(q + 1) : static_cast<uint32_t>(q);
-        ok = ld_relaxed_gpu(f.done + (u & ~kFreshBit)) >= need;
-      }
-    } else {
-      const uint32_t* nb = f.nbr + __ldg(f.off + s);
-      for (int j = lane; j < deg && ok; j += 32) {
-        const uint32_t x = __ldg(nb + j);
-        const uint32_t need = (x & kFreshBit) ? static_cast<uint32_t>(q + 1) : static_cast<uint32_t>(q);
-        ok = ld_relaxed_gpu(f.done + (x & ~kFreshBit)) >= need;
-      }
-    }
-    if (!__all_sync(0xffffffffu, ok)) continue;
-    fence_acq_rel_gpu();
-    const int gp = f.p0 + q;
-    const CoordsCG<R, kSoA> P{(gp & 1) ? f.buf1 : f.buf0, f.nv}, N{(gp & 1) ? f.buf0 : f.buf1, f.nv};
-    const R2 pv = P.load(s);
-    R2 cand;
-    bool acc;
-    if (small) {
-      if (lane < deg) {
-        const R2 c = P.load(u & ~kFreshBit);
-        sp[lane] = c;
-        sv[lane] = (u & kFreshBit) ? N.load(u & ~kFreshBit) : c;
-      }
-      __syncwarp();
-      R sx = R(0), sy = R(0);
-      for (int j = 0; j < deg; ++j) {  // neighbor_mean: the ordered chain (broadcast reads)
-        const R2 c = sv[j];
-        sx = O::add(sx, c.x);
-        sy = O::add(sy, c.y);
-      }
-      const R inv = inv_deg<R>(deg);
-      cand = O::make(O::mul(sx, inv), O::mul(sy, inv));
-      R tp = R(INFINITY), tc = R(INFINITY), nacc = R(0);
-      if (lane < deg) {
-        const int ia = static_cast<int>(fan_i1(fr)), ib = static_cast<int>(fan_i2(fr));
-        tp = rot_fast<R>(sp[ia], sp[ib], pv);
-        tc = rot_fast<R>(sv[ia], sv[ib], cand);
-        if constexpr (!kExact) {
-          tp = isfinite(tp) ? tp : R(0);
-          tc = isfinite(tc) ? tc : R(0);
-        }
-        nacc = tp * tc;
-      }
-      const bool bad = xonly || __any_sync(0xffffffffu, !(fabs(nacc) < R(1e30)));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        tp = min_ref(tp, __shfl_xor_sync(0xffffffffu, tp, o));
-        tc = min_ref(tc, __shfl_xor_sync(0xffffffffu, tc, o));
-      }
-      if constexpr (!kExact) {
-        acc = tc > tp;
-      } else if (!bad && tc > tp + R(kGuardCycle)) {
-        acc = true;
-      } else if (!bad && tc < tp - R(kGuardCycle)) {
-        acc = false;
-      } else {
-        R te = R(INFINITY), he = R(INFINITY);
-        if (lane < deg) {
-          const int ia = static_cast<int>(fan_i1(fr)), ib = static_cast<int>(fan_i2(fr));
-          const int k = fan_k(fr);
-          {
-            const R2 qa = sp[ia], qb = sp[ib];
-            const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
-            te = alpha_at<R>(k, pv.x, pv.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx), O::mul(daby, daby));
-          }
-          {
-            const R2 qa = sv[ia], qb = sv[ib];
-            const R dabx = O::sub(qb.x, qa.x), daby = O::sub(qb.y, qa.y);
-            he = alpha_at<R>(k, cand.x, cand.y, qa.x, qa.y, qb.x, qb.y, dabx, daby, O::mul(dabx, dabx),
-                             O::mul(daby, daby));
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          te = min_ref(te, __shfl_xor_sync(0xffffffffu, te, o));
-          he = min_ref(he, __shfl_xor_sync(0xffffffffu, he, o));
-        }
-        acc = he > te;
-      }
-      __syncwarp();  // the slices are reused by the warp's next entry
-    } else {
-      bool a0 = false;
-      R2 c0{};
-      if (lane == 0) a0 = flow_decide_global<R, kSoA>(f, s, deg, pv, P, N, xonly, c0);
-      acc = __shfl_sync(0xffffffffu, a0, 0);
-      cand.x = __shfl_sync(0xffffffffu, c0.x, 0);
-      cand.y = __shfl_sync(0xffffffffu, c0.y, 0);
-    }
-    if (lane == 0) {
-      N.store(s, acc ? cand : pv);
-      st_release_gpu(f.done + s, static_cast<uint32_t>(q + 1));
-      if (acc) {
-        ++accepted;
-        const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
-        const double d = static_cast<double>(O::sqrt(O::add(O::mul(dx, dx), O::mul(dy, dy))));
-        disp = d > disp ? d : disp;
-      }
-    }
-    e += W;
-    if (e >= f.n) {
-      if (lane == 0) {
-        if (accepted) atomicAdd(f.slot_acc + gp * kStatSlots + stat_slot, accepted);
-        if (disp > 0.0)
-          atomicMax(f.slot_md + gp * kStatSlots + stat_slot, static_cast<unsigned long long>(__double_as_longlong(disp)));
-      }
-      accepted = 0;
-      disp = 0.0;
-      e = first;
-      ++q;
-    }
-  }
-}
-
 // done[] for a launch: movable entries start at 0 passes, pinned slots were set to ~0u once.
 __global__ void __launch_bounds__(256) flow_reset(const uint32_t* __restrict__ rec, int64_t n, uint32_t* done) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
