@@ -18,13 +18,17 @@
 // get copies of order / rank / off / nbr / fan / tier lists.
 #include <cuda_runtime.h>
 
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "tsg_device.cuh"
@@ -300,6 +304,26 @@ __global__ void __launch_bounds__(kT) k_ext_firsts(const uint32_t* __restrict__ 
   }
 }
 
+// The tile's unique external slots (run firsts of its sorted candidates) at ext_off[t].
+__global__ void __launch_bounds__(kT) k_ext_compact(const uint32_t* __restrict__ cand, const uint8_t* __restrict__ first,
+                                                    const uint32_t* __restrict__ tbound,
+                                                    const uint32_t* __restrict__ ext_off, uint32_t* __restrict__ ext) {
+  using Scan = cub::BlockScan<uint32_t, kT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int64_t t = blockIdx.x;
+  const uint32_t b = tbound[t], e = tbound[t + 1];
+  uint32_t out = ext_off[t];
+  for (uint32_t c = b; c < e; c += kT) {
+    const uint32_t i = c + threadIdx.x;
+    const uint32_t f = i < e ? first[i] : 0u;
+    uint32_t pos, total;
+    Scan(tmp).ExclusiveSum(f, pos, total);
+    if (f) ext[out + pos] = cand[i];
+    out += total;
+    __syncthreads();
+  }
+}
+
 __global__ void k_tile_bounds(const uint32_t* __restrict__ off, int64_t nv, int64_t ntiles, uint32_t* __restrict__ b) {
   FOR_I(ntiles + 1) {
     const int64_t s = i * kTile;
@@ -362,6 +386,62 @@ __global__ void k_widen(const uint32_t* __restrict__ in, int64_t n, uint64_t* __
 
 __global__ void k_narrow(const uint64_t* __restrict__ in, int64_t n, uint32_t* __restrict__ out) {
   FOR_I(n) out[i] = static_cast<uint32_t>(in[i]);
+}
+
+// Segment offsets [s0, s0 + count] relative to the first (one chunked CUB call).
+template <class Off>
+__global__ void k_rel_offsets(const Off* __restrict__ off, int64_t s0, int64_t count, uint32_t* __restrict__ rel) {
+  FOR_I(count + 1) rel[i] = static_cast<uint32_t>(off[s0 + i] - off[s0]);
+}
+
+// Segmented sorts in chunks of segments (each call well under 2^31 items and its own temp
+// storage): CUB's segmented sort at 1.5e9 items (cfg5) faulted on the device.
+// TSG_SEG_CHUNK overrides the segments per chunk (tests exercise many chunks at small sizes).
+int64_t seg_chunk(int64_t dflt) {
+  static const int64_t env = [] {
+    const char* e = std::getenv("TSG_SEG_CHUNK");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : 0;
+  }();
+  return env ? env : dflt;
+}
+
+template <class Off, class K, class V>
+cudaError_t seg_sort(cudaStream_t s, const K* kin, K* kout, const V* vin, V* vout, const Off* off, int64_t nseg,
+                     int64_t per_chunk, bool stable) {
+  uint32_t* rel = nullptr;
+  cudaError_t e = cudaMallocAsync(&rel, 4 * (per_chunk + 1), s);
+  if (e != cudaSuccess) return e;
+  for (int64_t s0 = 0; s0 < nseg && e == cudaSuccess; s0 += per_chunk) {
+    const int64_t cnt = std::min(per_chunk, nseg - s0);
+    Off ends[2];
+    if ((e = cudaMemcpyAsync(&ends[0], off + s0, sizeof(Off), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(&ends[1], off + s0 + cnt, sizeof(Off), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) break;
+    const int64_t b = static_cast<int64_t>(ends[0]), n = static_cast<int64_t>(ends[1]) - b;
+    if (n <= 0) continue;
+    k_rel_offsets<<<blocks(cnt + 1), kT, 0, s>>>(off, s0, cnt, rel);
+    if ((e = cudaGetLastError()) != cudaSuccess) break;
+    size_t bytes = 0;
+    void* tmp = nullptr;
+    auto call = [&](void* t, size_t& bb) -> cudaError_t {
+      if constexpr (std::is_same_v<V, void>) {
+        return cub::DeviceSegmentedSort::SortKeys(t, bb, kin + b, kout + b, static_cast<int>(n), static_cast<int>(cnt),
+                                                  rel, rel + 1, s);
+      } else if (stable) {
+        return cub::DeviceSegmentedSort::StableSortPairs(t, bb, kin + b, kout + b, vin + b, vout + b,
+                                                         static_cast<int>(n), static_cast<int>(cnt), rel, rel + 1, s);
+      } else {
+        return cub::DeviceSegmentedSort::SortPairs(t, bb, kin + b, kout + b, vin + b, vout + b, static_cast<int>(n),
+                                                   static_cast<int>(cnt), rel, rel + 1, s);
+      }
+    };
+    if ((e = call(nullptr, bytes)) != cudaSuccess) break;
+    if ((e = cudaMallocAsync(&tmp, bytes ? bytes : 8, s)) != cudaSuccess) break;
+    e = call(tmp, bytes);
+    cudaFreeAsync(tmp, s);
+  }
+  cudaFreeAsync(rel, s);
+  return e;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -457,9 +537,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
     DL_CUDA(cudaGetLastError());
     k_window_offsets<<<blocks(ntiles + 1), kT, 0, s>>>(ntiles, nv, seg);
     DL_CUDA(cudaGetLastError());
-    DL_CUDA(cub_call(A, [&](void* t, size_t& b) {
-      return cub::DeviceSegmentedSort::StableSortPairs(t, b, key, key2, given, order, nv, ntiles, seg, seg + 1, s);
-    }));
+    DL_CUDA(seg_sort(s, key, key2, given, order, seg, ntiles, seg_chunk(65536), true));
   } else {
     k_iota64<<<blocks(nv), kT, 0, s>>>(nv, order);
     DL_CUDA(cudaGetLastError());
@@ -567,10 +645,8 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
     DL_CUDA(cudaMalloc(&L.vinc, 4 * (itotal ? itotal : 1)));
     k_vinc<<<blocks(nv), kT, 0, s>>>(order, inc_off, inc, tri_rank, ioff64, nv, vtmp);
     DL_CUDA(cudaGetLastError());
-    DL_CUDA(cub_call(A, [&](void* t, size_t& b) {
-      return cub::DeviceSegmentedSort::SortKeys(t, b, vtmp, L.vinc, static_cast<int64_t>(itotal), nv, L.vinc_off,
-                                                L.vinc_off + 1, s);
-    }));
+    DL_CUDA(seg_sort(s, vtmp, L.vinc, static_cast<const void*>(nullptr), static_cast<void*>(nullptr), L.vinc_off, nv,
+                     seg_chunk(1 << 20), false));
   }
 
   // ---- tier lists (slot order), `large` by descending valence (stable)
@@ -631,9 +707,8 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   DL_CUDA(cudaGetLastError());
   k_tile_bounds<<<blocks(ntiles + 1), kT, 0, s>>>(L.off, nv, ntiles, tbound);
   DL_CUDA(cudaGetLastError());
-  DL_CUDA(cub_call(A, [&](void* t, size_t& b) {
-    return cub::DeviceSegmentedSort::SortKeys(t, b, cand, cand2, static_cast<int64_t>(total), ntiles, tbound, tbound + 1, s);
-  }));
+  DL_CUDA(seg_sort(s, cand, cand2, static_cast<const void*>(nullptr), static_cast<void*>(nullptr), tbound, ntiles,
+                   seg_chunk(16384), false));
   k_ext_firsts<<<static_cast<unsigned>(ntiles), kT, 0, s>>>(cand2, tbound, ntiles, first, ext_cnt);
   DL_CUDA(cudaGetLastError());
   DL_CUDA(cudaMalloc(&L.ext_off, 4 * (ntiles + 1)));
@@ -654,13 +729,8 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   hm.max_ext = static_cast<int32_t>(mx[0]);
   hm.max_rec_words = static_cast<int32_t>(mx[1]);
   DL_CUDA(cudaMalloc(&L.ext, 4 * (hext ? hext : 1)));
-  {
-    int64_t* nsel;
-    DL_CUDA(A.get(&nsel, 1));
-    DL_CUDA(cub_call(A, [&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, cand2, first, L.ext, nsel, static_cast<int64_t>(total), s);
-    }));
-  }
+  k_ext_compact<<<static_cast<unsigned>(ntiles), kT, 0, s>>>(cand2, first, tbound, L.ext_off, L.ext);
+  DL_CUDA(cudaGetLastError());
   DL_CUDA(cudaMalloc(&L.trec, 4 * (hwords ? hwords : 1)));
   DL_CUDA(cudaMemsetAsync(L.trec, 0, 4 * (hwords ? hwords : 1), s));
   k_tile_words<<<blocks(nv), kT, 0, s>>>(deg, L.off, L.nbr, cycpos, cycrot, has_cycle, L.tmeta, L.tile_rec, L.ext_off,

@@ -42,3 +42,21 @@ def test_device_hilbert_order_equals_host(capi, gpu_ctx, ts):
     for xy in (ts.delaunay_arrays(100000, 4)[0], ts.grid_arrays(300, 200, 0.3, 1)[0],
                np.vstack([ts.delaunay_arrays(5000, 1)[0], [[np.nan, 0.5]], [[2.0, 2.0]]])):
         assert np.array_equal(gpu_ctx.hilbert_order(xy), capi.hilbert_order(xy))
+
+
+def test_device_layout_in_many_sort_chunks(ts):
+    """The segmented sorts run in chunks of segments (cfg5 scale); a tiny chunk size forces
+    hundreds of chunks on a small mesh (child process: TSG_SEG_CHUNK is read once)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, sys.argv[1]); import paper_1502_00355_b200 as ts; "
+            "from paper_1502_00355_b200 import capi; ctx = capi.Context(0); "
+            "xy, tri = ts.graded_arrays(50000, 4, 3e-3, 600); topo = ctx.topology(len(xy), tri); "
+            "print(repr(ctx.layout_check(xy, tri, topo, capi.hilbert_order(xy))))")
+    r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, TSG_SEG_CHUNK="7"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert r.stdout.strip().endswith("''"), r.stdout
