@@ -9,7 +9,7 @@ import json
 import os
 import sys
 
-NODE_KERNELS = ("tile_update", "warp_update", "hub_fast_update", "node_update", "hub_update")
+NODE_KERNELS = ("tile_update", "side_rows", "warp_update", "hub_fast_update", "node_update", "hub_update")
 
 
 def main(path, key, passes):
