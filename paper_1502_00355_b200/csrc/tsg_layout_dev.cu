@@ -728,11 +728,11 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
     return "a tile references more than " + std::to_string(kNoLocal - kTile - 1) + " external vertices";
   hm.max_ext = static_cast<int32_t>(mx[0]);
   hm.max_rec_words = static_cast<int32_t>(mx[1]);
-  DL_CUDA(cudaMalloc(&L.ext, 4 * (hext ? hext : 1)));
+  DL_CUDA(cudaMalloc(&L.ext, sizeof(uint32_t) * static_cast<size_t>(hext ? hext : 1)));
   k_ext_compact<<<static_cast<unsigned>(ntiles), kT, 0, s>>>(cand2, first, tbound, L.ext_off, L.ext);
   DL_CUDA(cudaGetLastError());
-  DL_CUDA(cudaMalloc(&L.trec, 4 * (hwords ? hwords : 1)));
-  DL_CUDA(cudaMemsetAsync(L.trec, 0, 4 * (hwords ? hwords : 1), s));
+  DL_CUDA(cudaMalloc(&L.trec, sizeof(uint32_t) * static_cast<size_t>(hwords ? hwords : 1)));
+  DL_CUDA(cudaMemsetAsync(L.trec, 0, sizeof(uint32_t) * static_cast<size_t>(hwords ? hwords : 1), s));
   k_tile_words<<<blocks(nv), kT, 0, s>>>(deg, L.off, L.nbr, cycpos, cycrot, has_cycle, L.tmeta, L.tile_rec, L.ext_off,
                                          L.ext, nv, L.trec);
   DL_CUDA(cudaGetLastError());
