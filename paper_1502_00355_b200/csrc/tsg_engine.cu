@@ -469,8 +469,9 @@ struct tsg_mesh {
   tsg::PeerSync* d_peer_sync = nullptr;
   tsg::PeerEntry* d_peer_tab = nullptr;
   int32_t* d_push_peer = nullptr;
-  uint32_t *d_push_src = nullptr, *d_push_dst = nullptr;
+  uint32_t *d_push_src = nullptr, *d_push_dst = nullptr;  // rows of valence > 31 (peer_push)
   int64_t n_push = 0;
+  uint32_t *d_fpush_mask = nullptr, *d_fpush_off = nullptr, *d_fpush_peer = nullptr, *d_fpush_dst = nullptr;  // tile rows
   uint32_t peer_tick = 0;  // last tick of the previous peer run (identical on every rank)
   uint32_t h_peer_tick0 = 0;  // host copy of this run's start tick (source of an async copy)
 };
@@ -835,6 +836,8 @@ struct Engine {
     t.small_max = kMaxSmallDeg;
     t.medium_max = kMaxMedDeg;
     t.nv = m->hm.nv;
+    if (m->peer_world > 1 && m->d_fpush_mask)
+      t.push = tsg::TilePush{m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst, m->d_peer_tab};
     return t;
   }
 
@@ -1184,7 +1187,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     err = tsg::build_device_layout(s, *d, kTiers, m->hm, L);
     if (!err.empty()) {
       tsg::free_layout(L);
-      return fail(err.find("cuda") != std::string::npos ? TSG_ERR_CUDA : TSG_ERR_INVALID, err);
+      return fail(err.rfind("CUDA: ", 0) == 0 ? TSG_ERR_CUDA : TSG_ERR_INVALID, err);
     }
     const auto& h = m->hm;
     const int64_t ntiles = (h.nv + tsg::kTile - 1) / tsg::kTile;
@@ -1303,7 +1306,8 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
                   m->d_tri, m->d_hubs, m->d_medium, m->d_large, m->d_maxabs, m->d_order, m->d_tri_order, m->d_alpha, m->d_xy_stage,
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_side_ctr, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage,
-                  m->d_peer_sync, m->d_peer_tab, m->d_push_peer, m->d_push_src, m->d_push_dst};
+                  m->d_peer_sync, m->d_peer_tab, m->d_push_peer, m->d_push_src, m->d_push_dst,
+                  m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst};
   for (void* p : ptrs) cudaFree(p);
   for (int b = 0; b < 2; ++b) {
     cudaFree(m->d_batch_in[b]);
@@ -2280,32 +2284,62 @@ tsg_status tsg_peer_setup(tsg_mesh* m, int32_t rank, int32_t world, void* const*
       return fail(TSG_ERR_INVALID, "missing peer mapping");
     tab[r] = tsg::PeerEntry{static_cast<tsg::PeerSync*>(peer_sync[r]), peer_buf0[r], peer_buf1[r], peer_nv[r]};
   }
-  std::vector<int32_t> pp(n_push);
-  std::vector<uint32_t> src(n_push), dst(n_push);
+  // Split the plan: tile rows (valence 1..31) are pushed by tile_update itself right after their
+  // local store (per-slot CSR + bitmask); longer rows by peer_push after the side kernels;
+  // pinned vertices never change, so their halo copies stay as set_coords left them.
+  const int64_t nv = m->hm.nv;
+  std::vector<int32_t> pp;
+  std::vector<uint32_t> src, dst;
+  std::vector<uint32_t> fcnt(nv + 1, 0), fmask((nv + 31) / 32, 0);
+  std::vector<std::pair<uint32_t, uint32_t>> fent(n_push);  // (slot, entry index) of tile rows
+  int64_t nf = 0;
   for (int64_t i = 0; i < n_push; ++i) {
     const int32_t q = push_peer[i];
     if (q < 0 || q >= world || q == rank) return fail(TSG_ERR_INVALID, "push peer out of range");
-    if (push_src_ids[i] < 0 || push_src_ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "push source out of range");
+    if (push_src_ids[i] < 0 || push_src_ids[i] >= nv) return fail(TSG_ERR_INVALID, "push source out of range");
     if (push_dst_slots[i] < 0 || push_dst_slots[i] >= peer_nv[q]) return fail(TSG_ERR_INVALID, "push slot out of range");
-    pp[i] = q;
-    src[i] = static_cast<uint32_t>(m->hm.rank[push_src_ids[i]]);
-    dst[i] = static_cast<uint32_t>(push_dst_slots[i]);
+    const uint32_t sl = static_cast<uint32_t>(m->hm.rank[push_src_ids[i]]);
+    const uint32_t deg = m->hm.off[sl + 1] - m->hm.off[sl];
+    if (deg == 0) continue;
+    if (deg <= static_cast<uint32_t>(tsg::kMaxCycleDeg)) {
+      fent[nf++] = {sl, static_cast<uint32_t>(i)};
+      ++fcnt[sl + 1];
+      fmask[sl >> 5] |= 1u << (sl & 31);
+    } else {
+      pp.push_back(q);
+      src.push_back(sl);
+      dst.push_back(static_cast<uint32_t>(push_dst_slots[i]));
+    }
   }
-  cudaFree(m->d_peer_tab);
-  cudaFree(m->d_push_peer);
-  cudaFree(m->d_push_src);
-  cudaFree(m->d_push_dst);
+  for (int64_t v = 0; v < nv; ++v) fcnt[v + 1] += fcnt[v];
+  std::vector<uint32_t> fpeer(nf), fdst(nf), fpos(fcnt.begin(), fcnt.end() - 1);
+  for (int64_t k = 0; k < nf; ++k) {
+    const uint32_t sl = fent[k].first, i = fent[k].second;
+    const uint32_t at = fpos[sl]++;
+    fpeer[at] = static_cast<uint32_t>(push_peer[i]);
+    fdst[at] = static_cast<uint32_t>(push_dst_slots[i]);
+  }
+  for (void* p : {static_cast<void*>(m->d_peer_tab), static_cast<void*>(m->d_push_peer),
+                  static_cast<void*>(m->d_push_src), static_cast<void*>(m->d_push_dst),
+                  static_cast<void*>(m->d_fpush_mask), static_cast<void*>(m->d_fpush_off),
+                  static_cast<void*>(m->d_fpush_peer), static_cast<void*>(m->d_fpush_dst)})
+    cudaFree(p);
   m->d_peer_tab = nullptr;
   m->d_push_peer = nullptr;
   m->d_push_src = m->d_push_dst = nullptr;
+  m->d_fpush_mask = m->d_fpush_off = m->d_fpush_peer = m->d_fpush_dst = nullptr;
   int64_t b = 0;
   cudaStream_t s = m->ctx->stream;
   if ((st = upload(&m->d_peer_tab, tab, &b, s))) return st;
   if ((st = upload(&m->d_push_peer, pp, &b, s))) return st;
   if ((st = upload(&m->d_push_src, src, &b, s))) return st;
   if ((st = upload(&m->d_push_dst, dst, &b, s))) return st;
+  if ((st = upload(&m->d_fpush_mask, fmask, &b, s))) return st;
+  if ((st = upload(&m->d_fpush_off, fcnt, &b, s))) return st;
+  if ((st = upload(&m->d_fpush_peer, fpeer, &b, s))) return st;
+  if ((st = upload(&m->d_fpush_dst, fdst, &b, s))) return st;
   TSG_CUDA(cudaStreamSynchronize(s));
-  m->n_push = n_push;
+  m->n_push = static_cast<int64_t>(pp.size());
   m->peer_rank = rank;
   m->peer_world = world;
   m->gc.reset();

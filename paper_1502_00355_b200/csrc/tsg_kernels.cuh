@@ -404,7 +404,40 @@ __device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typena
 // Tile arrays (tsg_prep.hpp build_tiles).
 constexpr int kTileMinBlocks = 3;  // 256-thread CTAs per SM the register budget is sized for
 
+// Peer-memory partitions (tsg_peer.cuh): one rank's view of another (mapped pointers).
+struct PeerSync;
+struct PeerEntry {
+  PeerSync* sync;
+  void* buf0;
+  void* buf1;
+  int64_t nv;
+};
+
+// Halo stores fused into the tile kernel (peer-memory driver; all null otherwise): right after
+// a tile row's new value is stored locally it is stored into every peer whose halo holds the
+// vertex, so the exchange overlaps the pass tile by tile instead of following it.
+struct TilePush {
+  const uint32_t* mask;   // bit (s & 31) of word s >> 5: slot s is in some peer's halo
+  const uint32_t* off;    // destinations of slot s: entries off[s] .. off[s+1]-1
+  const uint32_t* peer;   // destination rank
+  const uint32_t* dst;    // destination slot in that rank's mesh
+  const PeerEntry* tab;   // the world's mapped buffers
+};
+
+template <typename R, bool kSoA>
+__device__ __forceinline__ bool push_to_peers(const TilePush& p, int pass, int64_t s, typename Arith<R>::R2 v) {
+  if (!p.mask || !((__ldg(p.mask + (s >> 5)) >> (s & 31)) & 1u)) return false;
+  const uint32_t k1 = __ldg(p.off + s + 1);
+  for (uint32_t k = __ldg(p.off + s); k < k1; ++k) {
+    const PeerEntry e = p.tab[__ldg(p.peer + k)];
+    const Coords<R, kSoA> D{static_cast<R*>((pass & 1) ? e.buf0 : e.buf1), e.nv};
+    D.store(__ldg(p.dst + k), v);
+  }
+  return true;
+}
+
 struct TileArgs {
+  TilePush push;
   const uint32_t* meta;      // per slot: first word | deg << 16 | group stride << 20
   const uint32_t* rec;       // words: row[j] | cycle[j] << 16 (local indices)
   const uint32_t* tile_rec;  // ntiles + 1 (first word of each tile, multiples of 4)
@@ -648,6 +681,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   int8_t* const decision = a.decision;
   int accepted = 0;
   double disp = 0.0;
+  bool pushed = false;
 
   // One vertex of the tile (local index i).
   auto vertex = [&](int i, uint32_t meta) {
@@ -736,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
       }
     }
     N.store(s, acc ? cand : pv);
+    pushed |= push_to_peers<R, kSoA>(t.push, pass, s, acc ? cand : pv);
     if (acc) {
       ++accepted;
       const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
@@ -798,6 +833,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
       const bool acc = hyp > thr;
       const int64_t s = base + i;
       N.store(s, acc ? cand : pv);
+      pushed |= push_to_peers<R, kSoA>(t.push, pass, s, acc ? cand : pv);
       if (acc) {
         ++accepted;
         const R dx = O::sub(cand.x, pv.x), dy = O::sub(cand.y, pv.y);
@@ -808,6 +844,7 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     }
   }
   commit_stats_warp(accepted, disp, a.slot_acc + pass * kStatSlots, a.slot_md + pass * kStatSlots);
+  if (pushed) __threadfence_system();  // peer stores before the pass barrier's release (peer_sync)
   TSG_TRACE_SYNC();
   TSG_TRACE_END(0, blockIdx.x, tid == 0)
 }

@@ -486,7 +486,7 @@ cudaError_t to_host(std::vector<T>& h, const T* d, int64_t n, cudaStream_t s) {
 #define DL_CUDA(x)                                                                  \
   do {                                                                              \
     cudaError_t e_ = (x);                                                           \
-    if (e_ != cudaSuccess) return std::string(#x) + ": " + cudaGetErrorString(e_); \
+    if (e_ != cudaSuccess) return std::string("CUDA: ") + #x + ": " + cudaGetErrorString(e_); \
   } while (0)
 
 }  // namespace

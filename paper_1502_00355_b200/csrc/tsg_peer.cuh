@@ -6,8 +6,10 @@
 //
 // Per pass on rank r (reference loop proj/src/smoothing.cpp:98-141):
 //   1. the node kernels update r's owned vertices (N buffer);
-//   2. peer_push: every owned vertex that lies in peer q's halo is stored straight into q's N
-//      buffer at q's slot for it (P2P stores over NVLink; same-device pointers in tests);
+//   2. every owned vertex that lies in peer q's halo is stored straight into q's N buffer at q's
+//      slot for it (P2P stores over NVLink; same-device pointers in tests): by tile_update right
+//      after it stores the vertex locally (TilePush: the exchange overlaps the pass tile by
+//      tile), by peer_push after the side kernels for rows of valence > 31;
 //   3. peer_sync (one warp): r's {accepted, max displacement} of the pass is written into every
 //      rank's stats table, then r publishes tick t = tick0 + pass + 1 into flag[r] of every
 //      peer (st.release.sys after a system fence) and waits until every peer's flag in its own
@@ -37,12 +39,7 @@ struct PeerSync {  // one per mesh; peers map it
   uint32_t tick0;                       // this run's start tick (written by the host)
 };
 
-struct PeerEntry {  // one per rank, as mapped in this process
-  PeerSync* sync;
-  void* buf0;
-  void* buf1;
-  int64_t nv;
-};
+// PeerEntry (one per rank, as mapped in this process) and TilePush: tsg_kernels.cuh.
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
