@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <type_traits>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -362,6 +363,25 @@ __global__ void dist_halo_unpack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b
 // The dynamic shared-memory limit of a kernel is a per-function, per-device setting shared by
 // every mesh: only ever raise it (a later mesh needing less must not lower the limit an earlier
 // mesh's launches rely on).
+// Slots per tile the tile kernel is compiled for (tsg_mesh_upload picks one per mesh).
+constexpr int kTileSizes[] = {768, 1024, 1280};
+
+bool tile_supported(int tile) {
+  for (int t : kTileSizes)
+    if (t == tile) return true;
+  return false;
+}
+
+// f(std::integral_constant<int, tile>) for a supported tile size.
+template <class F>
+void with_tile(int tile, F&& f) {
+  switch (tile) {
+    case 768: f(std::integral_constant<int, 768>{}); break;
+    case 1024: f(std::integral_constant<int, 1024>{}); break;
+    default: f(std::integral_constant<int, 1280>{}); break;
+  }
+}
+
 template <class K>
 cudaError_t raise_smem_limit(K* fn, int bytes) {
   static std::mutex mu;
@@ -700,12 +720,15 @@ struct Engine {
       a.list = nullptr;
       a.count = nv;
       const tsg::TileArgs ta = tile_args(m);
-      const unsigned ntiles = static_cast<unsigned>((nv + tsg::kTile - 1) / tsg::kTile);
-      const size_t smem = tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap);
-      if (tiles_staged(m))
-        tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true><<<ntiles, kTileThreads, smem, s>>>(a, ta);
-      else
-        tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false><<<ntiles, kTileThreads, smem, s>>>(a, ta);
+      const unsigned ntiles = static_cast<unsigned>((nv + ta.tile - 1) / ta.tile);
+      const size_t smem = tsg::tile_smem_bytes<R>(ta.tile, ta.ext_cap, ta.rec_cap);
+      const bool staged = tiles_staged(m);
+      with_tile(ta.tile, [&](auto K) {
+        if (staged)
+          tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true, K><<<ntiles, kTileThreads, smem, s>>>(a, ta);
+        else
+          tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false, K><<<ntiles, kTileThreads, smem, s>>>(a, ta);
+      });
       TSG_LAUNCHED();
       ++*kernels;
     }
@@ -831,10 +854,13 @@ struct Engine {
     t.tile_rec = m->d_tile_rec;
     t.ext_off = m->d_ext_off;
     t.ext = m->d_tile_ext;
-    t.ext_cap = std::min(m->hm.max_ext, kTileExtCap);
+    // Even, so that the words after the staged coordinates stay 16-byte aligned for fp32 pairs
+    // (bulk copies and uint4 stores).
+    t.ext_cap = (std::min(m->hm.max_ext, kTileExtCap) + 1) & ~1;
     t.rec_cap = std::min(m->hm.max_rec_words, kTileRecCap);
     t.small_max = kMaxSmallDeg;
     t.medium_max = kMaxMedDeg;
+    t.tile = m->hm.tile;
     t.nv = m->hm.nv;
     if (m->peer_world > 1 && m->d_fpush_mask)
       t.push = tsg::TilePush{m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst, m->d_peer_tab};
@@ -847,22 +873,31 @@ struct Engine {
     TSG_CUDA(raise_smem_limit(tsg::hub_fast_update<R, kSoA>, static_cast<int>(hub_fast_cap(m) * sizeof(R2))));
     {
       const tsg::TileArgs ta = tile_args(m);
-      const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.ext_cap, ta.rec_cap));
+      const int smem = static_cast<int>(tsg::tile_smem_bytes<R>(ta.tile, ta.ext_cap, ta.rec_cap));
       if (std::getenv("TSG_DIAG"))
-        std::fprintf(stderr, "[tsg] tile smem %d B (ext_cap %d, rec_cap %d words), large rows %zu (hub CTAs %lld)\n",
-                     smem, ta.ext_cap, ta.rec_cap, m->hm.large.size(), static_cast<long long>(m->n_hub_fast));
-      TSG_CUDA(raise_smem_limit(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>, smem));
-      TSG_CUDA(raise_smem_limit(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>, smem));
+        std::fprintf(stderr, "[tsg] tile %d slots, smem %d B (ext_cap %d, rec_cap %d words), large rows %zu (hub CTAs %lld)\n",
+                     ta.tile, smem, ta.ext_cap, ta.rec_cap, m->hm.large.size(), static_cast<long long>(m->n_hub_fast));
+      cudaError_t e = cudaSuccess;
+      with_tile(ta.tile, [&](auto K) {
+        e = raise_smem_limit(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true, K>, smem);
+        if (e == cudaSuccess) e = raise_smem_limit(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false, K>, smem);
+      });
+      TSG_CUDA(e);
     }
     // Kernels that run concurrently on one SM must agree on its L1 / shared-memory split: the
     // tile and side-tier kernels all ask for the maximum shared-memory carveout, so that a
     // side-tier CTA does not pin an SM to a smaller split that excludes the tile kernel's CTAs.
     {
       const int kMax = cudaSharedmemCarveoutMaxShared;
-      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
-      TSG_CUDA(cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
+      cudaError_t e = cudaSuccess;
+      with_tile(m->hm.tile, [&](auto K) {
+        e = cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true, K>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, kMax);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false, K>,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, kMax);
+      });
+      TSG_CUDA(e);
       TSG_CUDA(cudaFuncSetAttribute(tsg::hub_fast_update<R, kSoA>, cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
       TSG_CUDA(cudaFuncSetAttribute(tsg::warp_update<R, kSoA, kWarpTierWarps, kWarpTierCap>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, kMax));
@@ -1159,6 +1194,39 @@ tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, 
   return TSG_OK;
 }
 
+namespace {
+
+// Shared memory of one tile CTA: dynamic (tile_smem_bytes) + ~3 KB static + 1 KB reserved.
+size_t tile_smem_estimate(const tsg::HostMesh& hm, int rsize) {
+  return 2 * static_cast<size_t>(rsize) * (hm.tile + ((std::min(hm.max_ext, kTileExtCap) + 1) & ~1)) +
+         4 * static_cast<size_t>(std::min(hm.max_rec_words, kTileRecCap)) + 4 * static_cast<size_t>(hm.tile) + 4096;
+}
+
+// kTileMinBlocks tile CTAs still fit one SM's 228 KB.
+bool tile_fits(const tsg::HostMesh& hm, int rsize) {
+  return tsg::kTileMinBlocks * tile_smem_estimate(hm, rsize) <= 228 * 1024;
+}
+
+// Slots per tile (a compiled size, kTileSizes).  Larger tiles stage fewer external
+// coordinates per vertex (halo ~ perimeter / area); smaller tiles balance the last waves of the
+// grid better.  Measured on one B200, 3 CTAs per SM (profiles/r02/tile_sizes.txt):
+//   cfg3 16M f64  768 31.9 / 1024 34.0 / 1280 35.5 G/s;  cfg4 64M f64 1024 38.8 / 1280 40.4;
+//   cfg3 f32 1024 41.7 / 1280 43.9;  cfg2 1M f64 768 22.5 / 1024 22.0 / 1280 21.1;
+//   cfg2 1M f32 768 31.6 / 1024 32.3 / 1280 29.6.
+// So: 1280 once the grid runs >= 8 waves of 1280-slot tiles; below that 1024 for fp32 meshes
+// of at least one wave and 768 otherwise.  TSG_TILE forces a size (tests, measurements); upload
+// falls back to kTile when a larger tile exceeds a layout or shared-memory limit.
+int32_t choose_tile(int64_t nv, int num_sms, int rsize) {
+  if (const char* e = std::getenv("TSG_TILE")) return tile_supported(std::atoi(e)) ? std::atoi(e) : -1;
+  const double slots = static_cast<double>(std::max(1, num_sms)) * tsg::kTileMinBlocks;
+  const double nvd = static_cast<double>(nv);
+  if (nvd >= 8.0 * slots * 1280) return 1280;
+  if (rsize == 4 && nvd >= slots * 1024) return 1024;
+  return 768;
+}
+
+}  // namespace
+
 tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** out) {
   TSG_LOCK_CTX(ctx);
   if (!ctx || !d || !out) return fail(TSG_ERR_INVALID, "null argument");
@@ -1177,6 +1245,9 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   cudaStream_t s = ctx->stream;
   int64_t* b = &m->bytes;
   tsg_status st;
+  TSG_CUDA(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int32_t tile = choose_tile(d->nv, m->num_sms, m->rsize);
+  if (tile < 0) return fail(TSG_ERR_INVALID, "TSG_TILE must be one of 768, 1024, 1280");
   // Device layout: built on the GPU (tsg_layout_dev.cu, default) or on the host
   // (build_host_mesh, TSG_HOST_PREP=1); identical arrays either way.
   static const bool host_prep = std::getenv("TSG_HOST_PREP") != nullptr;
@@ -1184,13 +1255,20 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     std::string err = tsg::validate_desc(*d);
     if (!err.empty()) return fail(TSG_ERR_INVALID, err);
     tsg::DeviceLayout L;
-    err = tsg::build_device_layout(s, *d, kTiers, m->hm, L);
+    err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tile);
+    // Larger tiles can overflow the 15-bit word offsets (rows of high valence) or the shared
+    // memory of kTileMinBlocks CTAs: fall back to kTile, whose limits every mesh meets.
+    if (tile != tsg::kTile && err.rfind("CUDA: ", 0) != 0 && (!err.empty() || !tile_fits(m->hm, m->rsize))) {
+      tsg::free_layout(L);
+      L = tsg::DeviceLayout{};
+      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tsg::kTile);
+    }
     if (!err.empty()) {
       tsg::free_layout(L);
       return fail(err.rfind("CUDA: ", 0) == 0 ? TSG_ERR_CUDA : TSG_ERR_INVALID, err);
     }
     const auto& h = m->hm;
-    const int64_t ntiles = (h.nv + tsg::kTile - 1) / tsg::kTile;
+    const int64_t ntiles = (h.nv + h.tile - 1) / h.tile;
     m->d_off = L.off;
     m->d_nbr = L.nbr;
     m->d_fan = L.fan;
@@ -1212,7 +1290,9 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     if ((st = upload(&m->d_medium, h.medium, b, s))) return st;
     if ((st = upload(&m->d_large, h.large, b, s))) return st;
   } else {
-    const std::string err = tsg::build_host_mesh(*d, kTiers, m->hm);
+    std::string err = tsg::build_host_mesh(*d, kTiers, m->hm, tile);
+    if (tile != tsg::kTile && (!err.empty() || !tile_fits(m->hm, m->rsize)))
+      err = tsg::build_host_mesh(*d, kTiers, m->hm, tsg::kTile);
     if (!err.empty()) return fail(TSG_ERR_INVALID, err);
     const auto& h = m->hm;
     if ((st = upload(&m->d_off, h.off, b, s))) return st;
@@ -1252,7 +1332,6 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if ((st = dalloc(&m->d_ext, 3, b))) return st;
   if ((st = dalloc(&m->d_side_ctr, 2, b))) return st;
   TSG_CUDA(cudaMemsetAsync(m->d_side_ctr, 0, 2 * sizeof(uint32_t), s));
-  TSG_CUDA(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->ctx->device));
   for (int32_t s2 : hm.hubs) m->hub_max_deg = std::max<int32_t>(m->hub_max_deg, hm.off[s2 + 1] - hm.off[s2]);
   while (m->n_hub_fast < static_cast<int64_t>(hm.large.size()) &&
          hm.off[hm.large[m->n_hub_fast] + 1] - hm.off[hm.large[m->n_hub_fast]] > static_cast<uint32_t>(kHubFastMin))
@@ -1275,9 +1354,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     // ... and only when one side CTA fits in the shared memory left by kTileMinBlocks tile CTAs
     // (dynamic + ~3 KB static + 1 KB reserved each; 228 KB per SM).
     const size_t pair = 2 * m->rsize;
-    const size_t tile_smem = pair * (tsg::kTile + std::min(hm.max_ext, kTileExtCap)) +
-                             4 * static_cast<size_t>(std::min(hm.max_rec_words, kTileRecCap)) + 4 * tsg::kTile +
-                             4096;
+    const size_t tile_smem = tile_smem_estimate(hm, m->rsize);
     const size_t side_smem = kSideWarps * static_cast<size_t>(kWarpTierCap) * pair + 1024;
     const bool fits = tsg::kTileMinBlocks * tile_smem + side_smem <= 228 * 1024;
     m->side_persist_auto = !hm.large.empty() && side_us <= tile_us && fits;
@@ -2401,10 +2478,14 @@ tsg_status tsg_debug_layout_check(tsg_context* ctx, const tsg_mesh_desc* d, char
   if (!ctx || !d || !mismatch || cap < 1) return fail(TSG_ERR_INVALID, "null argument");
   TSG_CUDA(cudaSetDevice(ctx->device));
   tsg::HostMesh H, D;
-  std::string err = tsg::build_host_mesh(*d, kTiers, H);
+  int num_sms = 0;
+  TSG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int32_t tile = choose_tile(d->nv, num_sms, d->precision == TSG_F64 ? 8 : 4);
+  if (tile < 0) return fail(TSG_ERR_INVALID, "TSG_TILE must be one of 768, 1024, 1280");
+  std::string err = tsg::build_host_mesh(*d, kTiers, H, tile);
   if (!err.empty()) return fail(TSG_ERR_INVALID, "host: " + err);
   tsg::DeviceLayout L;
-  err = tsg::build_device_layout(ctx->stream, *d, kTiers, D, L);
+  err = tsg::build_device_layout(ctx->stream, *d, kTiers, D, L, tile);
   if (err.empty()) err = tsg::download_layout(ctx->stream, L, D);
   tsg::free_layout(L);
   if (!err.empty()) return fail(TSG_ERR_CUDA, "device: " + err);
@@ -2430,6 +2511,7 @@ tsg_status tsg_debug_layout_check(tsg_context* ctx, const tsg_mesh_desc* d, char
   cmp("ext_off", H.ext_off, D.ext_off);
   cmp("ext", H.ext, D.ext);
   cmp("trec", H.trec, D.trec);
+  if (bad.empty() && H.tile != D.tile) bad = "tile";
   if (bad.empty() && (H.max_ext != D.max_ext || H.max_rec_words != D.max_rec_words || H.max_deg != D.max_deg))
     bad = "scalars";
   std::snprintf(mismatch, static_cast<size_t>(cap), "%s", bad.c_str());

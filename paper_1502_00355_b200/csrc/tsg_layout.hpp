@@ -12,7 +12,8 @@ constexpr int kMaxCycleDeg = 31;  // tile (thread-per-vertex) rows: valence <= 3
 #ifndef TSG_TILE
 #define TSG_TILE 1024
 #endif
-constexpr int kTile = TSG_TILE;
+constexpr int kTile = TSG_TILE;  // default slots per tile (a mesh may use up to kTileMax)
+constexpr int kTileMax = 1536;  // group stride (11 bits) < 2048; meta word offsets 15 bits
 constexpr uint32_t kNoLocal = 0x3fffu;  // cycle entry of a row without a single link cycle
 // Tile row word: row[j] (bits 0-13) | cycle[j] (bits 16-29) | k[j] (bits 30-31).
 constexpr uint32_t kLocalMask = 0x3fffu;

@@ -226,9 +226,9 @@ __global__ void k_tier_flags(const uint32_t* __restrict__ deg, int64_t nv, Tiers
 
 // Per tile: tmeta of the small rows (group bases in ascending valence, stable rank inside a
 // group) and the tile's word count.  One CTA per tile; degrees staged in shared memory.
-__global__ void __launch_bounds__(kT) k_tile_meta(const uint32_t* __restrict__ deg, int64_t nv,
+__global__ void __launch_bounds__(kT) k_tile_meta(const uint32_t* __restrict__ deg, int64_t nv, int kTile,
                                                   uint32_t* __restrict__ tmeta, uint32_t* __restrict__ words) {
-  __shared__ uint8_t d_s[kTile];
+  __shared__ uint8_t d_s[kTileMax];
   __shared__ uint32_t count[kMaxCycleDeg + 1], gbase[kMaxCycleDeg + 2];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
   const int n = static_cast<int>(nv - base < kTile ? nv - base : kTile);
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kT) k_tile_meta(const uint32_t* __restrict__ d
 // External-slot candidates: for every row entry of a small row, the neighbour slot if it lies
 // outside the row's tile, else UINT32_MAX (dropped after the sort).
 __global__ void k_ext_candidates(const uint32_t* __restrict__ deg, const uint32_t* __restrict__ off,
-                                 const uint32_t* __restrict__ nbr, int64_t nv, uint32_t* __restrict__ cand) {
+                                 const uint32_t* __restrict__ nbr, int64_t nv, int kTile, uint32_t* __restrict__ cand) {
   FOR_I(nv) {
     const uint32_t d = deg[i];
     const uint32_t o = off[i], o1 = off[i + 1];
@@ -324,7 +324,8 @@ __global__ void __launch_bounds__(kT) k_ext_compact(const uint32_t* __restrict__
   }
 }
 
-__global__ void k_tile_bounds(const uint32_t* __restrict__ off, int64_t nv, int64_t ntiles, uint32_t* __restrict__ b) {
+__global__ void k_tile_bounds(const uint32_t* __restrict__ off, int64_t nv, int64_t ntiles, int kTile,
+                              uint32_t* __restrict__ b) {
   FOR_I(ntiles + 1) {
     const int64_t s = i * kTile;
     b[i] = off[s < nv ? s : nv];
@@ -347,7 +348,7 @@ __global__ void k_tile_words(const uint32_t* __restrict__ deg, const uint32_t* _
                              const uint8_t* __restrict__ cycrot, const uint8_t* __restrict__ has_cycle,
                              const uint32_t* __restrict__ tmeta, const uint32_t* __restrict__ tile_rec,
                              const uint32_t* __restrict__ ext_off, const uint32_t* __restrict__ ext, int64_t nv,
-                             uint32_t* __restrict__ trec) {
+                             int kTile, uint32_t* __restrict__ trec) {
   FOR_I(nv) {
     const uint32_t d = deg[i];
     if (!(d >= 1 && d <= static_cast<uint32_t>(kMaxCycleDeg))) continue;
@@ -372,7 +373,7 @@ __global__ void k_tile_words(const uint32_t* __restrict__ deg, const uint32_t* _
   }
 }
 
-__global__ void k_window_offsets(int64_t ntiles, int64_t nv, int64_t* __restrict__ seg) {
+__global__ void k_window_offsets(int64_t ntiles, int64_t nv, int kTile, int64_t* __restrict__ seg) {
   FOR_I(ntiles + 1) seg[i] = i * kTile < nv ? i * kTile : nv;
 }
 
@@ -492,8 +493,10 @@ cudaError_t to_host(std::vector<T>& h, const T* d, int64_t n, cudaStream_t s) {
 }  // namespace
 
 std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
-                                DeviceLayout& L) {
+                                DeviceLayout& L, int32_t tile) {
   const int64_t nv = d.nv, nt = d.nt;
+  if (tile < 256 || tile > kTileMax || tile % 256) return "tile size must be a multiple of 256 in [256, 1536]";
+  const int kTile = tile;
   if (nv <= 0 || nt <= 0) return "mesh must have vertices and triangles";
   if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
   if (nt >= (int64_t{1} << 32)) return "triangle count exceeds 2^32";
@@ -501,6 +504,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   hm = HostMesh{};
   hm.nv = nv;
   hm.nt = nt;
+  hm.tile = tile;
   const int64_t nnb = d.nbr_off[nv], ninc = d.inc_off[nv];
   const int64_t ntiles = (nv + kTile - 1) / kTile;
 
@@ -535,7 +539,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
     DL_CUDA(cudaMemcpyAsync(given, d.order, 8 * nv, cudaMemcpyHostToDevice, s));
     k_window_keys<<<blocks(nv), kT, 0, s>>>(given, bnd, nbr_off, nv, key);
     DL_CUDA(cudaGetLastError());
-    k_window_offsets<<<blocks(ntiles + 1), kT, 0, s>>>(ntiles, nv, seg);
+    k_window_offsets<<<blocks(ntiles + 1), kT, 0, s>>>(ntiles, nv, kTile, seg);
     DL_CUDA(cudaGetLastError());
     DL_CUDA(seg_sort(s, key, key2, given, order, seg, ntiles, seg_chunk(65536), true));
   } else {
@@ -701,11 +705,11 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   DL_CUDA(A.get(&first, static_cast<int64_t>(total)));
   DL_CUDA(cudaMemsetAsync(words + ntiles, 0, 4, s));
   DL_CUDA(cudaMemsetAsync(ext_cnt + ntiles, 0, 4, s));
-  k_tile_meta<<<static_cast<unsigned>(ntiles), kT, 0, s>>>(deg, nv, L.tmeta, words);
+  k_tile_meta<<<static_cast<unsigned>(ntiles), kT, 0, s>>>(deg, nv, kTile, L.tmeta, words);
   DL_CUDA(cudaGetLastError());
-  k_ext_candidates<<<blocks(nv), kT, 0, s>>>(deg, L.off, L.nbr, nv, cand);
+  k_ext_candidates<<<blocks(nv), kT, 0, s>>>(deg, L.off, L.nbr, nv, kTile, cand);
   DL_CUDA(cudaGetLastError());
-  k_tile_bounds<<<blocks(ntiles + 1), kT, 0, s>>>(L.off, nv, ntiles, tbound);
+  k_tile_bounds<<<blocks(ntiles + 1), kT, 0, s>>>(L.off, nv, ntiles, kTile, tbound);
   DL_CUDA(cudaGetLastError());
   DL_CUDA(seg_sort(s, cand, cand2, static_cast<const void*>(nullptr), static_cast<void*>(nullptr), tbound, ntiles,
                    seg_chunk(16384), false));
@@ -726,6 +730,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   DL_CUDA(cudaStreamSynchronize(s));
   if (kTile + static_cast<int64_t>(mx[0]) >= static_cast<int64_t>(kNoLocal))
     return "a tile references more than " + std::to_string(kNoLocal - kTile - 1) + " external vertices";
+  if (mx[1] > kMetaBaseMask + 1) return "tile words exceed the meta offset field";
   hm.max_ext = static_cast<int32_t>(mx[0]);
   hm.max_rec_words = static_cast<int32_t>(mx[1]);
   DL_CUDA(cudaMalloc(&L.ext, sizeof(uint32_t) * static_cast<size_t>(hext ? hext : 1)));
@@ -734,7 +739,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   DL_CUDA(cudaMalloc(&L.trec, sizeof(uint32_t) * static_cast<size_t>(hwords ? hwords : 1)));
   DL_CUDA(cudaMemsetAsync(L.trec, 0, sizeof(uint32_t) * static_cast<size_t>(hwords ? hwords : 1), s));
   k_tile_words<<<blocks(nv), kT, 0, s>>>(deg, L.off, L.nbr, cycpos, cycrot, has_cycle, L.tmeta, L.tile_rec, L.ext_off,
-                                         L.ext, nv, L.trec);
+                                         L.ext, nv, kTile, L.trec);
   DL_CUDA(cudaGetLastError());
 
   // ---- host copies the host side reads (Form B schedules, halo plans, slots, tier sizes)
@@ -758,6 +763,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
 // Every HostMesh array of the device build, downloaded (tests: compared with build_host_mesh).
 std::string download_layout(cudaStream_t s, const DeviceLayout& L, HostMesh& hm) {
   const int64_t nv = hm.nv, nt = hm.nt;
+  const int64_t kTile = hm.tile;
   DL_CUDA(cudaStreamSynchronize(s));
   hm.fan16.resize(hm.nbr.size());
   if (!hm.nbr.empty()) DL_CUDA(cudaMemcpy(hm.fan16.data(), L.fan16, 2 * hm.nbr.size(), cudaMemcpyDeviceToHost));

@@ -25,7 +25,7 @@ struct DeviceLayout {
 // host mirror's nv, nt, order, rank, off, nbr, fan, tri_order, medium, hubs, large, max_deg,
 // max_ext, max_rec_words.  Returns "" or an error (arrays allocated so far stay in `L`).
 std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
-                                DeviceLayout& L);
+                                DeviceLayout& L, int32_t tile = kTile);
 // The remaining HostMesh arrays from the device (fan16, tri, vinc_off, vinc, tmeta, tile_rec,
 // ext_off, ext, trec): for tests that compare with build_host_mesh.
 std::string download_layout(cudaStream_t s, const DeviceLayout& L, HostMesh& hm);

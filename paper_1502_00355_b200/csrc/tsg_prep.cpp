@@ -104,6 +104,7 @@ struct PhaseTimer {
 // words stored entry-major: word j of the k-th row of a group of n rows at group base + j*n + k.
 std::string build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg) {
   const int64_t nv = hm.nv;
+  const int64_t kTile = hm.tile;
   const int64_t ntiles = (nv + kTile - 1) / kTile;
   hm.tmeta.assign(nv, 0);
   hm.tile_rec.assign(ntiles + 1, 0);
@@ -153,6 +154,7 @@ std::string build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t 
   hm.ext_off[ntiles] = static_cast<uint32_t>(eu);
   if (kTile + max_ext >= static_cast<int64_t>(kNoLocal))
     return "a tile references more than " + std::to_string(kNoLocal - kTile - 1) + " external vertices";
+  if (max_words > static_cast<int32_t>(kMetaBaseMask) + 1) return "tile words exceed the meta offset field";
   if (wu >= 0xffffffffULL) return "tile records exceed 2^32 words";
   hm.max_ext = max_ext;
   hm.max_rec_words = max_words;
@@ -272,7 +274,9 @@ std::string validate_desc(const tsg_mesh_desc& d) {
   return {};
 }
 
-std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm) {
+std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm, int32_t tile) {
+  if (tile < 256 || tile > kTileMax || tile % 256) return "tile size must be a multiple of 256 in [256, 1536]";
+  hm.tile = tile;
   const int64_t nv = d.nv, nt = d.nt;
   if (nv <= 0 || nt <= 0) return "mesh must have vertices and triangles";
   if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
@@ -305,7 +309,7 @@ std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh
     // rounds, overlapping the other warps' work instead of forming a tail (measured: ascending
     // with dynamic rounds 31.7 G, descending with static rounds 33.3 G node-upd/s on cfg3).
     // Results do not depend on the slot order.
-    constexpr int64_t kSigma = kTile;  // windows coincide with the tiles of tile_update
+    const int64_t kSigma = hm.tile;  // windows coincide with the tiles of tile_update
     auto degree_key = [&](int64_t v) -> int64_t {
       return d.boundary[v] ? 0 : d.nbr_off[v + 1] - d.nbr_off[v];
     };

@@ -72,6 +72,7 @@ struct HostMesh {
   std::vector<uint32_t> tmeta, tile_rec, ext_off, ext, trec;
   int32_t max_ext = 0, max_rec_words = 0;
   int32_t max_deg = 0;
+  int32_t tile = kTile;  // slots per tile (multiple of 256, <= kTileMax; chosen per mesh)
 };
 
 struct Phase {
@@ -108,7 +109,7 @@ constexpr int kChunkRecMaxDeg = 15;
 // permutation); "" when valid.  build_host_mesh runs them first.
 std::string validate_desc(const tsg_mesh_desc& d);
 // Returns "" on success, else an error message.
-std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out);
+std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out, int32_t tile = kTile);
 std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);
 void hilbert_order(int64_t nv, const double* xy, int64_t* order_out);
 std::string build_tiles(HostMesh& hm, const std::vector<uint32_t>& deg, int32_t max_deg);

@@ -60,3 +60,36 @@ def test_device_layout_in_many_sort_chunks(ts):
                        env=dict(os.environ, TSG_SEG_CHUNK="7"))
     assert r.returncode == 0, r.stderr[-3000:]
     assert r.stdout.strip().endswith("''"), r.stdout
+
+
+@pytest.mark.parametrize("tile", [768, 1024, 1280])
+def test_tile_sizes(capi, gpu_ctx, ts, golden, monkeypatch, tile):
+    """Slots per tile are chosen per mesh among the compiled sizes (tsg_engine.cu choose_tile);
+    TSG_TILE forces one.  Every size gives the same layout on both preps and the reference's
+    exact smoothing (golden d100k_formA_20, reordered and not, AoS and SoA)."""
+    from helpers import fixture, sha, smooth_kwargs_to_capi
+
+    monkeypatch.setenv("TSG_TILE", str(tile))
+    for name, (xy, tri) in list(_cases(ts))[:3]:
+        topo = ts.topology(len(xy), tri)
+        assert gpu_ctx.layout_check(xy, tri, topo, capi.hilbert_order(xy)) == "", name
+    case = golden["cases"]["d100k_formA_20"]
+    xy, tri = fixture(ts, case["kind"], case["args"])
+    kw = smooth_kwargs_to_capi(case["smooth"])
+    topo = ts.topology(len(xy), tri)
+    for order in (capi.hilbert_order(xy), None):
+        for precision_layout in ("aos", "soa"):
+            dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, layout=precision_layout, order=order)
+            cfg = capi.make_cfg(form=kw["form"], strategy=kw["strategy"], max_iters=kw["max_iters"],
+                                move_tol=kw["move_tol"], bbox_diag=ts.bbox_diagonal(xy))
+            res = dm.smooth(cfg)
+            assert [int(a) for a in res["accepted"]] == case["accepted"]
+            assert sha(dm.get_coords()) == case["xy_out"]
+            dm.free()
+
+
+def test_unsupported_tile_size_is_rejected(capi, gpu_ctx, ts, monkeypatch):
+    monkeypatch.setenv("TSG_TILE", "1000")
+    xy, tri = ts.delaunay_arrays(2000, 1)
+    with pytest.raises(RuntimeError, match="TSG_TILE"):
+        capi.DeviceMesh(gpu_ctx, xy, tri, ts.topology(len(xy), tri))

@@ -293,15 +293,20 @@ def test_continuing_runs_equal_one_long_run(capi, gpu_ctx, ts, port):
     dm.free()
 
 
-@pytest.mark.parametrize("form,chunks", [("a", 1), ("b", 1), ("b", 64)])
-def test_fp32_lockstep(capi, gpu_ctx, ts, port, form, chunks):
+@pytest.mark.parametrize("form,chunks,seed,ordered,layout", [
+    ("a", 1, 21, False, "aos"), ("b", 1, 21, False, "aos"), ("b", 64, 21, False, "aos"),
+    # Hilbert-ordered meshes run the staged tile path; the seeds give odd and even maximum
+    # external counts per tile (fp32 pairs are 8 bytes: the staged words must stay aligned).
+    ("a", 1, 21, True, "aos"), ("a", 1, 22, True, "aos"), ("a", 1, 23, True, "aos"), ("a", 1, 24, True, "soa")])
+def test_fp32_lockstep(capi, gpu_ctx, ts, port, form, chunks, seed, ordered, layout):
     """fp32: from the oracle's pass-q state, one device pass must make the same decisions except
     where the f64 margin is within EPS_F32, and land within REL_F32 of the f64 positions."""
-    xy, tri = ts.delaunay_arrays(30000, 21)
+    xy, tri = ts.delaunay_arrays(30000, seed)
     topo = ts.topology(len(xy), tri)
     diag = ts.bbox_diagonal(xy)
     state = np.array(xy, dtype=np.float32).astype(np.float64)  # f32-representable start
-    dm = capi.DeviceMesh(gpu_ctx, state, tri, topo, precision="f32")
+    dm = capi.DeviceMesh(gpu_ctx, state, tri, topo, precision="f32", layout=layout,
+                         order=capi.hilbert_order(xy) if ordered else None)
     flips = total = 0
     for q in range(5):
         dm.set_coords(state)
