@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <map>
 #include <type_traits>
 #include <memory>
@@ -440,6 +441,7 @@ struct tsg_mesh {
   int64_t n_side_cta = 0;  // persistent mode: leading rows too long for one warp (hub CTAs)
   unsigned long long* d_maxabs = nullptr;  // bits of max |coordinate|
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
+  bool host_rows_pending = false;  // hm.order / rank / nbr / fan not yet downloaded (ensure_host_rows)
   void* d_alpha = nullptr;
   double* d_xy_stage = nullptr;  // 2*nv original-order doubles
   double* d_batch_in[2] = {nullptr, nullptr};   // tsg_smooth_host_batch staging (lazy)
@@ -525,8 +527,36 @@ void free_form_b(tsg_mesh* m) {
   m->fb_nchunks = 0;
 }
 
+// The device layout leaves order / rank / rows / fan records on the device; host-side builders
+// (Form B schedules, halo plans, slot lookups, peer pushes) download them on first use.
+tsg_status ensure_host_rows(tsg_mesh* m) {
+  if (!m->host_rows_pending) return TSG_OK;
+  auto& hm = m->hm;
+  const int64_t nv = hm.nv, nrow = hm.off[nv];
+  cudaStream_t s = m->ctx->stream;
+  hm.order.resize(nv);
+  if (m->d_order) {
+    TSG_CUDA(cudaMemcpyAsync(hm.order.data(), m->d_order, 8 * nv, cudaMemcpyDeviceToHost, s));
+  } else {
+    for (int64_t v = 0; v < nv; ++v) hm.order[v] = v;
+  }
+  hm.nbr.resize(nrow);
+  hm.fan.resize(nrow);
+  if (nrow) {
+    TSG_CUDA(cudaMemcpyAsync(hm.nbr.data(), m->d_nbr, 4 * nrow, cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaMemcpyAsync(hm.fan.data(), m->d_fan, 4 * nrow, cudaMemcpyDeviceToHost, s));
+  }
+  TSG_CUDA(cudaStreamSynchronize(s));
+  hm.rank.resize(nv);
+  for (int64_t sl = 0; sl < nv; ++sl) hm.rank[hm.order[sl]] = sl;
+  m->host_rows_pending = false;
+  return TSG_OK;
+}
+
 tsg_status ensure_form_b(tsg_mesh* m, int32_t chunks) {
   if (m->fb_chunks == chunks) return TSG_OK;
+  tsg_status st0 = ensure_host_rows(m);
+  if (st0) return st0;
   free_form_b(m);
   m->gc.reset();
   tsg::FormBSchedule sch;
@@ -1196,6 +1226,20 @@ tsg_status tsg_selftest_alpha_cycle(tsg_context* ctx, int64_t n, uint64_t seed, 
 
 namespace {
 
+// TSG_PREP_TIMING=1: wall times of the upload phases on stderr (stream synchronised per mark).
+struct UploadTimer {
+  cudaStream_t s;
+  bool on = std::getenv("TSG_PREP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tsg upload] %-24s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 // Shared memory of one tile CTA: dynamic (tile_smem_bytes) + ~3 KB static + 1 KB reserved.
 size_t tile_smem_estimate(const tsg::HostMesh& hm, int rsize) {
   return 2 * static_cast<size_t>(rsize) * (hm.tile + ((std::min(hm.max_ext, kTileExtCap) + 1) & ~1)) +
@@ -1245,6 +1289,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   cudaStream_t s = ctx->stream;
   int64_t* b = &m->bytes;
   tsg_status st;
+  UploadTimer ut{s};
   TSG_CUDA(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   const int32_t tile = choose_tile(d->nv, m->num_sms, m->rsize);
   if (tile < 0) return fail(TSG_ERR_INVALID, "TSG_TILE must be one of 768, 1024, 1280");
@@ -1254,14 +1299,15 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if (!host_prep) {
     std::string err = tsg::validate_desc(*d);
     if (!err.empty()) return fail(TSG_ERR_INVALID, err);
+    ut.mark("validate");
     tsg::DeviceLayout L;
-    err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tile);
+    err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tile, false);
     // Larger tiles can overflow the 15-bit word offsets (rows of high valence) or the shared
     // memory of kTileMinBlocks CTAs: fall back to kTile, whose limits every mesh meets.
     if (tile != tsg::kTile && err.rfind("CUDA: ", 0) != 0 && (!err.empty() || !tile_fits(m->hm, m->rsize))) {
       tsg::free_layout(L);
       L = tsg::DeviceLayout{};
-      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tsg::kTile);
+      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tsg::kTile, false);
     }
     if (!err.empty()) {
       tsg::free_layout(L);
@@ -1283,7 +1329,8 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     m->d_tri = L.tri;
     m->d_order = L.order;
     m->d_tri_order = L.tri_order;
-    const int64_t nrow = static_cast<int64_t>(h.nbr.size());
+    m->host_rows_pending = true;
+    const int64_t nrow = static_cast<int64_t>(h.off[h.nv]);
     *b += 4 * (h.nv + 1) + 10 * nrow + 4 * h.nv + 8 * (ntiles + 1) + 12 * h.nt + 4 * (h.nv + 1) + 12 * h.nt +
           (L.order ? 8 * (h.nv + h.nt) : 0);
     if ((st = upload(&m->d_hubs, h.hubs, b, s))) return st;
@@ -1315,6 +1362,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
       if ((st = upload(&m->d_tri_order, h.tri_order, b, s))) return st;
     }
   }
+  ut.mark("layout");
   const auto& hm = m->hm;
   const int64_t nv = hm.nv, nt = hm.nt;
   for (void** p : {&m->buf[0], &m->buf[1], &m->init}) {
@@ -1363,12 +1411,14 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
                    hm.large.size(), side_us, tile_us, m->side_persist_auto ? "persistent" : "kernels",
                    static_cast<long long>(m->n_side_cta));
   }
+  ut.mark("buffers, side schedule");
   if ((st = ensure_stats_capacity(m.get(), 128))) return st;
   st = dispatch(m.get(), [&](auto E) { return decltype(E)::set_coords(m.get(), d->xy); });
   if (st) return st;
   st = dispatch(m.get(), [&](auto E) { return decltype(E)::prepare(m.get()); });
   if (st) return st;
   TSG_CUDA(cudaStreamSynchronize(s));
+  ut.mark("coords, prepare");
   *out = m.release();
   return TSG_OK;
 }
@@ -2083,6 +2133,7 @@ tsg_status tsg_halo_plan(tsg_mesh* m, const int64_t* send_ids, int64_t n_send, c
   if (!m || n_send < 0 || n_recv < 0 || (n_send && !send_ids) || (n_recv && !recv_ids))
     return fail(TSG_ERR_INVALID, "bad halo plan");
   TSG_CUDA(cudaSetDevice(m->ctx->device));
+  if (tsg_status st = ensure_host_rows(m)) return st;
   std::vector<int32_t> ss(n_send), rs(n_recv);
   for (int64_t i = 0; i < n_send; ++i) {
     if (send_ids[i] < 0 || send_ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "send id out of range");
@@ -2336,6 +2387,8 @@ tsg_status tsg_peer_local(tsg_mesh* m, void** buf0, void** buf1, void** sync, in
 tsg_status tsg_mesh_slots(tsg_mesh* m, const int64_t* ids, int64_t n, int64_t* slots_out) {
   TSG_LOCK_MESH(m);
   if (!m || n < 0 || (n > 0 && (!ids || !slots_out))) return fail(TSG_ERR_INVALID, "bad arguments");
+  TSG_CUDA(cudaSetDevice(m->ctx->device));
+  if (tsg_status st = ensure_host_rows(m)) return st;
   for (int64_t i = 0; i < n; ++i) {
     if (ids[i] < 0 || ids[i] >= m->hm.nv) return fail(TSG_ERR_INVALID, "vertex id out of range");
     slots_out[i] = m->hm.rank[ids[i]];
@@ -2353,6 +2406,7 @@ tsg_status tsg_peer_setup(tsg_mesh* m, int32_t rank, int32_t world, void* const*
   TSG_CUDA(cudaSetDevice(m->ctx->device));
   tsg_status st = tsg_peer_local(m, nullptr, nullptr, nullptr, nullptr);
   if (st) return st;
+  if ((st = ensure_host_rows(m))) return st;
   if (peer_sync[rank] != m->d_peer_sync || peer_buf0[rank] != m->buf[0] || peer_buf1[rank] != m->buf[1])
     return fail(TSG_ERR_INVALID, "the rank's own entry must be its tsg_peer_local pointers");
   std::vector<tsg::PeerEntry> tab(world);

@@ -402,7 +402,10 @@ __device__ __forceinline__ RingEdge<R> ring_edge(typename Arith<R>::R2 q, typena
 }
 
 // Tile arrays (tsg_prep.hpp build_tiles).
-constexpr int kTileMinBlocks = 3;  // 256-thread CTAs per SM the register budget is sized for
+#ifndef TSG_TILE_MIN_BLOCKS
+#define TSG_TILE_MIN_BLOCKS 3
+#endif
+constexpr int kTileMinBlocks = TSG_TILE_MIN_BLOCKS;  // 256-thread CTAs per SM the register budget is sized for
 
 // Peer-memory partitions (tsg_peer.cuh): one rank's view of another (mapped pointers).
 struct PeerSync;

@@ -25,6 +25,8 @@
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -492,8 +494,23 @@ cudaError_t to_host(std::vector<T>& h, const T* d, int64_t n, cudaStream_t s) {
 
 }  // namespace
 
+// TSG_PREP_TIMING=1: per-phase wall times of the device layout on stderr (stream synchronised
+// at each mark; profiling aid).
+struct DevPhaseTimer {
+  cudaStream_t s;
+  bool on = std::getenv("TSG_PREP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tsg layout] %-24s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
-                                DeviceLayout& L, int32_t tile) {
+                                DeviceLayout& L, int32_t tile, bool host_rows) {
   const int64_t nv = d.nv, nt = d.nt;
   if (tile < 256 || tile > kTileMax || tile % 256) return "tile size must be a multiple of 256 in [256, 1536]";
   const int kTile = tile;
@@ -501,6 +518,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   if (nv >= (int64_t{1} << 31) - 1) return "vertex count exceeds 2^31-1";
   if (nt >= (int64_t{1} << 32)) return "triangle count exceeds 2^32";
   Arena A{s, {}};
+  DevPhaseTimer pt{s};
   hm = HostMesh{};
   hm.nv = nv;
   hm.nt = nt;
@@ -526,6 +544,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   DL_CUDA(cudaMemcpyAsync(tri_in, d.tri, 12 * nt, cudaMemcpyHostToDevice, s));
   DL_CUDA(cudaMemcpyAsync(bnd, d.boundary, nv, cudaMemcpyHostToDevice, s));
 
+  pt.mark("inputs");
   // ---- slot order: degree-sorted windows of the locality order (stable), rank
   int64_t* order;
   DL_CUDA(A.get(&order, nv));
@@ -549,6 +568,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   k_rank<<<blocks(nv), kT, 0, s>>>(order, nv, rank);
   DL_CUDA(cudaGetLastError());
 
+  pt.mark("slot order");
   // ---- row lengths, checks, compact offsets
   uint32_t* deg;
   unsigned long long* flags;  // [0] inconsistent vertex, [1] broken rows vertex
@@ -585,6 +605,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   k_narrow<<<blocks(nv + 1), kT, 0, s>>>(off64, nv + 1, L.off);
   DL_CUDA(cudaGetLastError());
 
+  pt.mark("row lengths");
   // ---- device triangle order
   int64_t* tri_rank;
   DL_CUDA(A.get(&tri_rank, nt));
@@ -612,6 +633,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   k_tri_slots<<<blocks(nt), kT, 0, s>>>(tri_in, L.tri_order, rank, nt, L.tri);
   DL_CUDA(cudaGetLastError());
 
+  pt.mark("triangle order");
   // ---- rows: neighbour slots, fan records, fan16, link cycles
   DL_CUDA(cudaMalloc(&L.nbr, 4 * (total ? total : 1)));
   DL_CUDA(cudaMalloc(&L.fan, 4 * (total ? total : 1)));
@@ -626,6 +648,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
                                     L.fan, L.fan16, cycpos, cycrot, has_cycle, flags + 1);
   DL_CUDA(cudaGetLastError());
 
+  pt.mark("rows");
   // ---- incident CSR over slots (device triangle ids, ascending per row)
   uint64_t *icnt, *ioff64;
   DL_CUDA(A.get(&icnt, nv + 1));
@@ -653,6 +676,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
                      seg_chunk(1 << 20), false));
   }
 
+  pt.mark("incident CSR");
   // ---- tier lists (slot order), `large` by descending valence (stable)
   {
     uint8_t *fm, *fh, *fl;
@@ -693,6 +717,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
     DL_CUDA(to_host(hm.large, lrg, hn[2], s));
   }
 
+  pt.mark("tier lists");
   // ---- tiles: meta words, sorted external slots, entry-major words
   uint32_t *words, *ext_cnt, *tbound, *cand, *cand2;
   uint8_t* first;
@@ -742,13 +767,16 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
                                          L.ext, nv, kTile, L.trec);
   DL_CUDA(cudaGetLastError());
 
+  pt.mark("tiles");
   // ---- host copies the host side reads (Form B schedules, halo plans, slots, tier sizes)
-  DL_CUDA(to_host(hm.order, order, nv, s));
-  DL_CUDA(to_host(hm.rank, rank, nv, s));
   DL_CUDA(to_host(hm.off, L.off, nv + 1, s));
-  DL_CUDA(to_host(hm.nbr, L.nbr, static_cast<int64_t>(total), s));
-  DL_CUDA(to_host(hm.fan, L.fan, static_cast<int64_t>(total), s));
-  DL_CUDA(to_host(hm.tri_order, L.tri_order, nt, s));
+  if (host_rows) {
+    DL_CUDA(to_host(hm.order, order, nv, s));
+    DL_CUDA(to_host(hm.rank, rank, nv, s));
+    DL_CUDA(to_host(hm.nbr, L.nbr, static_cast<int64_t>(total), s));
+    DL_CUDA(to_host(hm.fan, L.fan, static_cast<int64_t>(total), s));
+    DL_CUDA(to_host(hm.tri_order, L.tri_order, nt, s));
+  }
   if (d.order) {
     DL_CUDA(cudaMalloc(&L.order, 8 * nv));
     DL_CUDA(cudaMemcpyAsync(L.order, order, 8 * nv, cudaMemcpyDeviceToDevice, s));
@@ -757,6 +785,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
     L.tri_order = nullptr;
   }
   DL_CUDA(cudaStreamSynchronize(s));
+  pt.mark("host copies");
   return "";
 }
 

@@ -24,8 +24,11 @@ struct DeviceLayout {
 // Builds the layout on `s` from the host description (validated by the caller).  Fills the
 // host mirror's nv, nt, order, rank, off, nbr, fan, tri_order, medium, hubs, large, max_deg,
 // max_ext, max_rec_words.  Returns "" or an error (arrays allocated so far stay in `L`).
+// host_rows: also download order / rank / nbr / fan / tri_order into hm (tests); otherwise hm
+// holds off, the tier lists and the tile sizes, and the rest stays on the device
+// (tsg_engine.cu ensure_host_rows downloads it when a host-side builder needs it).
 std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
-                                DeviceLayout& L, int32_t tile = kTile);
+                                DeviceLayout& L, int32_t tile = kTile, bool host_rows = true);
 // The remaining HostMesh arrays from the device (fan16, tri, vinc_off, vinc, tmeta, tile_rec,
 // ext_off, ext, trec): for tests that compare with build_host_mesh.
 std::string download_layout(cudaStream_t s, const DeviceLayout& L, HostMesh& hm);
