@@ -88,7 +88,14 @@ def algorithmic_bytes_per_pass(nv, nt, sum_deg, precision):
     return 2 * c * nv + 4 * (nv + 1) + 4 * sum_deg + 4 * (nv + 1) + 12 * nt + 12 * nt + nv
 
 
-def roofline_kernel(cfg):
+DRIVER_TEXT = {"graph": "conditional-WHILE CUDA graph, 1 launch per step",
+               "flow": "dataflow: one cooperative launch per step over (tile, pass) / (vertex, pass) items"}
+
+
+def roofline_kernel(cfg, schedule="graph"):
+    if cfg["form"] == "a" and schedule == "flow":
+        return ("tile_flow (the tile_update body as a dataflow over (tile, pass) items in one persistent "
+                "cooperative launch; meshes without rows of valence >= 32)")
     if cfg["form"] == "b":
         return ("Form B: formb_flow (dataflow over (vertex, pass), AUTO on deep narrow level structures) "
                 "or formb_chunk_update / node_update level kernels")
@@ -564,7 +571,12 @@ def main():
         # kernel the graph path uses on cfg3 (AUTO picks it there; serialised under ncu anyway).
         dm.side_schedule(os.environ.get("TSG_PROFILE_SIDE", "persist"))
         dm.restore_coords()
-        dm.smooth(mk("stream"))
+        if dm.smooth(mk("graph", 2))["schedule"] == "flow":  # cooperative launches: visible to ncu
+            dm.restore_coords()
+            dm.smooth(mk("graph"))
+        else:
+            dm.restore_coords()
+            dm.smooth(mk("stream"))
         torch.cuda.synchronize()
         log("[bench] profile run done")
         return
@@ -574,6 +586,7 @@ def main():
         r = dm.smooth(scfg)
     launches_per_step = r["launches"]
     iters_per_step = r["iterations"]
+    schedule = r["schedule"]
 
     sampler = ClockSampler(local_rank)
     sampler.start()
@@ -690,12 +703,12 @@ def main():
             "config": workload_config(args, cfg, nv, nt, gargs, deg.max(), b_pass),
             "impl_config": {"swap": args.swap, "locality_order": "hilbert" if cfg["reorder"] else "none",
                             "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                            "driver": "conditional-WHILE CUDA graph, 1 launch per step",
+                            "driver": DRIVER_TEXT.get(schedule, schedule),
                             "passes_run_per_step": iters_per_step},
             "ms_per_pass": pass_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": roofline_kernel(cfg),
+                         "kernel": roofline_kernel(cfg, schedule),
                          "bytes_per_launch": b_pass, "launch_ms": node_ms_per_launch,
                          "launch_ms_stream_driver": node_ms_stream,
                          "bytes_model": "algorithmic: SURVEY 8(d) B_pass = 2c*nv + 8(nv+1) + 4*sum_deg + 24*nt + nv "

@@ -103,7 +103,15 @@ typedef struct {
   double device_ms;      /* CUDA-event time of the pass loop */
   double node_kernel_ms; /* CUDA-event time summed over node-update launches (stream driver) */
   int64_t launches;      /* kernels launched by this call */
+  int32_t schedule;      /* TSG_SCHEDULE_*: how the passes ran */
+  int32_t reserved;
 } tsg_smooth_stats;
+
+/* tsg_smooth_stats.schedule */
+#define TSG_SCHEDULE_GRAPH 0   /* per-pass kernels in a conditional-WHILE CUDA graph */
+#define TSG_SCHEDULE_STREAM 1  /* per-pass plain launches (TSG_DRIVER_STREAM) */
+#define TSG_SCHEDULE_PEER 2    /* peer-memory partitioned graph */
+#define TSG_SCHEDULE_FLOW 3    /* dataflow launch: tile_flow (Form A) / formb_flow (Form B) */
 
 /* Reductions of the quality audit (folds as the reference writes them: min / max start
  * at 2.0 / -2.0, NaN never replaces, ties keep the first triangle; histogram bins of width

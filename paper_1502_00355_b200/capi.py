@@ -64,7 +64,11 @@ class QualityReport(C.Structure):
 
 class SmoothStats(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("stop", C.c_int32), ("node_updates", C.c_int64),
-                ("device_ms", C.c_double), ("node_kernel_ms", C.c_double), ("launches", C.c_int64)]
+                ("device_ms", C.c_double), ("node_kernel_ms", C.c_double), ("launches", C.c_int64),
+                ("schedule", C.c_int32), ("reserved", C.c_int32)]
+
+
+SCHEDULE = {0: "graph", 1: "stream", 2: "peer", 3: "flow"}
 
 
 _lib = None
@@ -339,6 +343,7 @@ class DeviceMesh:
         it = st.iterations
         return dict(iterations=it, stop=STOP[st.stop], accepted=acc[:it], max_disp=md[:it],
                     device_ms=st.device_ms, node_kernel_ms=st.node_kernel_ms, launches=st.launches,
+                    schedule=SCHEDULE.get(st.schedule, str(st.schedule)),
                     node_updates=st.node_updates)
 
     def smooth_host(self, xy_in, cfg: SmoothCfg, xy_out=None):

@@ -56,6 +56,14 @@ struct Coords {
       return __ldg(reinterpret_cast<const R2*>(base) + i);
     }
   }
+  // L2-coherent read (ld.global.cg) of a value another CTA of the same launch published.
+  __device__ __forceinline__ R2 load_cg(int64_t i) const {
+    if constexpr (kSoA) {
+      return Arith<R>::make(__ldcg(base + i), __ldcg(base + nv + i));
+    } else {
+      return __ldcg(reinterpret_cast<const R2*>(base) + i);
+    }
+  }
   // Read of a buffer that other CTAs of the same launch may be writing (Form B fresh reads
   // happen only across launches, so plain loads are enough; no __ldg on mutable data).
   __device__ __forceinline__ R2 load_mut(int64_t i) const {

@@ -158,6 +158,39 @@ __global__ void reset_pass_state(tsg::PassState* st, int32_t* slot_acc, unsigned
 
 __global__ void zero_u64(unsigned long long* p) { *p = 0ull; }
 
+// Stop rule over the per-pass totals of a dataflow launch of np passes (the reference's order,
+// proj/src/smoothing.cpp:132-141): the first pass with no moves, or with a maximum displacement
+// below tol_abs, ends the smooth; else MaxIters.  One warp; the pass state it writes is what
+// finalize_pass would have left (the batch API reads the final buffer parity from it).  Only
+// used where passes after the stopping one cannot change the coordinates (tol_abs == 0: the
+// stop can only be NoMoves, after which every pass is a no-op).
+__global__ void flow_stop_state(const int32_t* slot_acc, const unsigned long long* slot_md, int32_t np, double tol_abs,
+                                tsg::PassState* st) {
+  const int lane = threadIdx.x;
+  int32_t it = np, stop = tsg::kStopMaxIters;
+  for (int32_t p = 0; p < np; ++p) {
+    int32_t a = slot_acc[static_cast<int64_t>(p) * tsg::kStatSlots + lane];
+    unsigned long long b = slot_md[static_cast<int64_t>(p) * tsg::kStatSlots + lane];
+    a = __reduce_add_sync(0xffffffffu, a);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long q = __shfl_xor_sync(0xffffffffu, b, o);
+      b = q > b ? q : b;
+    }
+    if (a == 0) {
+      it = p + 1;
+      stop = tsg::kStopNoMoves;
+      break;
+    }
+    if (__longlong_as_double(static_cast<long long>(b)) < tol_abs) {
+      it = p + 1;
+      stop = tsg::kStopDisplacement;
+      break;
+    }
+  }
+  if (lane == 0) *st = tsg::PassState{it, 1, stop, 0};
+}
+
 template <typename R>
 __global__ void to_double_scatter(const R* __restrict__ in, const int64_t* __restrict__ order,
                                   int64_t n, double* __restrict__ out) {
@@ -442,6 +475,8 @@ struct tsg_mesh {
   unsigned long long* d_maxabs = nullptr;  // bits of max |coordinate|
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   bool host_rows_pending = false;  // hm.order / rank / nbr / fan not yet downloaded (ensure_host_rows)
+  uint32_t* d_tflow = nullptr;     // tile_flow: done[ntiles] + item counter
+  bool forma_flow_auto = false;    // AUTO picks tile_flow for Form A (tsg_mesh_upload)
   void* d_alpha = nullptr;
   double* d_xy_stage = nullptr;  // 2*nv original-order doubles
   double* d_batch_in[2] = {nullptr, nullptr};   // tsg_smooth_host_batch staging (lazy)
@@ -1054,6 +1089,42 @@ struct Engine {
     return TSG_OK;
   }
 
+  // One launch of the Form A (tile, pass) dataflow kernel over passes [p0, p0 + np)
+  // (tile_flow, tsg_kernels.cuh).  Cooperative launch: the kernel's progress argument needs
+  // every CTA co-resident.
+  static tsg_status tile_flow_launch(tsg_mesh* m, const tsg_smooth_cfg& c, int32_t p0, int32_t np,
+                                     int64_t* kernels) {
+    cudaStream_t s = m->ctx->stream;
+    const int64_t ntiles = (m->hm.nv + m->hm.tile - 1) / m->hm.tile;
+    if (np <= 0 || ntiles == 0) return TSG_OK;
+    if (!m->d_tflow) TSG_CUDA(cudaMalloc(&m->d_tflow, sizeof(uint32_t) * (ntiles + 1)));
+    TSG_CUDA(cudaMemsetAsync(m->d_tflow, 0, sizeof(uint32_t) * (ntiles + 1), s));
+    Args a = base_args(m, c);
+    a.swap = TSG_SWAP_PINGPONG;  // the driver normalises copy mode afterwards (bit-identical)
+    a.list = nullptr;
+    a.count = m->hm.nv;
+    tsg::TileArgs ta = tile_args(m);
+    ta.flow = tsg::TileFlow{m->d_tflow, m->d_tflow + ntiles, p0, np, ntiles};
+    const size_t smem = tsg::tile_smem_bytes<R>(ta.tile, ta.ext_cap, ta.rec_cap);
+    cudaError_t e = cudaSuccess;
+    with_tile(ta.tile, [&](auto K) {
+      auto* fn = tsg::tile_flow<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, K>;
+      int per_sm = 0;
+      if ((e = raise_smem_limit(fn, static_cast<int>(smem))) != cudaSuccess) return;
+      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
+        return;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileThreads, smem)) != cudaSuccess) return;
+      const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * std::max(m->num_sms, 1);
+      const unsigned grid = static_cast<unsigned>(std::min(cap, ntiles * np));
+      void* args[] = {&a, &ta};
+      e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(kTileThreads), args, smem, s);
+    });
+    TSG_CUDA(e);
+    ++*kernels;
+    return TSG_OK;
+  }
+
   static tsg_status peer_push(tsg_mesh* m, cudaStream_t s, int64_t* kernels) {
     if (m->n_push == 0) return TSG_OK;
     tsg::peer_push<R, kSoA><<<grid_for(m->n_push, 256), 256, 0, s>>>(
@@ -1260,6 +1331,22 @@ bool tile_fits(const tsg::HostMesh& hm, int rsize) {
 // So: 1280 once the grid runs >= 8 waves of 1280-slot tiles; below that 1024 for fp32 meshes
 // of at least one wave and 768 otherwise.  TSG_TILE forces a size (tests, measurements); upload
 // falls back to kTile when a larger tile exceeds a layout or shared-memory limit.
+// Meshes small enough that the per-pass launch's wave tail and launch cost are a large share of
+// a pass: at most kFlowWaves waves of 1280-slot tiles (measured, cfg2 1M nodes fp64: 22.7 G
+// node-upd/s per-pass graph at 768 slots, 29.2 G dataflow at 1280; cfg4 64M: 40.3 graph vs
+// 35.6 dataflow — on large meshes a tile can wait on a neighbour tile far away in the
+// item order).
+constexpr double kFlowWaves = 4.0;
+bool flow_sized(int64_t nv, int num_sms) {
+  return static_cast<double>(nv) <= kFlowWaves * std::max(1, num_sms) * tsg::kTileMinBlocks * 1280.0;
+}
+// The dataflow launch's tile: 1280 slots once the mesh fills a wave of them, else 768 (more,
+// shorter items for meshes that do not fill the GPU).
+int32_t flow_tile(int64_t nv, int num_sms) {
+  return static_cast<double>(nv) >= static_cast<double>(std::max(1, num_sms)) * tsg::kTileMinBlocks * 1280.0 ? 1280
+                                                                                                             : 768;
+}
+
 int32_t choose_tile(int64_t nv, int num_sms, int rsize) {
   if (const char* e = std::getenv("TSG_TILE")) return tile_supported(std::atoi(e)) ? std::atoi(e) : -1;
   const double slots = static_cast<double>(std::max(1, num_sms)) * tsg::kTileMinBlocks;
@@ -1291,8 +1378,17 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   tsg_status st;
   UploadTimer ut{s};
   TSG_CUDA(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  const int32_t tile = choose_tile(d->nv, m->num_sms, m->rsize);
-  if (tile < 0) return fail(TSG_ERR_INVALID, "TSG_TILE must be one of 768, 1024, 1280");
+  const int32_t tile_graph = choose_tile(d->nv, m->num_sms, m->rsize);
+  if (tile_graph < 0) return fail(TSG_ERR_INVALID, "TSG_TILE must be one of 768, 1024, 1280");
+  // Small meshes smooth Form A through the (tile, pass) dataflow launch when every movable row
+  // fits the tile kernel; that launch has no wave tail and prefers 1280-slot tiles.  The tile
+  // size is chosen before the tiers are known: a mesh that turns out to have side rows is
+  // rebuilt at the per-pass graph's size.
+  const bool tile_forced = std::getenv("TSG_TILE") != nullptr;
+  const bool flow_size = flow_sized(d->nv, m->num_sms);
+  int32_t tile = tile_graph;
+  if (!tile_forced && flow_size) tile = flow_tile(d->nv, m->num_sms);
+  auto staged = [&] { return m->hm.max_ext <= kTileExtCap && m->hm.max_rec_words <= kTileRecCap; };
   // Device layout: built on the GPU (tsg_layout_dev.cu, default) or on the host
   // (build_host_mesh, TSG_HOST_PREP=1); identical arrays either way.
   static const bool host_prep = std::getenv("TSG_HOST_PREP") != nullptr;
@@ -1301,14 +1397,18 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     if (!err.empty()) return fail(TSG_ERR_INVALID, err);
     ut.mark("validate");
     tsg::DeviceLayout L;
-    err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tile, false);
+    auto build = [&](int32_t t) {
+      tsg::free_layout(L);
+      tile = t;
+      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, t, false);
+    };
+    auto cuda_err = [&] { return err.rfind("CUDA: ", 0) == 0; };
+    build(tile);
+    if (!tile_forced && tile != tile_graph && !cuda_err() && (!err.empty() || !m->hm.large.empty() || !staged()))
+      build(tile_graph);
     // Larger tiles can overflow the 15-bit word offsets (rows of high valence) or the shared
     // memory of kTileMinBlocks CTAs: fall back to kTile, whose limits every mesh meets.
-    if (tile != tsg::kTile && err.rfind("CUDA: ", 0) != 0 && (!err.empty() || !tile_fits(m->hm, m->rsize))) {
-      tsg::free_layout(L);
-      L = tsg::DeviceLayout{};
-      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, tsg::kTile, false);
-    }
+    if (tile != tsg::kTile && !cuda_err() && (!err.empty() || !tile_fits(m->hm, m->rsize))) build(tsg::kTile);
     if (!err.empty()) {
       tsg::free_layout(L);
       return fail(err.rfind("CUDA: ", 0) == 0 ? TSG_ERR_CUDA : TSG_ERR_INVALID, err);
@@ -1338,8 +1438,10 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     if ((st = upload(&m->d_large, h.large, b, s))) return st;
   } else {
     std::string err = tsg::build_host_mesh(*d, kTiers, m->hm, tile);
+    if (!tile_forced && tile != tile_graph && (!err.empty() || !m->hm.large.empty() || !staged()))
+      err = tsg::build_host_mesh(*d, kTiers, m->hm, tile = tile_graph);
     if (tile != tsg::kTile && (!err.empty() || !tile_fits(m->hm, m->rsize)))
-      err = tsg::build_host_mesh(*d, kTiers, m->hm, tsg::kTile);
+      err = tsg::build_host_mesh(*d, kTiers, m->hm, tile = tsg::kTile);
     if (!err.empty()) return fail(TSG_ERR_INVALID, err);
     const auto& h = m->hm;
     if ((st = upload(&m->d_off, h.off, b, s))) return st;
@@ -1363,6 +1465,7 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
     }
   }
   ut.mark("layout");
+  m->forma_flow_auto = flow_size && m->hm.large.empty() && staged();
   const auto& hm = m->hm;
   const int64_t nv = hm.nv, nt = hm.nt;
   for (void** p : {&m->buf[0], &m->buf[1], &m->init}) {
@@ -1434,7 +1537,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_side_ctr, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage,
                   m->d_peer_sync, m->d_peer_tab, m->d_push_peer, m->d_push_src, m->d_push_dst,
-                  m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst};
+                  m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst, m->d_tflow};
   for (void* p : ptrs) cudaFree(p);
   for (int b = 0; b < 2; ++b) {
     cudaFree(m->d_batch_in[b]);
@@ -1732,8 +1835,29 @@ bool flow_selected(const tsg_mesh* m, const tsg_smooth_cfg* c) {
   return m->fb_mode == TSG_FORMB_AUTO && m->flow_n > 0 && m->fb_auto_flow;
 }
 
+// Form A through the (tile, pass) dataflow kernel (tile_flow): meshes whose every movable row
+// is in the tile kernel (no side rows), all staged, one GPU, the graph driver.  TSG_FORMA_FLOW
+// = 0 / 1 forces it off / on where it applies; AUTO takes it where the per-pass launch's wave
+// tail and launch cost are a large share of the pass.
+bool tile_flow_selected(const tsg_mesh* m, const tsg_smooth_cfg* c) {
+  if (c->form != TSG_FORM_A || c->driver != TSG_DRIVER_GRAPH || m->peer_world > 1) return false;
+  if (!m->hm.large.empty() || !Engine<double, false>::tiles_staged(m)) return false;
+  static const bool sweep = std::getenv("TSG_TWOPHASE_SWEEP") != nullptr;
+  if (c->strategy == TSG_STRATEGY_TWOPHASE && sweep) return false;
+  const int64_t ntiles = (m->hm.nv + m->hm.tile - 1) / m->hm.tile;
+  if (ntiles * static_cast<int64_t>(c->max_iters) >= (int64_t{1} << 31)) return false;
+  if (const char* e = std::getenv("TSG_FORMA_FLOW")) return std::atoi(e) != 0;
+  return m->forma_flow_auto;
+}
+
 tsg_status smooth_flow(tsg_mesh* m, const tsg_smooth_cfg* c, double tol_abs, int32_t* it_out, int32_t* stop_out,
                        std::vector<int32_t>& acc, std::vector<unsigned long long>& md, int64_t* kernels) {
+  const bool form_a = c->form == TSG_FORM_A;
+  auto launch = [&](int32_t p0, int32_t np) {
+    return dispatch(m, [&](auto E) {
+      return form_a ? decltype(E)::tile_flow_launch(m, *c, p0, np, kernels) : decltype(E)::flow_launch(m, p0, np, kernels);
+    });
+  };
   cudaStream_t s = m->ctx->stream;
   const int32_t P = c->max_iters;
   const int32_t round = tol_abs > 0.0 ? kFlowRound : P;
@@ -1748,9 +1872,10 @@ tsg_status smooth_flow(tsg_mesh* m, const tsg_smooth_cfg* c, double tol_abs, int
   while (p0 < P) {
     const int32_t np = std::min(round, P - p0);
     const bool may_replay = tol_abs > 0.0 && np > 1;
+    if (may_replay && !m->d_flow_save) TSG_CUDA(cudaMalloc(&m->d_flow_save, coord_bytes));
     if (may_replay)
       TSG_CUDA(cudaMemcpyAsync(m->d_flow_save, m->buf[p0 & 1], coord_bytes, cudaMemcpyDeviceToDevice, s));
-    tsg_status st = dispatch(m, [&](auto E) { return decltype(E)::flow_launch(m, p0, np, kernels); });
+    tsg_status st = launch(p0, np);
     if (st) return st;
     sa.resize(static_cast<size_t>(np) * tsg::kStatSlots);
     sm.resize(static_cast<size_t>(np) * tsg::kStatSlots);
@@ -1782,7 +1907,7 @@ tsg_status smooth_flow(tsg_mesh* m, const tsg_smooth_cfg* c, double tol_abs, int
     if (stop_at >= 0) {
       if (*stop_out == tsg::kStopDisplacement && stop_at + 1 < np) {
         TSG_CUDA(cudaMemcpyAsync(m->buf[p0 & 1], m->d_flow_save, coord_bytes, cudaMemcpyDeviceToDevice, s));
-        st = dispatch(m, [&](auto E) { return decltype(E)::flow_launch(m, p0, stop_at + 1, kernels); });
+        st = launch(p0, stop_at + 1);
         if (st) return st;
       }
       *it_out = p0 + stop_at + 1;
@@ -1816,7 +1941,7 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
   TSG_CUDA(cudaMemsetAsync(m->d_smd, 0, sizeof(unsigned long long) * tsg::kStatSlots * c->max_iters, s));
   if (diag_enabled()) TSG_CUDA(cudaMemsetAsync(m->d_rare, 0, sizeof(unsigned long long) * (m->cap + 16), s));
 
-  if (flow_selected(m, c)) {
+  if (flow_selected(m, c) || tile_flow_selected(m, c)) {
     std::vector<int32_t> acc;
     std::vector<unsigned long long> md;
     int32_t it = 0, stop = 0;
@@ -1851,6 +1976,7 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
       stats->device_ms = total_ms;
       stats->node_kernel_ms = total_ms;
       stats->launches = kernels;
+      stats->schedule = TSG_SCHEDULE_FLOW;
     }
     return TSG_OK;
   }
@@ -1957,6 +2083,7 @@ tsg_status tsg_smooth(tsg_mesh* m, const tsg_smooth_cfg* c, tsg_smooth_stats* st
     stats->node_kernel_ms = node_ms;
     stats->launches = peer ? 2 + kernels_per_pass * it
                       : c->driver == TSG_DRIVER_GRAPH ? kernels_per_pass * it : launches;
+    stats->schedule = peer ? TSG_SCHEDULE_PEER : c->driver == TSG_DRIVER_GRAPH ? TSG_SCHEDULE_GRAPH : TSG_SCHEDULE_STREAM;
   }
   return TSG_OK;
 }
@@ -1986,6 +2113,10 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
     m->h_batch_cap = n;
   }
   cudaStream_t s = ctx->stream;
+  // Form A through tile_flow when it is selected and the stop rule cannot fire after a pass
+  // that changed the coordinates (move_tol == 0); otherwise the graph.
+  const bool flow = tile_flow_selected(m, c) && c->move_tol * c->bbox_diag == 0.0;
+  if (flow && (st = ensure_stats_capacity(m, c->max_iters))) return st;
   // Item k uses staging slot k & 1.  The copy engines serve host<->device copies in issue
   // order, so the loop issues the input copy of item k+1 BEFORE the result copy of item k:
   //   copy_in : H2D(k+1)            (after item k-1 released the slot)
@@ -2008,9 +2139,22 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
     if (st) return st;
     TSG_CUDA(cudaEventRecord(ctx->ev_in_free[b], s));
     int64_t kpp = 0;
-    if ((st = smooth_enqueue_graph(m, c, &kpp))) return st;
+    int32_t swap = c->swap;
+    if (flow) {
+      // every pass in one dataflow launch, the stop rule on the device (tol_abs == 0)
+      reset_pass_state<<<grid_for(tsg::kStatSlots * c->max_iters, 256), 256, 0, s>>>(
+          m->d_state, m->d_sacc, m->d_smd, static_cast<int64_t>(tsg::kStatSlots) * c->max_iters, m->d_side_ctr);
+      TSG_LAUNCHED();
+      st = dispatch(m, [&](auto E) { return decltype(E)::tile_flow_launch(m, *c, 0, c->max_iters, &kpp); });
+      if (st) return st;
+      flow_stop_state<<<1, 32, 0, s>>>(m->d_sacc, m->d_smd, c->max_iters, 0.0, m->d_state);
+      TSG_LAUNCHED();
+      swap = TSG_SWAP_PINGPONG;  // the final coordinates are in buf[iterations & 1]
+    } else if ((st = smooth_enqueue_graph(m, c, &kpp))) {
+      return st;
+    }
     if (k >= 2) TSG_CUDA(cudaStreamWaitEvent(s, ctx->ev_out_free[b], 0));
-    st = dispatch(m, [&](auto E) { return decltype(E)::batch_store(m, c->swap, m->d_batch_out[b]); });
+    st = dispatch(m, [&](auto E) { return decltype(E)::batch_store(m, swap, m->d_batch_out[b]); });
     if (st) return st;
     save_state<<<1, 1, 0, s>>>(m->d_state, m->d_batch_state + k);
     TSG_LAUNCHED();
@@ -2026,7 +2170,7 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
     if (iterations_out) iterations_out[k] = m->h_batch_state[k].pass;
     if (stop_out) stop_out[k] = m->h_batch_state[k].stop;
   }
-  if (n > 0) m->cur = c->swap == TSG_SWAP_PINGPONG ? (m->h_batch_state[n - 1].pass & 1) : 0;
+  if (n > 0) m->cur = (flow || c->swap == TSG_SWAP_PINGPONG) ? (m->h_batch_state[n - 1].pass & 1) : 0;
   return TSG_OK;
 }
 

@@ -416,6 +416,38 @@ struct PeerEntry {
   int64_t nv;
 };
 
+// The (tile, pass) dataflow launch of tile_flow: items i = (pass p0 + i / ntiles, tile
+// i % ntiles) are taken in order from a global counter; done[t] = passes of this launch that
+// tile t has completed (st.release.gpu after its stores).
+struct TileFlow {
+  uint32_t* done;   // ntiles, zeroed before the launch
+  uint32_t* next;   // item counter, zeroed before the launch
+  int32_t p0, np;
+  int64_t ntiles;
+};
+
+__device__ __forceinline__ uint32_t tf_ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long tf_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *p >= need; a dependency that never arrives (a bug, not a schedule: every CTA is
+// co-resident and items are taken in order) traps after ~10 s instead of hanging the device.
+__device__ __forceinline__ void tf_wait(const uint32_t* p, uint32_t need) {
+  if (tf_ld_relaxed(p) >= need) return;
+  const unsigned long long t0 = tf_globaltimer();
+  for (int k = 1;; ++k) {
+    __nanosleep(64);
+    if (tf_ld_relaxed(p) >= need) return;
+    if ((k & 1023) == 0 && tf_globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+
 // Halo stores fused into the tile kernel (peer-memory driver; all null otherwise): right after
 // a tile row's new value is stored locally it is stored into every peer whose halo holds the
 // vertex, so the exchange overlaps the pass tile by tile instead of following it.
@@ -452,6 +484,7 @@ struct TileArgs {
   int32_t medium_max;        // the others at medium_max (tsg_prep.cpp)
   int32_t tile;              // slots per tile (HostMesh::tile, <= kTileMax)
   int64_t nv;
+  TileFlow flow;             // tile_flow only
 };
 
 template <typename R>
@@ -602,11 +635,16 @@ __device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& 
 // kStaged: every tile's external coordinates and words fit the shared-memory caps.
 // kSlots: slots per tile (= t.tile; a compile-time constant, measured 3% faster than a runtime
 // tile size on cfg3).
-template <typename R, bool kSoA, int kThreads, int kMaxDeg, bool kStaged, int kSlots>
-__global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
+// kFlow: one item of tile_flow (tile `tile`, pass `pass`): waits for the pass-1 results of the
+// tiles it reads, loads coordinates through L2 (ld.cg) and publishes done[tile] at the end;
+// otherwise the tile is blockIdx.x and the pass comes from the device pass state.
+template <typename R, bool kSoA, int kThreads, int kMaxDeg, bool kStaged, int kSlots, bool kFlow>
+__device__ __forceinline__ void tile_item(const PassArgs<R, kSoA>& a, const TileArgs& t, const int tile, int pass,
+                                          const int it) {
   using O = Arith<R>;
   using R2 = typename O::R2;
   constexpr bool kExact = sizeof(R) == 8;
+  static_assert(!kFlow || kStaged, "the dataflow launch stages every tile");
   static_assert(kSlots % kThreads == 0 && kSlots <= kTileMax, "whole vertices per thread");
   extern __shared__ __align__(16) unsigned char tile_smem[];
   __shared__ uint64_t bar;
@@ -618,12 +656,15 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   uint32_t* meta_s = words + t.rec_cap;
 
   const int tid = threadIdx.x;
-  const int tile = static_cast<int>(blockIdx.x);
   const int64_t base = static_cast<int64_t>(tile) * kT;
   const int n_in = static_cast<int>(t.nv - base < kT ? t.nv - base : kT);
   // The pass state (which coordinate buffer is current) is read in parallel with the tile's
   // parity-independent records; only the coordinate copies wait for it.
-  const int2 state = *reinterpret_cast<const int2*>(a.st);
+  int2 state;
+  if constexpr (kFlow)
+    state = make_int2(pass, 0);
+  else
+    state = *reinterpret_cast<const int2*>(a.st);
   const uint32_t e0 = __ldg(t.ext_off + tile), ne = __ldg(t.ext_off + tile + 1) - e0;
   const uint32_t r0 = __ldg(t.tile_rec + tile), nr = __ldg(t.tile_rec + tile + 1) - r0;
   const int n_ext = static_cast<int>(kStaged || ne < static_cast<uint32_t>(t.ext_cap) ? ne : t.ext_cap);
@@ -633,6 +674,8 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   const bool bulk = !kSoA && n_in == kT;
   if (tid == 0) {
     qn_s = 0;
+    if (kFlow && it > 0)  // the previous item's barrier completed (and was waited on) before its end
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(&bar)) : "memory");
     mbar_init(&bar, 1);
     if (bulk) {
       mbar_expect_tx(&bar, kT * sizeof(R2) + kT * 4u + 4u * n_rec);
@@ -650,12 +693,34 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   }
   Coords<R, kSoA> P, N;
   select_buffers(a, state.x, P, N);
-  const int pass = state.x;
+  pass = state.x;
+  auto load = [&](int64_t i) {
+    if constexpr (kFlow)
+      return P.load_cg(i);
+    else
+      return P.load(i);
+  };
+  const uint32_t need = static_cast<uint32_t>(pass - t.flow.p0);  // (kFlow)
+  if constexpr (kFlow) {
+    // Pass `pass` reads the pass-1 results of this tile and of the tiles owning its external
+    // slots (and overwrites the buffer their pass-1 reads used): each thread waits for the
+    // producers of what it copies, then acquires.
+    if (need > 0) {
+      tf_wait(t.flow.done + tile, need);
+#pragma unroll
+      for (int j = 0; j < kExtRegs; ++j)
+        if (tid + j * kThreads < n_ext) tf_wait(t.flow.done + eidx[j] / kSlots, need);
+      for (int k = tid + kExtRegs * kThreads; k < n_ext; k += kThreads)
+        tf_wait(t.flow.done + __ldg(t.ext + e0 + k) / kSlots, need);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk reads
+  }
   TSG_TRACE_BEGIN(pass, blockIdx.x)
   if (bulk && tid == 0) bulk_g2s(pts, P.base + 2 * base, kT * sizeof(R2), &bar);
   if (!bulk) {
     for (int i = tid; i < n_in; i += kThreads) {
-      pts[i] = P.load(base + i);
+      pts[i] = load(base + i);
       meta_s[i] = __ldg(t.meta + base + i);
     }
     const uint4* src = reinterpret_cast<const uint4*>(t.rec + r0);
@@ -667,21 +732,23 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
     const int k = tid + j * kThreads;
     if (k < n_ext) {
       if constexpr (kSoA)
-        pts[kT + k] = P.load(eidx[j]);
+        pts[kT + k] = load(eidx[j]);
       else
         cp_async<sizeof(R2)>(pts + kT + k, reinterpret_cast<const R2*>(P.base) + eidx[j]);
     }
   }
   for (int k = tid + kExtRegs * kThreads; k < n_ext; k += kThreads) {
     if constexpr (kSoA)
-      pts[kT + k] = P.load(__ldg(t.ext + e0 + k));
+      pts[kT + k] = load(__ldg(t.ext + e0 + k));
     else
       cp_async<sizeof(R2)>(pts + kT + k, reinterpret_cast<const R2*>(P.base) + __ldg(t.ext + e0 + k));
   }
   if constexpr (!kSoA) cp_async_wait_all();
   __syncthreads();  // also publishes the mbarrier initialisation
   if (bulk) mbar_wait(&bar, 0);
-  if (state.y) return;  // (after the copies into this CTA's shared memory have landed)
+  if constexpr (!kFlow) {
+    if (state.y) return;  // (after the copies into this CTA's shared memory have landed)
+  }
 
   const TileView<R, kSoA, kStaged> tv{pts, words, P, t.ext + e0, t.rec + r0, t.ext_cap, t.rec_cap, kT};
   const bool xonly = exact_only(a.maxabs);
@@ -854,6 +921,38 @@ __global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs
   if (pushed) __threadfence_system();  // peer stores before the pass barrier's release (peer_sync)
   TSG_TRACE_SYNC();
   TSG_TRACE_END(0, blockIdx.x, tid == 0)
+  if constexpr (kFlow) {
+    __syncthreads();  // every store of the item (and every shared-memory read) is done
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(t.flow.done + tile), "r"(need + 1) : "memory");
+    }
+  }
+}
+
+template <typename R, bool kSoA, int kThreads, int kMaxDeg, bool kStaged, int kSlots>
+__global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_update(PassArgs<R, kSoA> a, TileArgs t) {
+  tile_item<R, kSoA, kThreads, kMaxDeg, kStaged, kSlots, false>(a, t, static_cast<int>(blockIdx.x), 0, 0);
+}
+
+// Form A passes [p0, p0 + np) as a dataflow over (tile, pass) items in one cooperative launch:
+// a CTA takes the next item from a global counter, so pass p + 1 starts on the tiles whose
+// neighbourhood has finished pass p while the last tiles of pass p are still running — no wave
+// tail and no launch per pass.  Progress: every CTA is co-resident and items are taken in
+// (pass, tile) order, so the earliest unfinished item only depends on finished ones.  Each
+// vertex still reads pass-start values only (same arithmetic as tile_update, bit-identical).
+template <typename R, bool kSoA, int kThreads, int kMaxDeg, int kSlots>
+__global__ void __launch_bounds__(kThreads, kTileMinBlocks) tile_flow(PassArgs<R, kSoA> a, TileArgs t) {
+  __shared__ int next_s[2];
+  const int64_t total = static_cast<int64_t>(t.flow.np) * t.flow.ntiles;
+  int64_t item = blockIdx.x;
+  for (int it = 0; item < total; ++it) {
+    if (threadIdx.x == 0) next_s[it & 1] = static_cast<int>(atomicAdd(t.flow.next, 1u) + gridDim.x);
+    const int pass = t.flow.p0 + static_cast<int>(item / t.flow.ntiles);
+    const int tile = static_cast<int>(item % t.flow.ntiles);
+    tile_item<R, kSoA, kThreads, kMaxDeg, true, kSlots, true>(a, t, tile, pass, it);  // ends with a barrier
+    item = next_s[it & 1];
+  }
 }
 
 // Warp per vertex, Form A fused, for rows above the cycle tiers (valence 16 .. any): the

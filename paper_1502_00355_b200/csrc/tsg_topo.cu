@@ -39,8 +39,10 @@ unsigned grid_of(int64_t n) {
   return static_cast<unsigned>(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
 }
 
-__global__ void corner_keys(const int32_t* __restrict__ tri, int64_t nt, uint32_t* __restrict__ cv,
-                            int32_t* __restrict__ ct, unsigned long long* __restrict__ inc_cnt) {
+// (Also the range check of every corner: *bad = 1 when one lies outside [0, nv).)
+__global__ void corner_keys(const int32_t* __restrict__ tri, int64_t nt, int64_t nv, uint32_t* __restrict__ cv,
+                            int32_t* __restrict__ ct, unsigned long long* __restrict__ inc_cnt,
+                            unsigned long long* __restrict__ bad) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
 #pragma unroll
@@ -48,7 +50,10 @@ __global__ void corner_keys(const int32_t* __restrict__ tri, int64_t nt, uint32_
       const uint32_t v = static_cast<uint32_t>(tri[3 * t + k]);
       cv[3 * t + k] = v;
       ct[3 * t + k] = static_cast<int32_t>(t);
-      atomicAdd(inc_cnt + v, 1ULL);
+      if (v < static_cast<uint64_t>(nv))
+        atomicAdd(inc_cnt + v, 1ULL);
+      else
+        *bad = 1;
     }
   }
 }
@@ -236,8 +241,6 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   if (!ctx || nv <= 0 || nt < 0 || nv >= (int64_t{1} << 31) || 3 * nt >= (int64_t{1} << 31) || (nt > 0 && !tri) ||
       !nbr_off || !inc_off || !boundary || !n_nbr_out || (nt > 0 && (!inc || !nbr)))
     return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: bad arguments");
-  for (int64_t i = 0; i < 3 * nt; ++i)
-    if (tri[i] < 0 || tri[i] >= nv) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: corner index out of range");
   TSG_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   const int64_t m3 = 3 * nt;
@@ -269,8 +272,17 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   TSG_CUDA(cudaMemsetAsync(d_inc_cnt, 0, 8 * (nv + 1), s));
   TSG_CUDA(cudaMemsetAsync(d_cnt, 0, 8 * (nv + 1), s));
   if (nt) TSG_CUDA(cudaMemcpyAsync(d_tri, tri, 4 * m3, cudaMemcpyHostToDevice, s));
-  corner_keys<<<grid_of(nt), kThreads, 0, s>>>(d_tri, nt, d_cv, d_ct, d_inc_cnt);
-  TSG_LAUNCHED();
+  {
+    unsigned long long* d_bad = nullptr;
+    unsigned long long h_bad = 0;
+    TSG_CUDA(B.get(&d_bad, 1));
+    TSG_CUDA(cudaMemsetAsync(d_bad, 0, 8, s));
+    corner_keys<<<grid_of(nt), kThreads, 0, s>>>(d_tri, nt, nv, d_cv, d_ct, d_inc_cnt, d_bad);
+    TSG_LAUNCHED();
+    TSG_CUDA(cudaMemcpyAsync(&h_bad, d_bad, 8, cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    if (h_bad) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: corner index out of range");
+  }
   // incident rows: stable sort of (vertex, triangle) by vertex (pairs generated in triangle order)
   TSG_CUDA(cub_call([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, d_cv, d_cv2, d_ct, d_inc, static_cast<int>(m3), 0, vbits, s);

@@ -367,3 +367,64 @@ def test_cycle_fast_alpha_error_is_inside_the_analysed_bound(gpu_ctx):
         assert err <= 9.5 * u, err / u
         assert 2 * err + 0.3 * u <= 2.0 ** -48
         assert nonfinite <= (1 << 22) // 1000
+
+
+FLOW_A_CASES = ["grid100_formA_tol0", "d10k_formA_tol0", "d10k_formA_serial_conv", "grid17x23_formA", "d300_formA",
+                "d100k_formA_20"]
+
+
+@pytest.mark.parametrize("layout,precision", [("aos", "f64"), ("soa", "f64")])
+@pytest.mark.parametrize("name", FLOW_A_CASES)
+def test_form_a_tile_flow_matches_golden(capi, gpu_ctx, ts, golden, monkeypatch, name, layout, precision):
+    """Form A through the (tile, pass) dataflow kernel (tile_flow, TSG_FORMA_FLOW=1): the
+    reference's digests bit for bit, including the displacement stop inside a 64-pass round
+    (replayed from the round start) and the no-moves stop."""
+    monkeypatch.setenv("TSG_FORMA_FLOW", "1")
+    case = golden["cases"][name]
+    xy, tri = fixture(ts, case["kind"], case["args"])
+    kw = smooth_kwargs_to_capi(case["smooth"])
+    dm, res = run_capi(capi, gpu_ctx, ts, xy, tri, kw["form"], kw["strategy"], kw["chunks"], kw["max_iters"],
+                       kw["move_tol"], layout, reorder=True, precision=precision)
+    assert res["schedule"] == "flow"
+    assert_case(res, case)
+    assert sha(dm.tri_alpha()) == case["tri_alpha"]
+    dm.free()
+
+
+@pytest.mark.parametrize("tile", ["768", "1024", "1280"])
+def test_form_a_tile_flow_tile_sizes_and_copy_swap(capi, gpu_ctx, ts, golden, monkeypatch, tile):
+    monkeypatch.setenv("TSG_FORMA_FLOW", "1")
+    monkeypatch.setenv("TSG_TILE", tile)
+    case = golden["cases"]["d100k_formA_20"]
+    xy, tri = fixture(ts, case["kind"], case["args"])
+    for swap in ("pingpong", "copy"):
+        dm, res = run_capi(capi, gpu_ctx, ts, xy, tri, "a", max_iters=20, swap=swap, reorder=True)
+        assert_case(res, case)
+        dm.free()
+
+
+def test_form_a_tile_flow_fp32_equals_graph(capi, gpu_ctx, ts, monkeypatch):
+    """fp32: the dataflow launch and the per-pass graph give identical bits (same arithmetic,
+    pass-start values only)."""
+    xy, tri = ts.delaunay_arrays(200000, 9)
+    out = {}
+    for flow in ("0", "1"):
+        monkeypatch.setenv("TSG_FORMA_FLOW", flow)
+        dm, res = run_capi(capi, gpu_ctx, ts, xy, tri, "a", max_iters=40, move_tol=1e-7, reorder=True,
+                           precision="f32")
+        out[flow] = (res["iterations"], list(res["accepted"]), res["xy"].copy())
+        dm.free()
+    assert out["0"][0] == out["1"][0] and out["0"][1] == out["1"][1]
+    assert np.array_equal(out["0"][2].view(np.uint64), out["1"][2].view(np.uint64))
+
+
+def test_form_a_tile_flow_not_taken_with_side_rows(capi, gpu_ctx, ts, port, monkeypatch):
+    """A mesh with rows of valence >= 32 keeps the per-pass graph (side_rows) under
+    TSG_FORMA_FLOW=1, with the reference's results."""
+    monkeypatch.setenv("TSG_FORMA_FLOW", "1")
+    xy, tri = ts.graded_arrays(60000, 3, 2e-3, 2048)
+    dm, res = run_capi(capi, gpu_ctx, ts, xy, tri, "a", max_iters=8, reorder=True)
+    assert res["schedule"] == "graph"
+    want = port.smooth(xy, tri, form="a", max_iters=8, move_tol=0.0)
+    assert np.array_equal(res["xy"].view(np.uint64), want.xy.view(np.uint64))
+    dm.free()
