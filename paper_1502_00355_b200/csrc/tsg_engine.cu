@@ -138,6 +138,7 @@ __global__ void coords_to_orig_parity(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kS
 }
 
 __global__ void save_state(const tsg::PassState* st, tsg::PassState* out) { *out = *st; }
+__global__ void set_state(tsg::PassState* st, int32_t pass, int32_t stop) { *st = tsg::PassState{pass, 1, stop, 0}; }
 
 // Start of a smooth: pass state, per-pass stat slots, and the side_rows ticket pair (normally
 // left zeroed by each launch's last warp; reset here too so an aborted run cannot leak into the
@@ -2116,7 +2117,13 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
   // Form A through tile_flow when it is selected and the stop rule cannot fire after a pass
   // that changed the coordinates (move_tol == 0); otherwise the graph.
   const bool flow = tile_flow_selected(m, c) && c->move_tol * c->bbox_diag == 0.0;
-  if (flow && (st = ensure_stats_capacity(m, c->max_iters))) return st;
+  // The other dataflow cases (Form B's formb_flow; Form A with a live displacement stop) run
+  // their rounds with the stop rule on the host: item by item, copies still on their streams.
+  const bool flow_sync = !flow && (tile_flow_selected(m, c) || (c->form == TSG_FORM_B &&
+                                                                (st = ensure_form_b(m, c->chunks)) == TSG_OK &&
+                                                                flow_selected(m, c)));
+  if (st) return st;
+  if ((flow || flow_sync) && (st = ensure_stats_capacity(m, c->max_iters))) return st;
   // Item k uses staging slot k & 1.  The copy engines serve host<->device copies in issue
   // order, so the loop issues the input copy of item k+1 BEFORE the result copy of item k:
   //   copy_in : H2D(k+1)            (after item k-1 released the slot)
@@ -2150,6 +2157,17 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
       flow_stop_state<<<1, 32, 0, s>>>(m->d_sacc, m->d_smd, c->max_iters, 0.0, m->d_state);
       TSG_LAUNCHED();
       swap = TSG_SWAP_PINGPONG;  // the final coordinates are in buf[iterations & 1]
+    } else if (flow_sync) {
+      reset_pass_state<<<grid_for(tsg::kStatSlots * c->max_iters, 256), 256, 0, s>>>(
+          m->d_state, m->d_sacc, m->d_smd, static_cast<int64_t>(tsg::kStatSlots) * c->max_iters, m->d_side_ctr);
+      TSG_LAUNCHED();
+      std::vector<int32_t> acc;
+      std::vector<unsigned long long> md;
+      int32_t it = 0, stop = 0;
+      if ((st = smooth_flow(m, c, c->move_tol * c->bbox_diag, &it, &stop, acc, md, &kpp))) return st;
+      set_state<<<1, 1, 0, s>>>(m->d_state, it, stop);
+      TSG_LAUNCHED();
+      swap = TSG_SWAP_PINGPONG;
     } else if ((st = smooth_enqueue_graph(m, c, &kpp))) {
       return st;
     }
@@ -2170,7 +2188,7 @@ tsg_status tsg_smooth_host_batch(tsg_mesh* m, int32_t n, const double* const* xy
     if (iterations_out) iterations_out[k] = m->h_batch_state[k].pass;
     if (stop_out) stop_out[k] = m->h_batch_state[k].stop;
   }
-  if (n > 0) m->cur = (flow || c->swap == TSG_SWAP_PINGPONG) ? (m->h_batch_state[n - 1].pass & 1) : 0;
+  if (n > 0) m->cur = (flow || flow_sync || c->swap == TSG_SWAP_PINGPONG) ? (m->h_batch_state[n - 1].pass & 1) : 0;
   return TSG_OK;
 }
 

@@ -86,13 +86,24 @@ def test_device_mesh_class_round_trip():
     assert r["iterations"] == 10 and len(r["max_disp_per_pass"]) == 10
 
 
-def test_smooth_host_batch_equals_single_calls(capi, gpu_ctx, ts, port):
+@pytest.mark.parametrize("form,strategy,move_tol,forma_flow", [
+    ("a", "fused", 1e-6, None),      # Form A dataflow, displacement stop live: rounds on the host
+    ("a", "fused", 0.0, None),       # Form A dataflow, one launch, stop rule on the device
+    ("a", "fused", 1e-6, "0"),       # Form A per-pass graph
+    ("b", "twophase", 1e-6, None),   # serial Form B (reference defaults): formb_flow
+])
+def test_smooth_host_batch_equals_single_calls(capi, gpu_ctx, ts, port, monkeypatch, form, strategy, move_tol,
+                                               forma_flow):
     """tsg_smooth_host_batch (copies overlapped with the passes, two staging slots) gives, item by
-    item, exactly what tsg_smooth_host gives; odd and even item counts, different inputs."""
+    item, exactly what tsg_smooth_host gives; odd and even item counts, different inputs; for
+    every schedule the batch path can take."""
+    if forma_flow is not None:
+        monkeypatch.setenv("TSG_FORMA_FLOW", forma_flow)
     xy, tri = ts.delaunay_arrays(7000, 21)
     topo = ts.topology(len(xy), tri)
     dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, order=capi.hilbert_order(xy))
-    cfg = capi.make_cfg(form="a", max_iters=30, move_tol=1e-6, bbox_diag=ts.bbox_diagonal(xy))
+    cfg = capi.make_cfg(form=form, strategy=strategy, max_iters=30, move_tol=move_tol,
+                        bbox_diag=ts.bbox_diagonal(xy))
     rng = np.random.default_rng(3)
     ins = [np.ascontiguousarray(xy + rng.normal(0, 1e-4, xy.shape) * (k % 2)) for k in range(5)]
     for n in (1, 2, 5):
@@ -102,7 +113,7 @@ def test_smooth_host_batch_equals_single_calls(capi, gpu_ctx, ts, port):
             want, r = dm.smooth_host(ins[k], cfg)
             assert its[k] == r["iterations"] and stops[k] == r["stop"]
             assert np.array_equal(outs[k].view(np.uint64), want.view(np.uint64))
-    want = port.smooth(ins[0], tri, form="a", max_iters=30, move_tol=1e-6)
+    want = port.smooth(ins[0], tri, form=form, max_iters=30, move_tol=move_tol)
     outs = [np.empty_like(xy)]
     dm.smooth_host_batch(ins[:1], cfg, outs)
     assert np.array_equal(outs[0].view(np.uint64), want.xy.view(np.uint64))
