@@ -187,6 +187,7 @@ class Port:
         L.orc_smooth_prepared.argtypes = [_i64, _i64] + [_P] * 7 + [C.c_int, _i64, C.c_int, _dbl,
                                                                     _P, _P, C.c_int, _P, _P, _P]
         L.orc_pass_lockstep.argtypes = [_i64, _i64] + [_P] * 7 + [C.c_int, _i64, C.c_int, _P, _P, _P]
+        L.orc_lockstep_sample.argtypes = [_P] * 8 + [_i64, C.c_int, _P, _P, _P]
 
     def alpha(self, p1, p2, p3) -> float:
         return self.lib.orc_alpha(*p1, *p2, *p3)
@@ -253,6 +254,20 @@ class Port:
             raise MemoryError("orc_smooth_prepared")
         it = int(st[0])
         return SmoothResult(xy, acc[:it].copy(), md[:it].copy(), it, STOP_NAMES[int(st[1])])
+
+    def lockstep_sample(self, topo, tri, xy, ids, precision=0):
+        """Form A lockstep pass evaluated only at `ids` (orc_lockstep_sample): (new positions of
+        ids, decisions, f64 margins)."""
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        tri = np.ascontiguousarray(tri, dtype=np.int32)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.zeros((len(ids), 2))
+        dec = np.zeros(len(ids), dtype=np.int8)
+        margin = np.zeros(len(ids))
+        self.lib.orc_lockstep_sample(_ptr(tri), _ptr(topo["nbr_off"]), _ptr(topo["nbr"]), _ptr(topo["inc_off"]),
+                                     _ptr(topo["inc"]), _ptr(topo["boundary"]), _ptr(xy), _ptr(ids), len(ids),
+                                     precision, _ptr(out), _ptr(dec), _ptr(margin))
+        return out, dec, margin
 
     def pass_lockstep(self, topo, tri, xy, form="a", chunks=1, precision=0):
         xy = np.ascontiguousarray(xy, dtype=np.float64)

@@ -103,3 +103,17 @@ def test_lockstep_f64_equals_one_pass(port, ts):
         r = port.smooth(xy, tri, form=form, chunks=chunks, max_iters=1, move_tol=0.0)
         assert np.array_equal(out.view(np.uint64), r.xy.view(np.uint64))
         assert int((dec == 1).sum()) == int(r.accepted[0])
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_lockstep_sample_equals_full_lockstep(port, ts, precision):
+    """The sampled Form A lockstep (cfg5 parity) equals the full lockstep pass at
+    the sampled vertices."""
+    xy, tri = ts.delaunay_arrays(20000, 8)
+    topo = port.topology(len(xy), tri)
+    full, dec, margin = port.pass_lockstep(topo, tri, xy, form="a", precision=precision)
+    ids = np.sort(np.random.default_rng(1).choice(len(xy), 3000, replace=False))
+    out, sdec, smargin = port.lockstep_sample(topo, tri, xy, ids, precision=precision)
+    assert np.array_equal(sdec, dec[ids])
+    assert np.array_equal(smargin, margin[ids])
+    assert np.array_equal(out.view(np.uint64), full[ids].view(np.uint64))
