@@ -133,7 +133,9 @@ def sampled_lockstep_check(dm, xy, tri, topo, diag, precision, n_sample=1_000_00
     has = lens > 0
     lmin[has] = np.minimum.reduceat(edge, first[has])
     kappa = 16.0
-    eps_v = np.maximum(eps, kappa * 2.0**-24 * np.abs(state).max() / lmin) if precision == "f32" else np.full(len(ids), 0.0)
+    with np.errstate(divide="ignore"):  # coincident points: l_min 0, the decision is degenerate
+        eps_v = (np.maximum(eps, kappa * 2.0**-24 * np.abs(state).max() / lmin) if precision == "f32"
+                 else np.zeros(len(ids)))
     beyond = int((differ & (margin > eps_v)).sum())
     err = float(np.abs(got[ids][same] - want[same]).max() / diag) if same.any() else 0.0
     pinned = bool(np.array_equal(d < 0, wdec < 0))

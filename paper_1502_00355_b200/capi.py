@@ -251,8 +251,8 @@ class Context:
         n = C.c_int64()
         check(lib().tsg_topology(self.h, nv, nt, _ptr(tri), _ptr(nbr_off), _ptr(nbr), len(nbr), _ptr(inc_off),
                                  _ptr(inc), _ptr(bnd), C.byref(n)), "tsg_topology")
-        return dict(nbr_off=nbr_off, nbr=nbr[: n.value].copy(), inc_off=inc_off, inc=inc[: 3 * nt],
-                    boundary=bnd)
+        # (views: the untouched tail of the 6*nt buffer was never paged in)
+        return dict(nbr_off=nbr_off, nbr=nbr[: n.value], inc_off=inc_off, inc=inc[: 3 * nt], boundary=bnd)
 
     def close(self):
         if self.h:
