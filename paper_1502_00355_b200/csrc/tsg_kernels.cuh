@@ -611,6 +611,15 @@ __device__ __noinline__ bool tile_decide_rare(const TileView<R, kSoA, kStaged>& 
   return hyp_e > thr_e;
 }
 
+#ifndef TSG_SUM_UNROLL
+#define TSG_SUM_UNROLL 4
+#endif
+#ifndef TSG_CYC_UNROLL
+#define TSG_CYC_UNROLL 1
+#endif
+constexpr int kSumUnroll = TSG_SUM_UNROLL;
+constexpr int kCycUnroll = TSG_CYC_UNROLL;
+
 // Tile-staged thread-per-vertex Form A fused update (small tier, deg <= kMaxDeg).
 //
 // One CTA owns kSlots consecutive slots (a Hilbert-compact patch, degree-sorted inside).  It
@@ -766,7 +775,7 @@ __device__ __forceinline__ void tile_item(const PassArgs<R, kSoA>& a, const Tile
     R sx = R(0), sy = R(0);
     {
       uint32_t w = w0;
-#pragma unroll 2
+#pragma unroll kSumUnroll
       for (int j = 0; j < deg; ++j, w += stride) {
         const R2 c = tv.get(tv.word(w) & kLocalMask);
         sx = O::add(sx, c.x);
@@ -804,7 +813,7 @@ __device__ __forceinline__ void tile_item(const PassArgs<R, kSoA>& a, const Tile
         RingEdge<R> ea = ring_edge<R>(tv.get(l0), pv, cand);
         uint32_t w = w0 + stride;
         int j = 1;
-#pragma unroll 1
+#pragma unroll kCycUnroll
         for (; j + 2 <= deg; j += 2, w += 2 * stride) {
           const RingEdge<R> eb = edge_at(w);
           tri(ea, eb);
