@@ -98,6 +98,12 @@ __device__ __forceinline__ void select_buffers(const PassArgs<R, kSoA>& a, int p
   }
 }
 
+// A block-uniform value every thread reads from device memory (the pass state), broadcast from
+// lane 0 so that the compiler sees a warp-uniform branch: an early return it must treat as
+// divergent leaves the block barriers after it reached by divergent warps (undefined for the
+// .aligned barrier of __syncthreads; compute-sanitizer synccheck).  All lanes active.
+__device__ __forceinline__ int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 __device__ __forceinline__ bool exact_only(const unsigned long long* maxabs) {
   return *maxabs >= static_cast<unsigned long long>(__double_as_longlong(kExactOnlyAbove));
 }
@@ -1228,7 +1234,7 @@ __global__ void __launch_bounds__(256) formb_chunk_update(PassArgs<R, kSoA> a, c
   extern __shared__ __align__(16) uint32_t rbuf[];  // [2][blockDim.x][kRecWords], then the rings
   R2* ring = reinterpret_cast<R2*>(rbuf + 2 * blockDim.x * kRecWords);  // [2 * kRecMaxDeg][blockDim.x]
   const int2 state = *reinterpret_cast<const int2*>(a.st);
-  if (state.y) return;
+  if (warp_uniform(state.y)) return;
   Coords<R, kSoA> P, N;
   select_buffers(a, state.x, P, N);
   const int pass = state.x;
@@ -1543,7 +1549,7 @@ __global__ void __launch_bounds__(kHubFastBlock) hub_fast_update(PassArgs<R, kSo
   extern __shared__ __align__(16) unsigned char hub_smem[];
   __shared__ HubShared<R> hs;
   const int2 state = *reinterpret_cast<const int2*>(a.st);
-  if (state.y) return;
+  if (warp_uniform(state.y)) return;
   Coords<R, kSoA> P, N;
   select_buffers(a, state.x, P, N);
   TSG_TRACE_BEGIN(state.x, blockIdx.x)
@@ -1565,7 +1571,7 @@ __global__ void __launch_bounds__(kHubBlock) hub_update(PassArgs<R, kSoA> a, int
   __shared__ R s_thr[kHubBlock / 32], s_hyp[kHubBlock / 32];
 
   const PassState* st = a.st;
-  if (st->done) return;
+  if (warp_uniform(st->done)) return;
   const int pass = st->pass;
   Coords<R, kSoA> P, N;
   select_buffers(a, pass, P, N);
