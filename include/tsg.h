@@ -155,6 +155,15 @@ tsg_status tsg_alpha_extrema(tsg_mesh* mesh, double* min_out, double* max_out, i
 
 /* ---- the hot path ---- */
 /*
+ * Upload from points and triangles only: the adjacency, constraints and device layout are built
+ * on the device without a host round trip (tsg_topology + the device layout of
+ * tsg_mesh_upload).  The desc's nbr_off / nbr / inc_off / inc / boundary are ignored (may be
+ * NULL); xy, tri, nv, nt, layout, precision and order are read.  Same mesh as tsg_mesh_upload
+ * with tsg_topology's arrays.
+ */
+tsg_status tsg_mesh_upload_triangles(tsg_context* ctx, const tsg_mesh_desc* desc, tsg_mesh** out);
+
+/*
  * Runs passes until max_iters, accepted == 0 (NoMoves) or max_disp < move_tol*bbox_diag
  * (Displacement), in the reference's order (src/smoothing.cpp:132-141).  Coordinates stay
  * on the device.  accepted_per_pass / max_disp_per_pass receive min(capacity, iterations)

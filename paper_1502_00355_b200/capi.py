@@ -27,7 +27,7 @@ STOP = ("max_iters", "displacement", "no_moves")
 # Every symbol include/tsg.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
     "tsg_abi_version", "tsg_last_error", "tsg_device_count", "tsg_context_create",
-    "tsg_context_destroy", "tsg_context_stream", "tsg_mesh_upload", "tsg_mesh_free",
+    "tsg_context_destroy", "tsg_context_stream", "tsg_mesh_upload", "tsg_mesh_upload_triangles", "tsg_mesh_free",
     "tsg_mesh_device_bytes", "tsg_mesh_set_coords", "tsg_mesh_get_coords", "tsg_mesh_restore_coords",
     "tsg_tri_alpha",
     "tsg_vertex_minima", "tsg_alpha_extrema", "tsg_smooth", "tsg_smooth_host",
@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
             "tsg_context_destroy": (i32, [P]),
             "tsg_context_stream": (P, [P]),
             "tsg_mesh_upload": (i32, [P, C.POINTER(MeshDesc), C.POINTER(P)]),
+            "tsg_mesh_upload_triangles": (i32, [P, C.POINTER(MeshDesc), C.POINTER(P)]),
             "tsg_mesh_free": (i32, [P]),
             "tsg_mesh_device_bytes": (i64, [P]),
             "tsg_mesh_set_coords": (i32, [P, P]),
@@ -275,11 +276,20 @@ def make_cfg(form="a", strategy="fused", chunks=1, swap="pingpong", max_iters=10
 class DeviceMesh:
     """A tsg_mesh: upload from host arrays (original numbering)."""
 
-    def __init__(self, ctx: Context, xy, tri, topo: dict, layout="aos", precision="f64", order=None):
+    def __init__(self, ctx: Context, xy, tri, topo, layout="aos", precision="f64", order=None):
+        """topo: the host adjacency dict (tsg_mesh_upload), or None to build it on the device
+        inside the upload (tsg_mesh_upload_triangles: no host round trip of the adjacency)."""
         self.ctx = ctx
         self.xy = np.ascontiguousarray(xy, dtype=np.float64)
         self.tri = np.ascontiguousarray(tri, dtype=np.int32)
         self.nv, self.nt = len(self.xy), len(self.tri)
+        if topo is None:
+            order = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+            d = MeshDesc(self.nv, self.nt, _ptr(self.xy), _ptr(self.tri), None, None, None, None, None, _ptr(order),
+                         LAYOUT[layout], PRECISION[precision])
+            self.h = C.c_void_p()
+            check(lib().tsg_mesh_upload_triangles(ctx.h, C.byref(d), C.byref(self.h)), "tsg_mesh_upload_triangles")
+            return
         keep = dict(nbr_off=np.ascontiguousarray(topo["nbr_off"], dtype=np.int64),
                     nbr=np.ascontiguousarray(topo["nbr"], dtype=np.int32),
                     inc_off=np.ascontiguousarray(topo["inc_off"], dtype=np.int64),

@@ -1228,6 +1228,15 @@ tsg_status tsg_context_create(int32_t device, tsg_context** out) {
   for (int b = 0; b < 2; ++b)
     for (cudaEvent_t* e : {&ctx->ev_in_ready[b], &ctx->ev_in_free[b], &ctx->ev_out_ready[b], &ctx->ev_out_free[b]})
       TSG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  // Mesh prep allocates its temporaries from the device's default pool (cudaMallocAsync); with
+  // the default release threshold (0) every synchronisation unmaps them and the next phase maps
+  // them again — measured: cfg3 device layout 0.4..1.7 s run to run.  Keep them in the pool.
+  {
+    cudaMemPool_t pool;
+    TSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    TSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   *out = ctx.release();
   return TSG_OK;
 }
@@ -1361,8 +1370,17 @@ int32_t choose_tile(int64_t nv, int num_sms, int rsize) {
 
 tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** out) {
   TSG_LOCK_CTX(ctx);
+  return tsg_internal::mesh_upload_impl(ctx, d, nullptr, out);
+}
+
+}  // extern "C"
+
+// din: the topology already on the device (tsg_mesh_upload_triangles, tsg_topo.cu); the desc's
+// CSR arrays are then not read.
+tsg_status tsg_internal::mesh_upload_impl(tsg_context* ctx, const tsg_mesh_desc* d, const tsg::DeviceInputs* din,
+                                          tsg_mesh** out) {
   if (!ctx || !d || !out) return fail(TSG_ERR_INVALID, "null argument");
-  if (!d->xy || !d->tri || !d->nbr_off || !d->nbr || !d->inc_off || !d->inc || !d->boundary)
+  if (!d->xy || !d->tri || (!din && (!d->nbr_off || !d->nbr || !d->inc_off || !d->inc || !d->boundary)))
     return fail(TSG_ERR_INVALID, "mesh description has null arrays");
   if (d->layout != TSG_LAYOUT_AOS && d->layout != TSG_LAYOUT_SOA)
     return fail(TSG_ERR_INVALID, "layout must be aos or soa");
@@ -1393,15 +1411,16 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   // Device layout: built on the GPU (tsg_layout_dev.cu, default) or on the host
   // (build_host_mesh, TSG_HOST_PREP=1); identical arrays either way.
   static const bool host_prep = std::getenv("TSG_HOST_PREP") != nullptr;
+  if (host_prep && din) return fail(TSG_ERR_INVALID, "TSG_HOST_PREP=1 needs the host topology (tsg_mesh_upload)");
   if (!host_prep) {
-    std::string err = tsg::validate_desc(*d);
+    std::string err = tsg::validate_desc(*d, din == nullptr);
     if (!err.empty()) return fail(TSG_ERR_INVALID, err);
     ut.mark("validate");
     tsg::DeviceLayout L;
     auto build = [&](int32_t t) {
       tsg::free_layout(L);
       tile = t;
-      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, t, false);
+      err = tsg::build_device_layout(s, *d, kTiers, m->hm, L, t, false, din);
     };
     auto cuda_err = [&] { return err.rfind("CUDA: ", 0) == 0; };
     build(tile);
@@ -1523,9 +1542,17 @@ tsg_status tsg_mesh_upload(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** 
   if (st) return st;
   TSG_CUDA(cudaStreamSynchronize(s));
   ut.mark("coords, prepare");
+  {
+    // the prep temporaries kept in the default pool during the upload go back to the device
+    cudaMemPool_t pool;
+    TSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    TSG_CUDA(cudaMemPoolTrimTo(pool, 0));
+  }
   *out = m.release();
   return TSG_OK;
 }
+
+extern "C" {
 
 tsg_status tsg_mesh_free(tsg_mesh* m) {
   TSG_LOCK_MESH(m);

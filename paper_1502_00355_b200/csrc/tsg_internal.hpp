@@ -70,3 +70,12 @@ struct CtxLock {
 }  // namespace tsg_abi
 
 #define TSG_LOCK_CTX(c) tsg_abi::CtxLock tsg_ctx_lock_(c)
+
+namespace tsg {
+struct DeviceInputs;
+}
+namespace tsg_internal {
+// tsg_mesh_upload with the topology either from the desc (din == nullptr) or already on the
+// device (tsg_mesh_upload_triangles); caller holds the context lock.
+tsg_status mesh_upload_impl(tsg_context* ctx, const tsg_mesh_desc* d, const tsg::DeviceInputs* din, tsg_mesh** out);
+}  // namespace tsg_internal

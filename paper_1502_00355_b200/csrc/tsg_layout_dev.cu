@@ -510,7 +510,7 @@ struct DevPhaseTimer {
 };
 
 std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
-                                DeviceLayout& L, int32_t tile, bool host_rows) {
+                                DeviceLayout& L, int32_t tile, bool host_rows, const DeviceInputs* din) {
   const int64_t nv = d.nv, nt = d.nt;
   if (tile < 256 || tile > kTileMax || tile % 256) return "tile size must be a multiple of 256 in [256, 1536]";
   const int kTile = tile;
@@ -523,7 +523,7 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   hm.nv = nv;
   hm.nt = nt;
   hm.tile = tile;
-  const int64_t nnb = d.nbr_off[nv], ninc = d.inc_off[nv];
+  const int64_t nnb = din ? din->nnb : d.nbr_off[nv], ninc = din ? din->ninc : d.inc_off[nv];
   const int64_t ntiles = (nv + kTile - 1) / kTile;
 
   // ---- inputs on the device
@@ -537,12 +537,15 @@ std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Ti
   DL_CUDA(A.get(&tri_in, 3 * nt));
   DL_CUDA(A.get(&bnd, nv));
   DL_CUDA(A.get(&rank, nv));
-  DL_CUDA(cudaMemcpyAsync(nbr_off, d.nbr_off, 8 * (nv + 1), cudaMemcpyHostToDevice, s));
-  DL_CUDA(cudaMemcpyAsync(inc_off, d.inc_off, 8 * (nv + 1), cudaMemcpyHostToDevice, s));
-  if (nnb) DL_CUDA(cudaMemcpyAsync(nbr, d.nbr, 4 * nnb, cudaMemcpyHostToDevice, s));
-  if (ninc) DL_CUDA(cudaMemcpyAsync(inc, d.inc, 4 * ninc, cudaMemcpyHostToDevice, s));
-  DL_CUDA(cudaMemcpyAsync(tri_in, d.tri, 12 * nt, cudaMemcpyHostToDevice, s));
-  DL_CUDA(cudaMemcpyAsync(bnd, d.boundary, nv, cudaMemcpyHostToDevice, s));
+  {
+    const cudaMemcpyKind kind = din ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    DL_CUDA(cudaMemcpyAsync(nbr_off, din ? din->nbr_off : d.nbr_off, 8 * (nv + 1), kind, s));
+    DL_CUDA(cudaMemcpyAsync(inc_off, din ? din->inc_off : d.inc_off, 8 * (nv + 1), kind, s));
+    if (nnb) DL_CUDA(cudaMemcpyAsync(nbr, din ? din->nbr : d.nbr, 4 * nnb, kind, s));
+    if (ninc) DL_CUDA(cudaMemcpyAsync(inc, din ? din->inc : d.inc, 4 * ninc, kind, s));
+    DL_CUDA(cudaMemcpyAsync(tri_in, din ? din->tri : d.tri, 12 * nt, kind, s));
+    DL_CUDA(cudaMemcpyAsync(bnd, din ? din->boundary : d.boundary, nv, kind, s));
+  }
 
   pt.mark("inputs");
   // ---- slot order: degree-sorted windows of the locality order (stable), rank

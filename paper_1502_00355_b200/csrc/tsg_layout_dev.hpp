@@ -24,11 +24,24 @@ struct DeviceLayout {
 // Builds the layout on `s` from the host description (validated by the caller).  Fills the
 // host mirror's nv, nt, order, rank, off, nbr, fan, tri_order, medium, hubs, large, max_deg,
 // max_ext, max_rec_words.  Returns "" or an error (arrays allocated so far stay in `L`).
+// Topology already on the device (tsg_mesh_upload_triangles): used instead of the desc's host
+// nbr_off / nbr / inc_off / inc / boundary / tri arrays.
+struct DeviceInputs {
+  const int64_t* nbr_off = nullptr;  // nv + 1
+  const int32_t* nbr = nullptr;
+  const int64_t* inc_off = nullptr;  // nv + 1
+  const int32_t* inc = nullptr;
+  const int32_t* tri = nullptr;      // 3 nt
+  const uint8_t* boundary = nullptr;
+  int64_t nnb = 0, ninc = 0;
+};
+
 // host_rows: also download order / rank / nbr / fan / tri_order into hm (tests); otherwise hm
 // holds off, the tier lists and the tile sizes, and the rest stays on the device
 // (tsg_engine.cu ensure_host_rows downloads it when a host-side builder needs it).
 std::string build_device_layout(cudaStream_t s, const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& hm,
-                                DeviceLayout& L, int32_t tile = kTile, bool host_rows = true);
+                                DeviceLayout& L, int32_t tile = kTile, bool host_rows = true,
+                                const DeviceInputs* din = nullptr);
 // The remaining HostMesh arrays from the device (fan16, tri, vinc_off, vinc, tmeta, tile_rec,
 // ext_off, ext, trec): for tests that compare with build_host_mesh.
 std::string download_layout(cudaStream_t s, const DeviceLayout& L, HostMesh& hm);

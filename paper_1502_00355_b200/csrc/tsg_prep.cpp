@@ -218,7 +218,9 @@ void hilbert_order(int64_t nv, const double* xy, int64_t* order_out) {
 // proj/src/mesh.cpp:69-81): corner ids in range, CSR offsets starting at 0 and
 // non-decreasing, entries in range, neighbour rows strictly ascending.  Runs in parallel
 // chunks; returns the first problem found.
-std::string validate_desc(const tsg_mesh_desc& d) {
+namespace {
+
+std::string validate_topology(const tsg_mesh_desc& d) {
   const int64_t nv = d.nv, nt = d.nt;
   std::atomic<int> bad{0};  // bit 0 tri, 1 nbr, 2 inc
   parallel_ranges(nt, [&](int64_t b, int64_t e) {
@@ -257,6 +259,16 @@ std::string validate_desc(const tsg_mesh_desc& d) {
   const int f = bad.load();
   if (f & 2) return "neighbour CSR malformed (offsets decreasing, id out of range or row not strictly ascending)";
   if (f & 4) return "incident CSR malformed (offsets decreasing or triangle id out of range)";
+  return {};
+}
+
+}  // namespace
+
+std::string validate_desc(const tsg_mesh_desc& d, bool topology) {
+  const int64_t nv = d.nv;
+  if (topology) {
+    if (std::string e = validate_topology(d); !e.empty()) return e;
+  }
   if (d.order) {
     std::vector<std::atomic<uint8_t>> seen(nv);
     std::atomic<bool> ok{true};

@@ -107,7 +107,9 @@ constexpr int kChunkRecMaxDeg = 15;
 
 // Structural checks of a caller's description (corner ids, CSR offsets / entries, the order
 // permutation); "" when valid.  build_host_mesh runs them first.
-std::string validate_desc(const tsg_mesh_desc& d);
+// topology = false: the desc's CSR arrays are not used (built on the device); only the order
+// permutation is checked.
+std::string validate_desc(const tsg_mesh_desc& d, bool topology = true);
 // Returns "" on success, else an error message.
 std::string build_host_mesh(const tsg_mesh_desc& d, const Tiers& tiers, HostMesh& out, int32_t tile = kTile);
 std::string build_form_b(const HostMesh& hm, int32_t chunks, const Tiers& tiers, FormBSchedule& out);

@@ -29,6 +29,7 @@
 
 #include "tsg.h"
 #include "tsg_internal.hpp"
+#include "tsg_layout_dev.hpp"
 
 namespace {
 
@@ -234,24 +235,32 @@ int end_bit_for(int64_t nv) {
 
 }  // namespace
 
-extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, const int32_t* tri, int64_t* nbr_off,
-                                   int32_t* nbr, int64_t nbr_cap, int64_t* inc_off, int32_t* inc, uint8_t* boundary,
-                                   int64_t* n_nbr_out) {
-  TSG_LOCK_CTX(ctx);
-  if (!ctx || nv <= 0 || nt < 0 || nv >= (int64_t{1} << 31) || 3 * nt >= (int64_t{1} << 31) || (nt > 0 && !tri) ||
-      !nbr_off || !inc_off || !boundary || !n_nbr_out || (nt > 0 && (!inc || !nbr)))
-    return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: bad arguments");
-  TSG_CUDA(cudaSetDevice(ctx->device));
+namespace {
+
+// The topology on the device (buffers owned by B): triangles uploaded, unique-neighbour rows,
+// incident rows, boundary flags.  Shared by tsg_topology (downloads them) and
+// tsg_mesh_upload_triangles (hands them to the device layout without a host round trip).
+struct TopoDev {
+  const int32_t* tri = nullptr;  // 3 nt
+  const unsigned long long* off = nullptr;      // nv + 1 (int64 values)
+  const int32_t* nbr = nullptr;  // off[nv]
+  const unsigned long long* inc_off = nullptr;  // nv + 1
+  const int32_t* inc = nullptr;  // 3 nt
+  const uint8_t* bnd = nullptr;  // nv
+  int64_t n_nbr = 0;
+};
+
+tsg_status topology_device(tsg_context* ctx, int64_t nv, int64_t nt, const int32_t* tri, DevBufs& B, TopoDev& out) {
   cudaStream_t s = ctx->stream;
   const int64_t m3 = 3 * nt;
   const int vbits = end_bit_for(nv);
-  DevBufs B{s, {}};
+  DevBufs Tmp{s, {}};  // temporaries; the outputs come from the caller's B
   auto cub_call = [&](auto&& f) -> cudaError_t {
     size_t bytes = 0;
     cudaError_t e = f(nullptr, bytes);
     if (e != cudaSuccess) return e;
     char* t = nullptr;
-    if ((e = B.get(&t, static_cast<int64_t>(bytes))) != cudaSuccess) return e;
+    if ((e = Tmp.get(&t, static_cast<int64_t>(bytes))) != cudaSuccess) return e;
     return f(t, bytes);
   };
   int32_t *d_tri, *d_ct, *d_inc;
@@ -259,23 +268,23 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   unsigned long long *d_inc_cnt, *d_inc_off, *d_cnt, *d_off;
   uint8_t *d_bnd, *d_big;
   TSG_CUDA(B.get(&d_tri, m3));
-  TSG_CUDA(B.get(&d_cv, m3));
-  TSG_CUDA(B.get(&d_cv2, m3));
-  TSG_CUDA(B.get(&d_ct, m3));
+  TSG_CUDA(Tmp.get(&d_cv, m3));
+  TSG_CUDA(Tmp.get(&d_cv2, m3));
+  TSG_CUDA(Tmp.get(&d_ct, m3));
   TSG_CUDA(B.get(&d_inc, m3));
-  TSG_CUDA(B.get(&d_inc_cnt, nv + 1));
+  TSG_CUDA(Tmp.get(&d_inc_cnt, nv + 1));
   TSG_CUDA(B.get(&d_inc_off, nv + 1));
-  TSG_CUDA(B.get(&d_cnt, nv + 1));
+  TSG_CUDA(Tmp.get(&d_cnt, nv + 1));
   TSG_CUDA(B.get(&d_off, nv + 1));
   TSG_CUDA(B.get(&d_bnd, nv));
-  TSG_CUDA(B.get(&d_big, nv));
+  TSG_CUDA(Tmp.get(&d_big, nv));
   TSG_CUDA(cudaMemsetAsync(d_inc_cnt, 0, 8 * (nv + 1), s));
   TSG_CUDA(cudaMemsetAsync(d_cnt, 0, 8 * (nv + 1), s));
   if (nt) TSG_CUDA(cudaMemcpyAsync(d_tri, tri, 4 * m3, cudaMemcpyHostToDevice, s));
   {
     unsigned long long* d_bad = nullptr;
     unsigned long long h_bad = 0;
-    TSG_CUDA(B.get(&d_bad, 1));
+    TSG_CUDA(Tmp.get(&d_bad, 1));
     TSG_CUDA(cudaMemsetAsync(d_bad, 0, 8, s));
     corner_keys<<<grid_of(nt), kThreads, 0, s>>>(d_tri, nt, nv, d_cv, d_ct, d_inc_cnt, d_bad);
     TSG_LAUNCHED();
@@ -295,9 +304,9 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   TSG_LAUNCHED();
   int32_t *d_iota, *d_bigv;
   int64_t* d_nbig;
-  TSG_CUDA(B.get(&d_iota, nv));
-  TSG_CUDA(B.get(&d_bigv, nv));
-  TSG_CUDA(B.get(&d_nbig, 1));
+  TSG_CUDA(Tmp.get(&d_iota, nv));
+  TSG_CUDA(Tmp.get(&d_bigv, nv));
+  TSG_CUDA(Tmp.get(&d_nbig, 1));
   iota32<<<grid_of(nv), kThreads, 0, s>>>(nv, d_iota);
   TSG_LAUNCHED();
   TSG_CUDA(cub_call([&](void* t, size_t& b) {
@@ -309,8 +318,8 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   unsigned long long *d_coff = nullptr, *d_ccnt = nullptr;
   int32_t *d_cand = nullptr, *d_cand2 = nullptr;
   if (nbig > 0) {
-    TSG_CUDA(B.get(&d_ccnt, nbig + 1));
-    TSG_CUDA(B.get(&d_coff, nbig + 1));
+    TSG_CUDA(Tmp.get(&d_ccnt, nbig + 1));
+    TSG_CUDA(Tmp.get(&d_coff, nbig + 1));
     TSG_CUDA(cudaMemsetAsync(d_ccnt + nbig, 0, 8, s));
     big_cand_counts<<<grid_of(nbig), kThreads, 0, s>>>(d_inc_off, d_bigv, nbig, d_ccnt);
     TSG_LAUNCHED();
@@ -319,8 +328,8 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
     TSG_CUDA(cudaMemcpyAsync(&ncand, d_coff + nbig, 8, cudaMemcpyDeviceToHost, s));
     TSG_CUDA(cudaStreamSynchronize(s));
     if (ncand >= (1ULL << 31)) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: hub rows exceed 2^31 entries");
-    TSG_CUDA(B.get(&d_cand, static_cast<int64_t>(ncand)));
-    TSG_CUDA(B.get(&d_cand2, static_cast<int64_t>(ncand)));
+    TSG_CUDA(Tmp.get(&d_cand, static_cast<int64_t>(ncand)));
+    TSG_CUDA(Tmp.get(&d_cand2, static_cast<int64_t>(ncand)));
     big_candidates<<<grid_of(nbig), kThreads, 0, s>>>(d_tri, d_inc_off, d_inc, d_bigv, nbig, d_coff, d_cand);
     TSG_LAUNCHED();
     TSG_CUDA(cub_call([&](void* t, size_t& b) {
@@ -334,7 +343,6 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   unsigned long long h_total = 0;
   TSG_CUDA(cudaMemcpyAsync(&h_total, d_off + nv, 8, cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaStreamSynchronize(s));
-  if (static_cast<int64_t>(h_total) > nbr_cap) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: nbr capacity too small");
   int32_t* d_nbr;
   TSG_CUDA(B.get(&d_nbr, static_cast<int64_t>(h_total)));
   local_rows<<<grid_of(nv), kThreads, 0, s>>>(d_tri, d_inc_off, d_inc, nv, 1, d_cnt, d_bnd, d_big, d_off, d_nbr);
@@ -344,6 +352,36 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
     TSG_LAUNCHED();
   }
   static_assert(sizeof(unsigned long long) == sizeof(int64_t), "offset width");
+  out.tri = d_tri;
+  out.off = d_off;
+  out.nbr = d_nbr;
+  out.inc_off = d_inc_off;
+  out.inc = d_inc;
+  out.bnd = d_bnd;
+  out.n_nbr = static_cast<int64_t>(h_total);
+  return TSG_OK;
+}
+
+}  // namespace
+
+extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, const int32_t* tri, int64_t* nbr_off,
+                                   int32_t* nbr, int64_t nbr_cap, int64_t* inc_off, int32_t* inc, uint8_t* boundary,
+                                   int64_t* n_nbr_out) {
+  TSG_LOCK_CTX(ctx);
+  if (!ctx || nv <= 0 || nt < 0 || nv >= (int64_t{1} << 31) || 3 * nt >= (int64_t{1} << 31) || (nt > 0 && !tri) ||
+      !nbr_off || !inc_off || !boundary || !n_nbr_out || (nt > 0 && (!inc || !nbr)))
+    return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: bad arguments");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const int64_t m3 = 3 * nt;
+  DevBufs B{s, {}};
+  TopoDev T;
+  if (tsg_status st = topology_device(ctx, nv, nt, tri, B, T)) return st;
+  if (T.n_nbr > nbr_cap) return tsg_abi::fail(TSG_ERR_INVALID, "tsg_topology: nbr capacity too small");
+  const unsigned long long h_total = static_cast<unsigned long long>(T.n_nbr);
+  const unsigned long long *d_off = T.off, *d_inc_off = T.inc_off;
+  const int32_t *d_nbr = T.nbr, *d_inc = T.inc;
+  const uint8_t* d_bnd = T.bnd;
   TSG_CUDA(cudaMemcpyAsync(nbr_off, d_off, 8 * (nv + 1), cudaMemcpyDeviceToHost, s));
   TSG_CUDA(cudaMemcpyAsync(inc_off, d_inc_off, 8 * (nv + 1), cudaMemcpyDeviceToHost, s));
   if (h_total) TSG_CUDA(cudaMemcpyAsync(nbr, d_nbr, 4 * h_total, cudaMemcpyDeviceToHost, s));
@@ -352,6 +390,31 @@ extern "C" tsg_status tsg_topology(tsg_context* ctx, int64_t nv, int64_t nt, con
   TSG_CUDA(cudaStreamSynchronize(s));
   *n_nbr_out = static_cast<int64_t>(h_total);
   return TSG_OK;
+}
+
+// Upload from points and triangles only: the topology stays on the device and feeds the device
+// layout directly (no host round trip of the ~100 B/node of adjacency).  The desc's topology
+// arrays are ignored; xy, tri, counts, layout, precision and order are read.
+extern "C" tsg_status tsg_mesh_upload_triangles(tsg_context* ctx, const tsg_mesh_desc* d, tsg_mesh** out) {
+  TSG_LOCK_CTX(ctx);
+  if (!ctx || !d || !out || !d->xy || !d->tri) return tsg_abi::fail(TSG_ERR_INVALID, "null argument");
+  const int64_t nv = d->nv, nt = d->nt;
+  if (nv <= 0 || nt <= 0 || nv >= (int64_t{1} << 31) || 3 * nt >= (int64_t{1} << 31))
+    return tsg_abi::fail(TSG_ERR_INVALID, "tsg_mesh_upload_triangles: bad counts");
+  TSG_CUDA(cudaSetDevice(ctx->device));
+  DevBufs B{ctx->stream, {}};
+  TopoDev T;
+  if (tsg_status st = topology_device(ctx, nv, nt, d->tri, B, T)) return st;
+  tsg::DeviceInputs din;
+  din.nbr_off = reinterpret_cast<const int64_t*>(T.off);
+  din.nbr = T.nbr;
+  din.inc_off = reinterpret_cast<const int64_t*>(T.inc_off);
+  din.inc = T.inc;
+  din.tri = T.tri;
+  din.boundary = T.bnd;
+  din.nnb = T.n_nbr;
+  din.ninc = 3 * nt;
+  return tsg_internal::mesh_upload_impl(ctx, d, &din, out);
 }
 
 // tsg_hilbert_order on the device: same keys (bounding box and quantisation on the host, exact

@@ -93,3 +93,30 @@ def test_unsupported_tile_size_is_rejected(capi, gpu_ctx, ts, monkeypatch):
     xy, tri = ts.delaunay_arrays(2000, 1)
     with pytest.raises(RuntimeError, match="TSG_TILE"):
         capi.DeviceMesh(gpu_ctx, xy, tri, ts.topology(len(xy), tri))
+
+
+@pytest.mark.parametrize("with_order", [True, False])
+def test_upload_from_triangles_equals_upload(capi, gpu_ctx, ts, with_order):
+    """tsg_mesh_upload_triangles (adjacency built and consumed on the device) gives the same mesh
+    as tsg_mesh_upload with tsg_topology's host arrays: identical smoothing, α field and minima."""
+    for name, (xy, tri) in _cases(ts):
+        if len(xy) < 16:
+            continue
+        order = capi.hilbert_order(xy) if with_order else None
+        res = []
+        for topo in (gpu_ctx.topology(len(xy), tri), None):
+            dm = capi.DeviceMesh(gpu_ctx, xy, tri, topo, order=order)
+            r = dm.smooth(capi.make_cfg(form="a", max_iters=6, move_tol=0.0, bbox_diag=ts.bbox_diagonal(xy)))
+            res.append((list(r["accepted"]), dm.get_coords().copy(), dm.tri_alpha().copy(), dm.vertex_minima().copy()))
+            dm.free()
+        assert res[0][0] == res[1][0], name
+        for k in (1, 2, 3):
+            assert np.array_equal(res[0][k].view(np.uint64), res[1][k].view(np.uint64)), (name, k)
+
+
+def test_upload_from_triangles_rejects_bad_corners(capi, gpu_ctx, ts):
+    xy, tri = ts.delaunay_arrays(2000, 1)
+    bad = tri.copy()
+    bad[7, 1] = len(xy)
+    with pytest.raises(RuntimeError, match="corner index out of range"):
+        capi.DeviceMesh(gpu_ctx, xy, bad, None)
