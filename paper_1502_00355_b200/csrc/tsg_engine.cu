@@ -399,11 +399,7 @@ __global__ void dist_halo_unpack(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b
 // every mesh: only ever raise it (a later mesh needing less must not lower the limit an earlier
 // mesh's launches rely on).
 // Slots per tile the tile kernel is compiled for (tsg_mesh_upload picks one per mesh).
-#ifdef TSG_TILE_1536
-constexpr int kTileSizes[] = {768, 1024, 1280, 1536};
-#else
 constexpr int kTileSizes[] = {768, 1024, 1280};
-#endif
 
 bool tile_supported(int tile) {
   for (int t : kTileSizes)
@@ -417,9 +413,6 @@ void with_tile(int tile, F&& f) {
   switch (tile) {
     case 768: f(std::integral_constant<int, 768>{}); break;
     case 1024: f(std::integral_constant<int, 1024>{}); break;
-#ifdef TSG_TILE_1536
-    case 1536: f(std::integral_constant<int, 1536>{}); break;
-#endif
     default: f(std::integral_constant<int, 1280>{}); break;
   }
 }
