@@ -158,7 +158,7 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons, sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 50 ms during the timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -174,7 +174,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
@@ -183,11 +183,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        """Start of the timed region (wall clock): stop() keeps the samples taken after it."""
+        self.t_mark = time.time()
 
     def stop(self):
         if not self.proc:
             return None
+        t_end = time.time()
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -196,7 +201,13 @@ class ClockSampler:
         self.thread.join(timeout=2)
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        t0 = getattr(self, "t_mark", 0.0)
+        inside = [ln for t, ln in self.lines if t0 <= t <= t_end]
+        window = "timed region"
+        if not inside and self.lines:  # a region shorter than the 50 ms sampling period
+            inside = [min(self.lines, key=lambda x: abs(x[0] - t0))[1]]
+            window = "nearest sample (timed region shorter than the sampling period)"
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -211,7 +222,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window}
 
 
 # Passes per reference sample (the reference arm's step, the cpu_baseline leg and the parity
@@ -440,9 +451,11 @@ def run_partitioned(args, cfg, rank, world, dev_index, dist, torch):
         it, launches_per_step = step()
     sampler = ClockSampler(dev_index)
     sampler.start()
+    time.sleep(0.3)
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.mark()
     e0.record(stream)
     updates = 0
     passes_run = 0
@@ -643,6 +656,7 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark()
     e0.record(stream)
     updates = 0
     launches = 0
