@@ -933,6 +933,24 @@ struct Engine {
     return t;
   }
 
+  // Tile CTAs resident per SM (registers and the mesh's shared memory).
+  static tsg_status tile_blocks_per_sm(tsg_mesh* m, int* out) {
+    const tsg::TileArgs ta = tile_args(m);
+    const size_t smem = tsg::tile_smem_bytes<R>(ta.tile, ta.ext_cap, ta.rec_cap);
+    const bool staged = tiles_staged(m);
+    cudaError_t e = cudaSuccess;
+    with_tile(ta.tile, [&](auto K) {
+      if (staged)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            out, tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, true, K>, kTileThreads, smem);
+      else
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            out, tsg::tile_update<R, kSoA, kTileThreads, tsg::kMaxCycleDeg, false, K>, kTileThreads, smem);
+    });
+    TSG_CUDA(e);
+    return TSG_OK;
+  }
+
   // Opt-in shared memory for the hub kernels (done outside any stream capture).
   static tsg_status prepare(tsg_mesh* m) {
     TSG_CUDA(raise_smem_limit(tsg::formb_chunk_update<R, kSoA>, kChunkRecSmem));
@@ -1540,6 +1558,19 @@ tsg_status tsg_internal::mesh_upload_impl(tsg_context* ctx, const tsg_mesh_desc*
   if (st) return st;
   st = dispatch(m.get(), [&](auto E) { return decltype(E)::prepare(m.get()); });
   if (st) return st;
+  if (m->side_persist_auto) {
+    // The persistent side kernel lives in the registers and shared memory that kTileMinBlocks
+    // tile CTAs leave on an SM; a tile kernel that fits more CTAs (fp32: 58 registers, 4 CTAs)
+    // leaves no room, and the side kernel would only run where tile CTAs end (measured, cfg3
+    // fp32: 0.366 ms per pass persistent vs 0.344 ms with the per-tier grids after the tiles).
+    int per_sm = 0;
+    st = dispatch(m.get(), [&](auto E) { return decltype(E)::tile_blocks_per_sm(m.get(), &per_sm); });
+    if (st) return st;
+    if (per_sm > tsg::kTileMinBlocks) m->side_persist_auto = false;
+    if (std::getenv("TSG_DIAG"))
+      std::fprintf(stderr, "[tsg] tile CTAs per SM %d -> side rows %s\n", per_sm,
+                   m->side_persist_auto ? "persistent" : "kernels");
+  }
   TSG_CUDA(cudaStreamSynchronize(s));
   ut.mark("coords, prepare");
   {
