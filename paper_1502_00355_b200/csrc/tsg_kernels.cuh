@@ -432,9 +432,11 @@ struct TileFlow {
   int64_t ntiles;
 };
 
-__device__ __forceinline__ uint32_t tf_ld_relaxed(const uint32_t* p) {
+// Acquire load of a done counter: a value >= need synchronizes-with the producer's release, so
+// this thread's later loads of that tile's coordinates see its stores (no separate fence).
+__device__ __forceinline__ uint32_t tf_ld_acquire(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ unsigned long long tf_globaltimer() {
@@ -445,11 +447,11 @@ __device__ __forceinline__ unsigned long long tf_globaltimer() {
 // Spin until *p >= need; a dependency that never arrives (a bug, not a schedule: every CTA is
 // co-resident and items are taken in order) traps after ~10 s instead of hanging the device.
 __device__ __forceinline__ void tf_wait(const uint32_t* p, uint32_t need) {
-  if (tf_ld_relaxed(p) >= need) return;
+  if (tf_ld_acquire(p) >= need) return;
   const unsigned long long t0 = tf_globaltimer();
   for (int k = 1;; ++k) {
     __nanosleep(64);
-    if (tf_ld_relaxed(p) >= need) return;
+    if (tf_ld_acquire(p) >= need) return;
     if ((k & 1023) == 0 && tf_globaltimer() - t0 > 10000000000ull) __trap();
   }
 }
@@ -718,8 +720,8 @@ __device__ __forceinline__ void tile_item(const PassArgs<R, kSoA>& a, const Tile
   const uint32_t need = static_cast<uint32_t>(pass - t.flow.p0);  // (kFlow)
   if constexpr (kFlow) {
     // Pass `pass` reads the pass-1 results of this tile and of the tiles owning its external
-    // slots (and overwrites the buffer their pass-1 reads used): each thread waits for the
-    // producers of what it copies, then acquires.
+    // slots (and overwrites the buffer their pass-1 reads used): each thread waits, with acquire
+    // loads, for the producers of what it copies.
     if (need > 0) {
       tf_wait(t.flow.done + tile, need);
 #pragma unroll
@@ -727,7 +729,6 @@ __device__ __forceinline__ void tile_item(const PassArgs<R, kSoA>& a, const Tile
         if (tid + j * kThreads < n_ext) tf_wait(t.flow.done + eidx[j] / kSlots, need);
       for (int k = tid + kExtRegs * kThreads; k < n_ext; k += kThreads)
         tf_wait(t.flow.done + __ldg(t.ext + e0 + k) / kSlots, need);
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk reads
   }
@@ -939,7 +940,8 @@ __device__ __forceinline__ void tile_item(const PassArgs<R, kSoA>& a, const Tile
   if constexpr (kFlow) {
     __syncthreads();  // every store of the item (and every shared-memory read) is done
     if (tid == 0) {
-      __threadfence();
+      // Release by one thread after the barrier: cumulative over the CTA's stores (they happen
+      // before it through bar.sync), so no full fence is needed (measured: cfg2 +3 %, fp32 +6 %).
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(t.flow.done + tile), "r"(need + 1) : "memory");
     }
   }
