@@ -1360,11 +1360,12 @@ bool tile_fits(const tsg::HostMesh& hm, int rsize) {
 // of at least one wave and 768 otherwise.  TSG_TILE forces a size (tests, measurements); upload
 // falls back to kTile when a larger tile exceeds a layout or shared-memory limit.
 // Meshes small enough that the per-pass launch's wave tail and launch cost are a large share of
-// a pass: at most kFlowWaves waves of 1280-slot tiles (measured, cfg2 1M nodes fp64: 22.7 G
-// node-upd/s per-pass graph at 768 slots, 29.2 G dataflow at 1280; cfg4 64M: 40.3 graph vs
-// 35.6 dataflow — on large meshes a tile can wait on a neighbour tile far away in the
-// item order).
-constexpr double kFlowWaves = 4.0;
+// a pass: at most kFlowWaves waves of 1280-slot tiles.  Measured, random Delaunay fp64
+// (profiles/r02/flow_sizes.txt; per-pass graph at its own tile size vs the dataflow launch):
+// 1M 22.7 -> 30.4, 2M 26.0 -> 32.4, 4M 29.1 -> 33.9, 8M 34.6 -> 34.8 G node-upd/s; cfg4 64M
+// 40.3 -> 35.6 (a tile can wait on a neighbour tile far away in the item order, and the
+// per-pass graph's tail is already < 1 %).
+constexpr double kFlowWaves = 12.0;
 bool flow_sized(int64_t nv, int num_sms) {
   return static_cast<double>(nv) <= kFlowWaves * std::max(1, num_sms) * tsg::kTileMinBlocks * 1280.0;
 }
