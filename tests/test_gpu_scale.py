@@ -156,3 +156,18 @@ def test_cfg4_64m_grid_matches_reference(capi, gpu_ctx, ts, ref):
     del topo
     _assert_same(res, want, "cfg4")
     dm.free()
+
+
+def test_dataflow_launch_at_3m_vs_oracle(capi, gpu_ctx, ts, port):
+    """A 3M-node mesh takes the Form A dataflow launch under AUTO (at most 12 waves of
+    1280-slot tiles, no side rows): bit-identical to the oracle over 6 passes, with the
+    no-moves / max-iters bookkeeping of the device stop rule."""
+    xy, tri = ts.delaunay_arrays(3_000_000, 17)
+    dm = capi.DeviceMesh(gpu_ctx, xy, tri, None, order=capi.hilbert_order(xy))
+    res = dm.smooth(capi.make_cfg(form="a", max_iters=6, move_tol=0.0, bbox_diag=ts.bbox_diagonal(xy)))
+    assert res["schedule"] == "flow"
+    want = port.smooth(xy, tri, form="a", max_iters=6, move_tol=0.0)
+    assert [int(a) for a in res["accepted"]] == [int(a) for a in want.accepted]
+    assert np.array_equal(res["max_disp"].view(np.uint64), want.max_disp.view(np.uint64))
+    assert np.array_equal(dm.get_coords().view(np.uint64), want.xy.view(np.uint64))
+    dm.free()
