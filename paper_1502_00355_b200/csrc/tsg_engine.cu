@@ -112,12 +112,13 @@ __global__ void coords_from_orig(const double* __restrict__ xy, const int64_t* _
 }
 
 template <typename R, bool kSoA>
-__global__ void coords_to_orig(tsg::Coords<R, kSoA> b, const int64_t* __restrict__ order,
+__global__ void coords_to_orig(tsg::Coords<R, kSoA> b, const int32_t* __restrict__ rank,
                                int64_t nv, double* __restrict__ xy) {
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t v = order ? order[s] : s;
-    const auto p = b.load_mut(s);
+  // Gather by original id (coalesced writes, random 16-byte reads): measured cheaper than the
+  // scatter by slot (random partial-sector writes read the sectors back: cfg3 339 vs 564 us).
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const auto p = b.load_mut(rank ? rank[v] : v);
     reinterpret_cast<double2*>(xy)[v] = make_double2(static_cast<double>(p.x), static_cast<double>(p.y));
   }
 }
@@ -126,15 +127,21 @@ __global__ void coords_to_orig(tsg::Coords<R, kSoA> b, const int64_t* __restrict
 // from the pass counter (ping-pong: the last pass wrote buffer (pass & 1) ? buf1 : buf0).
 template <typename R, bool kSoA>
 __global__ void coords_to_orig_parity(tsg::Coords<R, kSoA> b0, tsg::Coords<R, kSoA> b1, int32_t swap,
-                                      const tsg::PassState* st, const int64_t* __restrict__ order, int64_t nv,
+                                      const tsg::PassState* st, const int32_t* __restrict__ rank, int64_t nv,
                                       double* __restrict__ xy) {
   const tsg::Coords<R, kSoA> b = (swap == tsg::kSwapPingPong && (st->pass & 1)) ? b1 : b0;
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t v = order ? order[s] : s;
-    const auto p = b.load_mut(s);
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const auto p = b.load_mut(rank ? rank[v] : v);
     reinterpret_cast<double2*>(xy)[v] = make_double2(static_cast<double>(p.x), static_cast<double>(p.y));
   }
+}
+
+// rank[order[s]] = s: the slot of each original vertex (for the gathers above).
+__global__ void rank_of_order(const int64_t* __restrict__ order, int64_t nv, int32_t* __restrict__ rank) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < nv;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    rank[order[s]] = static_cast<int32_t>(s);
 }
 
 __global__ void save_state(const tsg::PassState* st, tsg::PassState* out) { *out = *st; }
@@ -476,6 +483,7 @@ struct tsg_mesh {
   unsigned long long* d_maxabs = nullptr;  // bits of max |coordinate|
   int64_t *d_order = nullptr, *d_tri_order = nullptr;
   bool host_rows_pending = false;  // hm.order / rank / nbr / fan not yet downloaded (ensure_host_rows)
+  int32_t* d_rank = nullptr;       // original id -> slot (ensure_rank; null without a locality order)
   uint32_t* d_tflow = nullptr;     // tile_flow: done[ntiles] + item counter
   bool forma_flow_auto = false;    // AUTO picks tile_flow for Form A (tsg_mesh_upload)
   void* d_alpha = nullptr;
@@ -661,6 +669,16 @@ tsg::Coords<R, kSoA> coords_of(const tsg_mesh* m, int i) {
 bool diag_enabled() {
   static const bool on = std::getenv("TSG_DIAG") != nullptr;
   return on;
+}
+
+// The device inverse of the slot order (write-back gathers), built on first use.
+tsg_status ensure_rank(tsg_mesh* m) {
+  if (!m->d_order || m->d_rank) return TSG_OK;
+  const int64_t nv = m->hm.nv;
+  TSG_CUDA(cudaMalloc(&m->d_rank, sizeof(int32_t) * nv));
+  rank_of_order<<<grid_for(nv, 256), 256, 0, m->ctx->stream>>>(m->d_order, nv, m->d_rank);
+  TSG_LAUNCHED();
+  return TSG_OK;
 }
 
 // Everything templated on the coordinate type and layout.
@@ -1032,7 +1050,8 @@ struct Engine {
   static tsg_status get_coords(tsg_mesh* m, double* xy_host) {
     cudaStream_t s = m->ctx->stream;
     const int64_t nv = m->hm.nv;
-    coords_to_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, m->cur), m->d_order,
+    if (tsg_status st = ensure_rank(m)) return st;
+    coords_to_orig<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, m->cur), m->d_rank,
                                                               nv, m->d_xy_stage);
     TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpyAsync(xy_host, m->d_xy_stage, 2 * nv * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1055,8 +1074,9 @@ struct Engine {
   static tsg_status batch_store(tsg_mesh* m, int32_t swap, double* stage) {
     cudaStream_t s = m->ctx->stream;
     const int64_t nv = m->hm.nv;
+    if (tsg_status st = ensure_rank(m)) return st;
     coords_to_orig_parity<R, kSoA><<<grid_for(nv, 256), 256, 0, s>>>(coords_of<R, kSoA>(m, 0), coords_of<R, kSoA>(m, 1),
-                                                                     swap, m->d_state, m->d_order, nv, stage);
+                                                                     swap, m->d_state, m->d_rank, nv, stage);
     TSG_LAUNCHED();
     return TSG_OK;
   }
@@ -1597,7 +1617,7 @@ tsg_status tsg_mesh_free(tsg_mesh* m) {
                   m->d_vmin, m->d_decision, m->d_decision_orig, m->d_state, m->d_acc, m->d_md, m->d_sacc, m->d_smd,
                   m->d_ext, m->d_side_ctr, m->d_rare, m->d_send_slots, m->d_recv_slots, m->d_halo_stage,
                   m->d_peer_sync, m->d_peer_tab, m->d_push_peer, m->d_push_src, m->d_push_dst,
-                  m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst, m->d_tflow};
+                  m->d_fpush_mask, m->d_fpush_off, m->d_fpush_peer, m->d_fpush_dst, m->d_tflow, m->d_rank};
   for (void* p : ptrs) cudaFree(p);
   for (int b = 0; b < 2; ++b) {
     cudaFree(m->d_batch_in[b]);
