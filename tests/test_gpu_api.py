@@ -87,7 +87,8 @@ def test_device_mesh_class_round_trip():
 
 
 @pytest.mark.parametrize("form,strategy,move_tol,forma_flow", [
-    ("a", "fused", 1e-6, None),      # Form A dataflow, displacement stop live: rounds on the host
+    ("a", "fused", 1e-6, "1"),       # Form A dataflow forced, displacement stop live: rounds on the host
+    ("a", "fused", 1e-6, None),      # AUTO: the per-pass graph (displacement stop live)
     ("a", "fused", 0.0, None),       # Form A dataflow, one launch, stop rule on the device
     ("a", "fused", 1e-6, "0"),       # Form A per-pass graph
     ("b", "twophase", 1e-6, None),   # serial Form B (reference defaults): formb_flow
